@@ -1,0 +1,231 @@
+/*
+ * flexicache_b200.h — C ABI of the B200-native FlexiCache per-decode-step KV
+ * hot path (sm_100a).  Drop-in for the reference's Python hot-path calls
+ * (tierkv, /root/reference/pkg/src/tierkv); each entry point names the
+ * reference function(s) it replaces.
+ *
+ * Conventions
+ *  - The library never allocates device memory.  Every buffer is owned by the
+ *    caller (PyTorch on the host side) and passed as a raw device pointer in
+ *    an fc_store descriptor or as an argument with explicit sizes.
+ *  - Every call is asynchronous on the given cudaStream_t (passed as void*)
+ *    and returns an int status: FC_OK or a negative FC_E* code for
+ *    synchronous argument errors.  Device-side invariant violations (read of
+ *    the null block, pool exhaustion, capacity overflow) set sticky bits in
+ *    store->error_word, which the host wrapper inspects and maps to the
+ *    reference's exception types (errors.py:26,30).
+ *  - Stateless and reentrant: safe on distinct streams with distinct buffers.
+ *  - Layouts are documented in DESIGN.md §3.  Elements are bf16 (FC_BF16) or
+ *    fp32 (FC_F32).  Page size is 16 tokens; head_dim is 64 or 128.
+ */
+#ifndef FLEXICACHE_B200_H
+#define FLEXICACHE_B200_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define FC_OK               0
+#define FC_E_INVALID      (-1)  /* bad argument: maps to ValueError            */
+#define FC_E_UNSUPPORTED  (-2)  /* geometry not compiled (d, ps, G): ValueError */
+#define FC_E_CUDA         (-3)  /* CUDA launch/runtime error                     */
+#define FC_E_CAPACITY     (-4)  /* workspace / capacity too small                */
+
+/* element types */
+#define FC_BF16 0
+#define FC_F32  1
+
+/* sticky device error bits in *error_word */
+#define FC_ERR_POOL_EXHAUSTED   1u  /* PoolExhausted      (blocktable.py:52-54)      */
+#define FC_ERR_NULL_READ        2u  /* ConsistencyError   (blocktable.py:192-198,
+                                                           attention.py:101-105)     */
+#define FC_ERR_NULL_WRITE       4u  /* append into a page with no block              */
+#define FC_ERR_PAGES_CAP        8u  /* logical page beyond pages_cap                 */
+#define FC_ERR_SEL_CAP         16u  /* selection longer than sel_cap                 */
+#define FC_ERR_DOUBLE_EVICT    32u  /* ConsistencyError   (blocktable.py:319-322)    */
+
+#define FC_NULL_BLOCK 0             /* blocktable.py:25 */
+
+/*
+ * Device KV store: the batched, GPU-resident form of the reference's
+ * per-(request, layer, head) state — PhysicalPool + BlockTable
+ * (blocktable.py:28-440), MinMaxCache (scoring.py:114-139) and the per-head
+ * TopKSet (scoring.py:142-161).
+ */
+typedef struct fc_store {
+    int32_t batch_cap;   /* B_cap request rows                                   */
+    int32_t layers;      /* L                                                    */
+    int32_t kv_heads;    /* H_kv per layer                                       */
+    int32_t group;       /* G = H_q / H_kv (1..8)                                */
+    int32_t head_dim;    /* d: 64 or 128                                         */
+    int32_t page_size;   /* ps: 16                                               */
+    int32_t pages_cap;   /* N_cap logical pages per (row, layer, head)           */
+    int32_t sel_cap;     /* entries per selection row                            */
+    int32_t dtype;       /* FC_BF16 or FC_F32                                    */
+    int32_t n_blocks;    /* physical blocks incl. the null block 0               */
+    void    *kv_pool;    /* [n_blocks][2][ps][d] elements (K rows then V rows)   */
+    void    *summaries;  /* [B_cap][L][H][N_cap][2][d] elements (min, max rows)  */
+    int32_t *table;      /* [B_cap][L][H][N_cap] physical block, 0 = not resident*/
+    int32_t *seq_len;    /* [B_cap] tokens stored in every layer                 */
+    int32_t *sel;        /* [B_cap][L][H][sel_cap] ascending logical pages       */
+    int32_t *n_sel;      /* [B_cap][L][H]; 0 = no selection yet (attend all)     */
+    int32_t *free_stack; /* [n_blocks] LIFO free list, top at free_top-1         */
+    int32_t *free_top;   /* [1]                                                  */
+    int32_t *step;       /* [1] decode step t of the upcoming step (1-based)     */
+    uint32_t *error_word;/* [1] sticky FC_ERR_* bits                             */
+} fc_store;
+
+/* library identity */
+const char *fc_version(void);
+/* last CUDA error string seen by this thread (for FC_E_CUDA) */
+const char *fc_last_error(void);
+
+/* ---- (4) allocation and step bookkeeping ------------------------------- */
+
+/* Allocate logical pages [first_page, first_page+n_pages) for every
+ * (layer, head) of request row `row`, popping the device free list in
+ * (layer, head, page) order — the order of the reference prefill, which
+ * calls BlockTable.allocate_pages per head (simulator.py:361-364,
+ * blocktable.py:236-246, PhysicalPool.allocate_many :59-71). */
+int fc_alloc_pages(const fc_store *s, int row, int first_page, int n_pages,
+                   void *stream);
+
+/* End of a decode step for rows [0, batch): seq_len += 1; rows whose new
+ * length starts a page get that page for every (layer, head), popped in
+ * (row, layer, head) order — BlockTable.allocate_page_all_heads
+ * (blocktable.py:248-263) as driven by simulator._append_token
+ * (simulator.py:455-466).  Advances *step. */
+int fc_step_advance(const fc_store *s, int batch, void *stream);
+
+/* ---- (1) KV append + per-page min/max summaries ------------------------ */
+
+/* Prefill: write tokens [0, n_tokens) of request `row`, layer `layer` for
+ * all H heads from k/v [H][n_tokens][d] (store dtype) into their pages and
+ * build the page summaries — build_minmax (scoring.py:72-90). */
+int fc_kv_prefill(const fc_store *s, int row, int layer, const void *k,
+                  const void *v, int n_tokens, void *stream);
+
+/* Decode append for rows [0, batch) of layer `layer`: write k_new/v_new
+ * [batch][H][d] at position seq_len[row] and fold the key into that page's
+ * summary — update_minmax (scoring.py:59-69).  Does not advance seq_len. */
+int fc_kv_append(const fc_store *s, int layer, const void *k_new,
+                 const void *v_new, int batch, void *stream);
+
+/* Read back logical K/V of one (row, layer, head): pages [0, n_pages) into
+ * k_out/v_out [n_pages*ps][d] (store dtype), undoing the in-page swizzle.
+ * Non-resident pages are written as zeros. Test/offload helper. */
+int fc_kv_gather(const fc_store *s, int row, int layer, int head, int n_pages,
+                 void *k_out, void *v_out, void *stream);
+
+/* ---- (2) page scoring + top-K selection -------------------------------- */
+
+/* For every due (row, head) of `layer` among rows [0, batch): score its
+ * pages with the GQA group bound (Quest; score_pages scoring.py:102-111,
+ * summed over the G query heads) and select the top `topk` pages with the
+ * last page pinned (select_topk scoring.py:164-193) into sel/n_sel.
+ * Due = unstable[layer*H+h] || force_due || (*step % period == 0)
+ * (rerank_due scoring.py:196-202).  `extra_tokens` (0 or 1) is added to
+ * seq_len to count the token being appended this step.
+ * q: [batch][H*G][d] (store dtype).  scores_out: [B_cap*H][pages_cap] fp32
+ * workspace that receives the scores (pinned page = -inf).  counters:
+ * [B_cap*H] int32, zero-initialised once by the caller. */
+size_t fc_score_select_workspace_size(const fc_store *s);
+int fc_score_select(const fc_store *s, int layer, const void *q,
+                    const uint8_t *unstable, int period, int force_due,
+                    int topk, int extra_tokens, float *scores_out,
+                    int32_t *counters, int batch, void *stream);
+
+/* Score only (no selection): scores_out[(row*H+h)*pages_cap + p] for pages
+ * [0, n_pages) of every (row, head) of `layer` — score_pages. Used by the
+ * per-head API and the parity tests. */
+int fc_score_pages(const fc_store *s, int layer, const void *q,
+                   int extra_tokens, float *scores_out, int batch,
+                   void *stream);
+
+/* Select only: top-K over caller-provided scores [n_heads][stride] fp32
+ * with n_valid[i] candidates, pinning page n_valid[i]-1 when pin_last != 0.
+ * Output sel_out [n_heads][topk] ascending, n_out [n_heads].
+ * select_topk (scoring.py:164-193) bit-for-bit on the given scores. */
+int fc_select_topk(const float *scores, int stride, const int32_t *n_valid,
+                   int n_heads, int topk, int pin_last, int32_t *sel_out,
+                   int32_t *n_out, void *stream);
+
+/* ---- (3) paged sparse decode attention ---------------------------------- */
+
+/* For every (row, head) of `layer` among rows [0, batch): attend its query
+ * group q[row][h*G .. h*G+G) to the tokens of the pages
+ *   sel[0..n_sel) ∪ (max(sel), n_pages)           (n_sel == 0: all pages)
+ * — sparse_decode / dense_decode (attention.py:76-111) with the stable-head
+ * rule "selection at the last rerank plus pages appended since"
+ * (simulator.py:416-420,512).  attend_appended = 0 attends exactly
+ * sel[0..n_sel) (the per-call reference sparse_decode contract).  softmax scale = scale (1/sqrt(d) in the
+ * reference, attention.py:69).  out: [batch][H*G][d] store dtype;
+ * lse: optional [batch][H*G] fp32 natural-log sum-exp.  Split-K over pages
+ * (`pages_per_split`), combine fused in the last CTA of each head.
+ * `max_pages` bounds the attended pages of any head (grid size). */
+size_t fc_sparse_decode_workspace_size(const fc_store *s, int batch,
+                                       int max_pages, int pages_per_split);
+int fc_sparse_decode(const fc_store *s, int layer, const void *q, void *out,
+                     float *lse, float scale, int extra_tokens,
+                     int attend_appended, int max_pages,
+                     int pages_per_split, void *workspace, size_t ws_bytes,
+                     int batch, void *stream);
+
+/* ---- (4) stable-head rerank: recycle + tier copies ---------------------- */
+
+/* For every stable (row, head) of `layer` due this step: diff the resident
+ * set — old_sel[row][h][0..n_old) plus the pages appended since, i.e. every
+ * page above max(old_sel) — against the new selection (store sel/n_sel),
+ * pair evicted and promoted pages in ascending logical order and move their
+ * blocks, release surplus / allocate deficit blocks, and emit the copy list
+ * (row, head, logical page, dest block) — BlockTable.recycle
+ * (blocktable.py:296-357), promoted_delta (tiering.py:42-46).
+ * old_sel: [B_cap][H][sel_cap] int32, n_old: [B_cap][H] int32 (the
+ * selection at the previous rerank; snapshot it before fc_score_select).
+ * old_has_tail = 0 takes old_sel as the complete resident set (the per-call
+ * reference recycle contract).  extra_tokens as in fc_score_select.
+ * slow_resident: optional [B_cap][L][H][pages_cap] uint8, 1 = page has a
+ * slow-tier copy (checked for every promoted page, blocktable.py:323-327).
+ * copies: [max_copies][4] int32, n_copies: [1] int32 (appended atomically).
+ * workspace: fc_rerank_workspace_size() bytes.  Unstable heads are skipped
+ * (they never reload: tiering.py:164-166).  Within one call, surplus blocks
+ * of all heads are pushed (head order, ascending pages) before deficits are
+ * popped (head order, ascending pages); for a single head this is exactly
+ * the reference order, across heads it matches up to block relabelling
+ * (canonical_form, blocktable.py:414-428). */
+size_t fc_rerank_workspace_size(const fc_store *s);
+int fc_rerank_recycle(const fc_store *s, int layer, const int32_t *old_sel,
+                      const int32_t *n_old, const uint8_t *unstable,
+                      int period, int force_due, int old_has_tail,
+                      int extra_tokens, const uint8_t *slow_resident,
+                      int32_t *copies, int max_copies, int32_t *n_copies,
+                      void *workspace, int batch, void *stream);
+
+/* Copy promoted pages from the pinned host slow tier into their HBM blocks:
+ * copies [n][4] = (row, head, logical page, dest block) for layer `layer`;
+ * host_pages is host-pinned memory [B_cap][L][H][N_cap][2][ps][d] (same
+ * in-page layout as the pool), read with a zero-copy UVA gather kernel. */
+int fc_fetch_pages(const fc_store *s, int layer, const void *host_pages,
+                   const int32_t *copies, const int32_t *n_copies,
+                   int max_copies, void *stream);
+
+/* Offload full pages of stable heads to the pinned host slow tier:
+ * pages [n][4] = (row, layer, head, logical page), one write per page
+ * (TierStore._record write-once ledger, tiering.py:99-157). */
+int fc_offload_pages(const fc_store *s, void *host_pages, const int32_t *pages,
+                     int n_pages, void *stream);
+
+/* Evict (set to the null block and release) logical pages listed in
+ * pages [n][4] = (row, layer, head, logical page) — evict_many
+ * (blocktable.py:280-294). */
+int fc_evict_pages(const fc_store *s, const int32_t *pages, int n_pages,
+                   void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLEXICACHE_B200_H */

@@ -1,0 +1,38 @@
+"""B200-native FlexiCache per-decode-step KV hot path (sm_100a).
+
+Drop-in for the hot-path API of the reference package ``tierkv``
+(/root/reference/pkg/src/tierkv/__init__.py:22-54): head stability mask,
+page table, score / select / attend / rerank calls.  All numerics run in the
+hand-written CUDA library ``libflexicache_b200.so`` behind the C ABI in
+include/flexicache_b200.h; PyTorch provides device memory and streams.
+"""
+
+from .config import Config, HeadId, all_heads, pages_for_tokens
+from .errors import (AdmissionError, ConfigError, ConsistencyError, PoolExhausted,
+                     TierKVError)
+
+__version__ = "0.1.0"
+
+_LAZY = {
+    "KVStore": ".store", "DecodeEngine": ".engine", "HeadProfile": ".stability",
+    "MinMaxMeta": ".scoring", "MinMaxCache": ".scoring", "TopKSet": ".scoring",
+    "build_minmax": ".scoring", "update_minmax": ".scoring", "score_pages": ".scoring",
+    "score_page": ".scoring", "select_topk": ".scoring", "rerank_due": ".scoring",
+    "layer_scoring_skippable": ".scoring", "AttentionState": ".attention",
+    "dense_decode": ".attention", "sparse_decode": ".attention",
+    "sparsity_error": ".attention", "BlockTable": ".blocktable",
+    "PhysicalPool": ".blocktable", "RecyclePlan": ".blocktable", "NULL_BLOCK": ".blocktable",
+    "promoted_delta": ".tiering", "TierStore": ".tiering",
+}
+
+
+def __getattr__(name):
+    if name in _LAZY:
+        import importlib
+        mod = importlib.import_module(_LAZY[name], __name__)
+        return getattr(mod, name)
+    raise AttributeError(name)
+
+
+__all__ = sorted(["Config", "HeadId", "all_heads", "pages_for_tokens", "AdmissionError",
+                  "ConfigError", "ConsistencyError", "PoolExhausted", "TierKVError", *_LAZY])

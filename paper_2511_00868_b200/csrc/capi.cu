@@ -1,0 +1,240 @@
+// capi.cu — the extern "C" boundary (include/flexicache_b200.h).  Validates
+// arguments synchronously (negative status codes, mapped to the reference's
+// ValueError by the Python host layer) and launches the kernels.
+#include "store.cuh"
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "launchers.cuh"
+
+using namespace fc;
+
+static thread_local char g_last_error[256] = "";
+
+static int cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return FC_OK;
+    std::snprintf(g_last_error, sizeof(g_last_error), "%s", cudaGetErrorString(e));
+    return FC_E_CUDA;
+}
+
+static int invalid(const char *msg) {
+    std::snprintf(g_last_error, sizeof(g_last_error), "%s", msg);
+    return FC_E_INVALID;
+}
+
+static int check_store(const fc_store *s) {
+    if (!s) return invalid("null store");
+    if (s->page_size != kPageSize) {
+        std::snprintf(g_last_error, sizeof(g_last_error), "page_size %d not compiled (16 only)", s->page_size);
+        return FC_E_UNSUPPORTED;
+    }
+    if (s->head_dim != 64 && s->head_dim != 128) {
+        std::snprintf(g_last_error, sizeof(g_last_error), "head_dim %d not compiled (64, 128)", s->head_dim);
+        return FC_E_UNSUPPORTED;
+    }
+    if (s->dtype != FC_BF16 && s->dtype != FC_F32) return invalid("dtype must be FC_BF16 or FC_F32");
+    const int gmax = s->dtype == FC_BF16 ? 16 : 8;
+    if (s->group < 1 || s->group > gmax) {
+        std::snprintf(g_last_error, sizeof(g_last_error), "group %d outside 1..%d", s->group, gmax);
+        return FC_E_UNSUPPORTED;
+    }
+    if (s->batch_cap < 1 || s->layers < 1 || s->kv_heads < 1 || s->pages_cap < 1 || s->sel_cap < 1 ||
+        s->n_blocks < 2)
+        return invalid("store geometry must be positive (n_blocks >= 2)");
+    if (!s->kv_pool || !s->summaries || !s->table || !s->seq_len || !s->sel || !s->n_sel ||
+        !s->free_stack || !s->free_top || !s->step || !s->error_word)
+        return invalid("store has a null buffer");
+    return FC_OK;
+}
+
+#define FC_CHECK(x)                 \
+    do {                            \
+        const int _r = (x);         \
+        if (_r != FC_OK) return _r; \
+    } while (0)
+
+extern "C" {
+
+const char *fc_version(void) { return "flexicache-b200 0.1 sm_100a"; }
+const char *fc_last_error(void) { return g_last_error; }
+
+int fc_alloc_pages(const fc_store *s, int row, int first_page, int n_pages, void *stream) {
+    FC_CHECK(check_store(s));
+    if (row < 0 || row >= s->batch_cap) return invalid("row out of range");
+    if (first_page < 0 || n_pages < 0 || first_page + n_pages > s->pages_cap)
+        return invalid("pages beyond pages_cap");
+    if (n_pages == 0) return FC_OK;
+    return cuda_status(launch_alloc_pages(make_view(s), row, first_page, n_pages, (cudaStream_t)stream));
+}
+
+int fc_step_advance(const fc_store *s, int batch, void *stream) {
+    FC_CHECK(check_store(s));
+    if (batch < 0 || batch > s->batch_cap || batch > 1024) return invalid("batch out of range");
+    return cuda_status(launch_step_advance(make_view(s), batch, (cudaStream_t)stream));
+}
+
+int fc_kv_prefill(const fc_store *s, int row, int layer, const void *k, const void *v, int n_tokens,
+                  void *stream) {
+    FC_CHECK(check_store(s));
+    if (row < 0 || row >= s->batch_cap || layer < 0 || layer >= s->layers) return invalid("row/layer out of range");
+    if (!k || !v) return invalid("null k/v");
+    if (n_tokens < 0 || n_tokens > s->pages_cap * s->page_size) return invalid("n_tokens beyond capacity");
+    if (n_tokens == 0) return FC_OK;
+    return cuda_status(launch_prefill(make_view(s), s->dtype, row, layer, k, v, n_tokens, (cudaStream_t)stream));
+}
+
+int fc_kv_append(const fc_store *s, int layer, const void *k_new, const void *v_new, int batch, void *stream) {
+    FC_CHECK(check_store(s));
+    if (layer < 0 || layer >= s->layers) return invalid("layer out of range");
+    if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
+    if (!k_new || !v_new) return invalid("null k/v");
+    if (batch == 0) return FC_OK;
+    return cuda_status(launch_append(make_view(s), s->dtype, layer, k_new, v_new, batch, (cudaStream_t)stream));
+}
+
+int fc_kv_gather(const fc_store *s, int row, int layer, int head, int n_pages, void *k_out, void *v_out,
+                 void *stream) {
+    FC_CHECK(check_store(s));
+    if (row < 0 || row >= s->batch_cap || layer < 0 || layer >= s->layers || head < 0 || head >= s->kv_heads)
+        return invalid("row/layer/head out of range");
+    if (n_pages < 0 || n_pages > s->pages_cap) return invalid("n_pages out of range");
+    if (!k_out || !v_out) return invalid("null output");
+    if (n_pages == 0) return FC_OK;
+    return cuda_status(launch_gather(make_view(s), s->dtype, row, layer, head, n_pages, k_out, v_out,
+                                     (cudaStream_t)stream));
+}
+
+size_t fc_score_select_workspace_size(const fc_store *s) {
+    if (check_store(s) != FC_OK) return 0;
+    const size_t heads = (size_t)s->batch_cap * s->kv_heads;
+    return heads * s->pages_cap * sizeof(float) + heads * sizeof(int32_t);
+}
+
+int fc_score_select(const fc_store *s, int layer, const void *q, const uint8_t *unstable, int period,
+                    int force_due, int topk, int extra_tokens, float *scores_out, int32_t *counters,
+                    int batch, void *stream) {
+    FC_CHECK(check_store(s));
+    if (layer < 0 || layer >= s->layers) return invalid("layer out of range");
+    if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
+    if (period < 1) return invalid("period must be >= 1");  // rerank_due, scoring.py:198-199
+    if (topk < 1) return invalid("k must be >= 1");          // select_topk, scoring.py:174-175
+    if (topk > s->sel_cap) return FC_E_CAPACITY;
+    if (extra_tokens < 0 || extra_tokens > 1) return invalid("extra_tokens must be 0 or 1");
+    if (!q || !unstable || !scores_out || !counters) return invalid("null buffer");
+    if ((size_t)s->pages_cap * 4 > 200 * 1024) return FC_E_CAPACITY;
+    if (batch == 0) return FC_OK;
+    return cuda_status(launch_score(make_view(s), s->dtype, layer, q, unstable, period, force_due, topk,
+                                    extra_tokens, scores_out, counters, 1, batch, (cudaStream_t)stream));
+}
+
+int fc_score_pages(const fc_store *s, int layer, const void *q, int extra_tokens, float *scores_out, int batch,
+                   void *stream) {
+    FC_CHECK(check_store(s));
+    if (layer < 0 || layer >= s->layers) return invalid("layer out of range");
+    if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
+    if (extra_tokens < 0 || extra_tokens > 1) return invalid("extra_tokens must be 0 or 1");
+    if (!q || !scores_out) return invalid("null buffer");
+    if (batch == 0) return FC_OK;
+    static uint8_t *dummy = nullptr;  // never dereferenced when do_select == 0
+    return cuda_status(launch_score(make_view(s), s->dtype, layer, q, dummy, 1, 0, 1, extra_tokens, scores_out,
+                                    nullptr, 0, batch, (cudaStream_t)stream));
+}
+
+int fc_select_topk(const float *scores, int stride, const int32_t *n_valid, int n_heads, int topk, int pin_last,
+                   int32_t *sel_out, int32_t *n_out, void *stream) {
+    if (topk < 1) return invalid("k must be >= 1");
+    if (stride < 1 || n_heads < 0) return invalid("bad stride / n_heads");
+    if ((size_t)stride * 4 > 200 * 1024) return FC_E_CAPACITY;
+    if (!scores || !n_valid || !sel_out || !n_out) return invalid("null buffer");
+    if (n_heads == 0) return FC_OK;
+    return cuda_status(launch_select(scores, stride, n_valid, n_heads, topk, pin_last, sel_out, n_out,
+                                     (cudaStream_t)stream));
+}
+
+size_t fc_sparse_decode_workspace_size(const fc_store *s, int batch, int max_pages, int pages_per_split) {
+    if (check_store(s) != FC_OK || pages_per_split < 1) return 0;
+    const int max_splits = (max_pages + pages_per_split - 1) / pages_per_split;
+    return attn_workspace_bytes(make_view(s), batch, max_splits < 1 ? 1 : max_splits);
+}
+
+int fc_sparse_decode(const fc_store *s, int layer, const void *q, void *out, float *lse, float scale,
+                     int extra_tokens, int attend_appended, int max_pages, int pages_per_split, void *workspace, size_t ws_bytes,
+                     int batch, void *stream) {
+    FC_CHECK(check_store(s));
+    if (layer < 0 || layer >= s->layers) return invalid("layer out of range");
+    if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
+    if (!q || !out || !workspace) return invalid("null buffer");
+    if (pages_per_split < 1 || pages_per_split > 256) return invalid("pages_per_split must be in 1..256");
+    if (max_pages < 1) return invalid("max_pages must be >= 1");
+    if (!(scale > 0.f) || !std::isfinite(scale)) return invalid("scale must be positive");
+    if (extra_tokens < 0 || extra_tokens > 1) return invalid("extra_tokens must be 0 or 1");
+    const int max_splits = (max_pages + pages_per_split - 1) / pages_per_split;
+    const StoreView v = make_view(s);
+    const size_t need = attn_workspace_bytes(v, batch, max_splits);
+    if (ws_bytes < need) return FC_E_CAPACITY;
+    if (batch == 0) return FC_OK;
+    const size_t heads = (size_t)s->batch_cap * s->kv_heads;
+    AttnArgs a;
+    a.layer = layer; a.q = q; a.out = out; a.lse = lse;
+    a.scale_log2 = scale * 1.4426950408889634f;
+    a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.pps = pages_per_split; a.max_splits = max_splits;
+    char *w = (char *)workspace;
+    a.counters = (int32_t *)w;
+    a.part_ml = (float *)(w + heads * sizeof(int32_t));
+    a.part_o = a.part_ml + heads * max_splits * s->group * 2;
+    return cuda_status(launch_attn(v, s->dtype, a, batch, (cudaStream_t)stream));
+}
+
+size_t fc_rerank_workspace_size(const fc_store *s) {
+    if (check_store(s) != FC_OK) return 0;
+    return rerank_workspace_bytes(make_view(s));
+}
+
+int fc_rerank_recycle(const fc_store *s, int layer, const int32_t *old_sel, const int32_t *n_old,
+                      const uint8_t *unstable, int period, int force_due, int old_has_tail,
+                      int extra_tokens, const uint8_t *slow_resident, int32_t *copies, int max_copies, int32_t *n_copies,
+                      void *workspace, int batch, void *stream) {
+    FC_CHECK(check_store(s));
+    if (layer < 0 || layer >= s->layers) return invalid("layer out of range");
+    if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
+    if (period < 1) return invalid("period must be >= 1");
+    if (!old_sel || !n_old || !unstable || !copies || !n_copies || !workspace) return invalid("null buffer");
+    if (max_copies < 0) return invalid("max_copies must be >= 0");
+    if (s->sel_cap > 1024) return FC_E_CAPACITY;
+    if (batch == 0) return FC_OK;
+    return cuda_status(launch_rerank(make_view(s), layer, old_sel, n_old, unstable, period, force_due,
+                                     old_has_tail, extra_tokens, slow_resident, copies, max_copies, n_copies, workspace, batch,
+                                     (cudaStream_t)stream));
+}
+
+int fc_fetch_pages(const fc_store *s, int layer, const void *host_pages, const int32_t *copies,
+                   const int32_t *n_copies, int max_copies, void *stream) {
+    FC_CHECK(check_store(s));
+    if (layer < 0 || layer >= s->layers) return invalid("layer out of range");
+    if (!host_pages || !copies || !n_copies) return invalid("null buffer");
+    if (max_copies <= 0) return FC_OK;
+    const int pb = 2 * s->page_size * s->head_dim * (s->dtype == FC_BF16 ? 2 : 4);
+    return cuda_status(launch_fetch(make_view(s), layer, host_pages, copies, n_copies, max_copies, pb,
+                                    (cudaStream_t)stream));
+}
+
+int fc_offload_pages(const fc_store *s, void *host_pages, const int32_t *pages, int n_pages, void *stream) {
+    FC_CHECK(check_store(s));
+    if (!host_pages || !pages) return invalid("null buffer");
+    if (n_pages < 0) return invalid("n_pages must be >= 0");
+    if (n_pages == 0) return FC_OK;
+    const int pb = 2 * s->page_size * s->head_dim * (s->dtype == FC_BF16 ? 2 : 4);
+    return cuda_status(launch_offload(make_view(s), host_pages, pages, n_pages, pb, (cudaStream_t)stream));
+}
+
+int fc_evict_pages(const fc_store *s, const int32_t *pages, int n_pages, void *stream) {
+    FC_CHECK(check_store(s));
+    if (!pages) return invalid("null buffer");
+    if (n_pages < 0) return invalid("n_pages must be >= 0");
+    if (n_pages == 0) return FC_OK;
+    return cuda_status(launch_evict_pages(make_view(s), pages, n_pages, (cudaStream_t)stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,40 @@
+// launchers.cuh — host-side launcher declarations shared by the .cu files.
+#pragma once
+#include "store.cuh"
+
+namespace fc {
+struct AttnArgs {
+    int layer;
+    const void *q;
+    void *out;
+    float *lse;
+    float scale_log2;
+    int extra_tokens;
+    int attend_appended;
+    int pps;
+    int max_splits;
+    int32_t *counters;
+    float *part_ml;
+    float *part_o;
+};
+
+cudaError_t launch_alloc_pages(const StoreView &, int, int, int, cudaStream_t);
+cudaError_t launch_step_advance(const StoreView &, int, cudaStream_t);
+cudaError_t launch_evict_pages(const StoreView &, const int32_t *, int, cudaStream_t);
+cudaError_t launch_prefill(const StoreView &, int, int, int, const void *, const void *, int, cudaStream_t);
+cudaError_t launch_append(const StoreView &, int, int, const void *, const void *, int, cudaStream_t);
+cudaError_t launch_gather(const StoreView &, int, int, int, int, int, void *, void *, cudaStream_t);
+cudaError_t launch_score(const StoreView &, int, int, const void *, const uint8_t *, int, int, int, int,
+                         float *, int32_t *, int, int, cudaStream_t);
+cudaError_t launch_select(const float *, int, const int32_t *, int, int, int, int32_t *, int32_t *,
+                          cudaStream_t);
+cudaError_t launch_attn(const StoreView &, int, const AttnArgs &, int, cudaStream_t);
+size_t attn_workspace_bytes(const StoreView &, int, int);
+size_t rerank_workspace_bytes(const StoreView &);
+cudaError_t launch_rerank(const StoreView &, int, const int32_t *, const int32_t *, const uint8_t *, int,
+                          int, int, int, const uint8_t *, int32_t *, int, int32_t *, void *, int, cudaStream_t);
+cudaError_t launch_fetch(const StoreView &, int, const void *, const int32_t *, const int32_t *, int, int,
+                         cudaStream_t);
+cudaError_t launch_offload(const StoreView &, void *, const int32_t *, int, int, cudaStream_t);
+
+}  // namespace fc

@@ -1,0 +1,288 @@
+// recycle.cu — subsystem (4): stable-head rerank block recycling and the
+// pinned-host slow tier copies.
+//
+// Reference semantics:
+//   BlockTable.recycle  blocktable.py:296-357  evicted = old\new, promoted =
+//       new\old, paired ascending; surplus evictions freed, deficit allocated;
+//       copy list (promoted page, dest block); validations :313-327
+//   promoted_delta      tiering.py:42-46
+//   TierStore offload / reload (write-once ledger)  tiering.py:99-173
+//   simulator._rerank   simulator.py:500-547 (base = resident ∪ appended)
+//
+// The rerank is two launches per layer at a rerank step: a warp per head
+// computes the ascending diff with ballots and moves paired blocks in place
+// (the paper's fused recycle kernel), then one CTA applies
+// the free-list pushes/pops for all heads in head order.  Copies between the
+// pinned host tier and HBM are zero-copy UVA kernels: a
+// CTA per page moves 8 KiB with 16-byte loads, so many PCIe reads are in
+// flight without one cudaMemcpy per page.
+#include "store.cuh"
+#include <cub/block/block_scan.cuh>
+
+namespace fc {
+
+constexpr int kRecycleWarps = 4;
+constexpr int kListCap = 1024;  // max entries of an old/new selection list
+
+struct RerankWs {  // per head bh: [2 counts][kListCap free blocks][kListCap alloc pages]
+    int32_t *base;
+    __device__ __forceinline__ int32_t *cnt(int bh) const { return base + (int64_t)bh * (2 + 2 * kListCap); }
+    __device__ __forceinline__ int32_t *freed(int bh) const { return cnt(bh) + 2; }
+    __device__ __forceinline__ int32_t *alloc(int bh) const { return cnt(bh) + 2 + kListCap; }
+};
+
+FC_DEVINL bool sorted_contains(const int32_t *a, int n, int x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo < n && a[lo] == x;
+}
+
+__global__ void __launch_bounds__(kRecycleWarps * 32)
+rerank_diff_kernel(StoreView s, int layer, const int32_t *__restrict__ old_sel,
+                   const int32_t *__restrict__ n_old_arr, const uint8_t *__restrict__ unstable,
+                   int period, int force_due, int old_has_tail, int extra_tokens,
+                   const uint8_t *__restrict__ slow_resident,
+                   int32_t *copies, int max_copies, int32_t *n_copies, RerankWs ws, int batch) {
+    __shared__ int32_t s_ev[kRecycleWarps][kListCap];
+    __shared__ int32_t s_pr[kRecycleWarps][kListCap];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int bh = blockIdx.x * kRecycleWarps + w;
+    if (bh >= batch * s.H) return;
+    const int b = bh / s.H, h = bh % s.H;
+    int32_t *cnt = ws.cnt(bh);
+    const bool due = !unstable[layer * s.H + h] && (force_due || (*s.step % period == 0));
+    if (!due) {
+        if (lane == 0) { cnt[0] = 0; cnt[1] = 0; }
+        return;
+    }
+    const int hx = s.hix(b, layer, h);
+    const int n_pages = (s.seq_len[b] + extra_tokens + s.PS - 1) / s.PS;
+    const int32_t *olds = old_sel + (int64_t)bh * s.SELCAP;
+    const int n_old_sel = n_old_arr[bh];
+    const int hi_old = n_old_sel > 0 ? olds[n_old_sel - 1] : -1;
+    // resident set = old selection + pages appended since (simulator.py:512)
+    const int n_old = old_has_tail ? n_old_sel + max(0, n_pages - 1 - hi_old) : n_old_sel;
+    const int hi_res = old_has_tail ? max(hi_old, n_pages - 1) : hi_old;
+    const int32_t *news = s.sel + (int64_t)hx * s.SELCAP;
+    const int n_new = s.n_sel[hx];
+    int32_t *trow = s.table + s.table_off(hx, 0);
+    const unsigned lt = (1u << lane) - 1u;
+
+    // evicted = old \ new (ascending), validating residency of old
+    int n_ev = 0;
+    for (int base = 0; base < n_old; base += 32) {
+        const int i = base + lane;
+        bool ev = false;
+        int x = 0;
+        if (i < n_old) {
+            x = i < n_old_sel ? olds[i] : hi_old + 1 + (i - n_old_sel);
+            if (trow[x] == FC_NULL_BLOCK) set_error(s.err, FC_ERR_DOUBLE_EVICT);
+            ev = !sorted_contains(news, n_new, x);
+        }
+        const unsigned mk = __ballot_sync(0xffffffffu, ev);
+        if (ev) {
+            const int r = n_ev + __popc(mk & lt);
+            if (r < kListCap) s_ev[w][r] = x;
+        }
+        n_ev += __popc(mk);
+    }
+    // promoted = new \ old (ascending), validating non-residency and slow copy
+    int n_pr = 0;
+    for (int base = 0; base < n_new; base += 32) {
+        const int i = base + lane;
+        bool pr = false;
+        int x = 0;
+        if (i < n_new) {
+            x = news[i];
+            pr = (x > hi_res) || (x <= hi_old && !sorted_contains(olds, n_old_sel, x));
+            if (pr) {
+                if (trow[x] != FC_NULL_BLOCK) set_error(s.err, FC_ERR_DOUBLE_EVICT);
+                if (slow_resident && !slow_resident[s.table_off(hx, x)])
+                    set_error(s.err, FC_ERR_NULL_READ);
+            }
+        }
+        const unsigned mk = __ballot_sync(0xffffffffu, pr);
+        if (pr) {
+            const int r = n_pr + __popc(mk & lt);
+            if (r < kListCap) s_pr[w][r] = x;
+        }
+        n_pr += __popc(mk);
+    }
+    if (n_ev > kListCap || n_pr > kListCap) {
+        if (lane == 0) { set_error(s.err, FC_ERR_SEL_CAP); cnt[0] = 0; cnt[1] = 0; }
+        return;
+    }
+    __syncwarp();
+    const int m = min(n_ev, n_pr);
+    int cbase = 0;
+    if (lane == 0 && m > 0) cbase = atomicAdd(n_copies, m);
+    cbase = __shfl_sync(0xffffffffu, cbase, 0);
+    for (int i = lane; i < m; i += 32) {  // ascending pairs: evicted[i] hands its block to promoted[i]
+        const int e = s_ev[w][i], p = s_pr[w][i];
+        const int blk = trow[e];
+        trow[e] = FC_NULL_BLOCK;
+        trow[p] = blk;
+        if (cbase + i < max_copies) {
+            int32_t *cp = copies + 4 * (int64_t)(cbase + i);
+            cp[0] = b; cp[1] = h; cp[2] = p; cp[3] = blk;
+        } else {
+            set_error(s.err, FC_ERR_SEL_CAP);
+        }
+    }
+    int32_t *fr = ws.freed(bh);
+    for (int i = m + lane; i < n_ev; i += 32) {  // surplus evictions
+        const int e = s_ev[w][i];
+        fr[i - m] = trow[e];
+        trow[e] = FC_NULL_BLOCK;
+    }
+    int32_t *al = ws.alloc(bh);
+    for (int i = m + lane; i < n_pr; i += 32) al[i - m] = s_pr[w][i];  // deficit pages
+    if (lane == 0) { cnt[0] = n_ev - m; cnt[1] = n_pr - m; }
+}
+
+// one CTA: pushes of all heads (head order) then pops (head order)
+__global__ void __launch_bounds__(1024)
+rerank_commit_kernel(StoreView s, int layer, int32_t *copies, int max_copies, int32_t *n_copies,
+                     RerankWs ws, int batch) {
+    using Scan = cub::BlockScan<int, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int s_fail;
+    const int nh = batch * s.H;
+    const int top0 = *s.free_top;
+    // pass 1: pushes
+    int fcarry = 0;
+    for (int c0 = 0; c0 < nh; c0 += 1024) {
+        const int bh = c0 + threadIdx.x;
+        const int f = bh < nh ? ws.cnt(bh)[0] : 0;
+        int before, total;
+        Scan(tmp).ExclusiveSum(f, before, total);
+        for (int k = 0; k < f; ++k) s.free_stack[top0 + fcarry + before + k] = ws.freed(bh)[k];
+        fcarry += total;
+        __syncthreads();
+    }
+    const int top1 = top0 + fcarry;
+    // pass 2: pops
+    int acarry = 0;
+    for (int c0 = 0; c0 < nh; c0 += 1024) {
+        const int bh = c0 + threadIdx.x;
+        const int a = bh < nh ? ws.cnt(bh)[1] : 0;
+        int before, total;
+        Scan(tmp).ExclusiveSum(a, before, total);
+        if (threadIdx.x == 0) s_fail = (top1 - acarry - total < 0);
+        __syncthreads();
+        if (!s_fail && a > 0) {
+            const int b = bh / s.H, h = bh % s.H;
+            const int hx = s.hix(b, layer, h);
+            const int cb = atomicAdd(n_copies, a);
+            for (int k = 0; k < a; ++k) {
+                const int page = ws.alloc(bh)[k];
+                const int blk = s.free_stack[top1 - 1 - (acarry + before + k)];
+                s.table[s.table_off(hx, page)] = blk;
+                if (cb + k < max_copies) {
+                    int32_t *cp = copies + 4 * (int64_t)(cb + k);
+                    cp[0] = b; cp[1] = h; cp[2] = page; cp[3] = blk;
+                } else {
+                    set_error(s.err, FC_ERR_SEL_CAP);
+                }
+            }
+        }
+        if (s_fail) {
+            if (threadIdx.x == 0) set_error(s.err, FC_ERR_POOL_EXHAUSTED);
+            break;
+        }
+        acarry += total;
+        __syncthreads();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *s.free_top = top1 - acarry;
+}
+
+// ---------------------------------------------------------------------------
+// pinned-host <-> HBM page copies (zero-copy UVA)
+
+constexpr int kCopyThreads = 128;
+
+FC_DEVINL void copy_page(uint4 *dst, const uint4 *src, int n16) {
+    constexpr int U = 4;
+    for (int i0 = threadIdx.x; i0 < n16; i0 += kCopyThreads * U) {
+        uint4 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * kCopyThreads;
+            if (i < n16) r[u] = src[i];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * kCopyThreads;
+            if (i < n16) dst[i] = r[u];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kCopyThreads)
+fetch_kernel(StoreView s, int layer, const char *host_pages, const int32_t *copies,
+             const int32_t *n_copies, int max_copies, int page_bytes) {
+    const int n = min(*n_copies, max_copies);
+    for (int c = blockIdx.x; c < n; c += gridDim.x) {
+        const int b = copies[4 * c], h = copies[4 * c + 1], p = copies[4 * c + 2], blk = copies[4 * c + 3];
+        const int64_t src = (s.table_off(s.hix(b, layer, h), p)) * (int64_t)page_bytes;
+        copy_page(reinterpret_cast<uint4 *>(reinterpret_cast<char *>(s.pool) + (int64_t)blk * page_bytes),
+                  reinterpret_cast<const uint4 *>(host_pages + src), page_bytes / 16);
+    }
+}
+
+__global__ void __launch_bounds__(kCopyThreads)
+offload_kernel(StoreView s, char *host_pages, const int32_t *pages, int n, int page_bytes) {
+    for (int c = blockIdx.x; c < n; c += gridDim.x) {
+        const int b = pages[4 * c], l = pages[4 * c + 1], h = pages[4 * c + 2], p = pages[4 * c + 3];
+        const int64_t off = s.table_off(s.hix(b, l, h), p);
+        const int blk = s.table[off];
+        if (blk == FC_NULL_BLOCK) {
+            if (threadIdx.x == 0) set_error(s.err, FC_ERR_NULL_READ);
+            continue;
+        }
+        copy_page(reinterpret_cast<uint4 *>(host_pages + off * page_bytes),
+                  reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(s.pool) +
+                                                  (int64_t)blk * page_bytes),
+                  page_bytes / 16);
+    }
+}
+
+// ---------------------------------------------------------------------------
+
+size_t rerank_workspace_bytes(const StoreView &s) {
+    return (size_t)s.B * s.H * (2 + 2 * kListCap) * sizeof(int32_t);
+}
+
+cudaError_t launch_rerank(const StoreView &s, int layer, const int32_t *old_sel, const int32_t *n_old,
+                          const uint8_t *unstable, int period, int force_due, int old_has_tail,
+                          int extra_tokens, const uint8_t *slow_resident, int32_t *copies, int max_copies,
+                          int32_t *n_copies, void *workspace, int batch, cudaStream_t st) {
+    RerankWs ws{reinterpret_cast<int32_t *>(workspace)};
+    const int heads = batch * s.H;
+    rerank_diff_kernel<<<(heads + kRecycleWarps - 1) / kRecycleWarps, kRecycleWarps * 32, 0, st>>>(
+        s, layer, old_sel, n_old, unstable, period, force_due, old_has_tail, extra_tokens, slow_resident, copies, max_copies,
+        n_copies, ws, batch);
+    rerank_commit_kernel<<<1, 1024, 0, st>>>(s, layer, copies, max_copies, n_copies, ws, batch);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fetch(const StoreView &s, int layer, const void *host_pages, const int32_t *copies,
+                         const int32_t *n_copies, int max_copies, int page_bytes, cudaStream_t st) {
+    const int grid = max(1, min(max_copies, 148 * 8));
+    fetch_kernel<<<grid, kCopyThreads, 0, st>>>(s, layer, (const char *)host_pages, copies, n_copies,
+                                                max_copies, page_bytes);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_offload(const StoreView &s, void *host_pages, const int32_t *pages, int n,
+                           int page_bytes, cudaStream_t st) {
+    const int grid = max(1, min(n, 148 * 8));
+    offload_kernel<<<grid, kCopyThreads, 0, st>>>(s, (char *)host_pages, pages, n, page_bytes);
+    return cudaGetLastError();
+}
+
+}  // namespace fc

@@ -1,0 +1,202 @@
+"""DecodeEngine: the per-decode-step KV hot path for a batch of requests.
+
+This is the batched, GPU-resident counterpart of what the reference composes
+per head in Python (attention.sparsity_error, attention.py:150-159) and
+schedules in its simulator (simulator._decode_step / _append_token / _rerank,
+simulator.py:410-547).  One decode step over L layers is, per layer:
+
+  1. fc_kv_append      write the new token's k/v into its page and fold the
+                       key into that page's min/max summary   (subsystem 1)
+  2. fc_score_select   for due heads only (unstable every step, stable at
+                       t % R == 0; layers with no due head are skipped —
+                       layer_scoring_skippable, scoring.py:205-209): group
+                       page scores + exact top-K with the last page pinned
+                       (subsystem 2)
+  3. fc_sparse_decode  GQA split-K attention over sel ∪ pages appended since
+                       the head's last rerank, combine fused  (subsystem 3)
+
+then fc_step_advance (seq_len += 1; new pages allocated from the device free
+list).  Steps are replayed from CUDA graphs (one for rerank steps, one for
+plain steps) so the 3·L+1 launches cost no host time.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from .config import HeadId
+from .scoring import layer_scoring_skippable
+from .stability import HeadProfile
+from .store import PAGE_SIZE, KVStore
+
+
+class DecodeEngine:
+    def __init__(self, *, batch: int, layers: int, kv_heads: int, group: int, head_dim: int,
+                 ctx_cap_tokens: int, topk_pages: int, rerank_period: int,
+                 profile: HeadProfile, dtype=torch.bfloat16, device="cuda",
+                 n_blocks: int | None = None):
+        if profile.n_layers != layers or profile.n_heads_per_layer != kv_heads:
+            raise ValueError("profile grid does not match (layers, kv_heads)")
+        self.B, self.L, self.H, self.G, self.D = batch, layers, kv_heads, group, head_dim
+        self.K, self.R = topk_pages, rerank_period
+        self.profile = profile
+        self.device = torch.device(device)
+        pages_cap = ctx_cap_tokens // PAGE_SIZE + 1
+        if n_blocks is None:  # full residency: every page of every head has a block
+            n_blocks = batch * layers * kv_heads * pages_cap + 1
+        self.sel_slack = rerank_period // PAGE_SIZE + 2  # pages appended between reranks
+        self.store = KVStore(batch_cap=batch, layers=layers, kv_heads=kv_heads, group=group,
+                             head_dim=head_dim, pages_cap=pages_cap, n_blocks=n_blocks,
+                             sel_cap=topk_pages + self.sel_slack, dtype=dtype, device=self.device)
+        self.unstable = profile.mask_tensor(self.device).contiguous()
+        self.t = 1                # host mirror of store.step: the upcoming decode step
+        self.selected = False     # initial selection done (first step forces all heads due)
+        self.seq_host = [0] * batch
+        self.att_bound = min(pages_cap, topk_pages + self.sel_slack)
+        self.pps = self.store.choose_pages_per_split(batch, self.att_bound)
+        # static step buffers (CUDA-graph inputs/outputs)
+        Hq = kv_heads * group
+        self.q = torch.zeros((layers, batch, Hq, head_dim), dtype=dtype, device=self.device)
+        self.k_new = torch.zeros((layers, batch, kv_heads, head_dim), dtype=dtype, device=self.device)
+        self.v_new = torch.zeros_like(self.k_new)
+        self.out = torch.zeros_like(self.q)
+        self._graphs: dict[bool, torch.cuda.CUDAGraph] = {}
+
+    # -- prefill ----------------------------------------------------------------
+
+    def prefill(self, row: int, keys: torch.Tensor, values: torch.Tensor) -> None:
+        """keys/values [L, H, T, d] (any device): allocate pages for positions
+        0..T (the next decode position included) and write them with their
+        summaries (build_minmax, scoring.py:72-90)."""
+        L, H, T, d = keys.shape
+        self.store.alloc_pages(row, 0, T // PAGE_SIZE + 1)
+        for layer in range(L):
+            self.store.prefill(row, layer, keys[layer], values[layer])
+        self.store.seq_len[row] = T
+        self.seq_host[row] = T
+
+    def prefill_layer(self, row: int, layer: int, k: torch.Tensor, v: torch.Tensor,
+                      alloc: bool) -> None:
+        """Layer-at-a-time prefill (bench scale); ``alloc`` on the first layer."""
+        T = k.shape[1]
+        if alloc:
+            self.store.alloc_pages(row, 0, T // PAGE_SIZE + 1)
+        self.store.prefill(row, layer, k, v)
+        self.store.seq_len[row] = T
+        self.seq_host[row] = T
+
+    # -- one decode step -----------------------------------------------------------
+
+    def is_rerank_step(self, t: int | None = None) -> bool:
+        t = self.t if t is None else t
+        return t % self.R == 0
+
+    def _launch_step(self, rerank: bool, force_due: bool) -> None:
+        st = self.store
+        for layer in range(self.L):
+            st.append(layer, self.k_new[layer], self.v_new[layer], self.B)
+            if force_due or not self._layer_skippable(layer, rerank):
+                st.score_select(layer, self.q[layer], self.unstable, self.R, self.K, self.B,
+                                force_due=force_due, extra_tokens=1)
+            st.sparse_decode(layer, self.q[layer], self.out[layer], self.B,
+                             max_pages=self.att_bound, pps=self.pps, extra_tokens=1)
+        st.step_advance(self.B)
+
+    def _layer_skippable(self, layer: int, rerank: bool) -> bool:
+        # a representative step of the same kind: R (rerank) or 1 (plain, R > 1)
+        t = self.R if rerank else (1 if self.R > 1 else self.R)
+        return layer_scoring_skippable(layer, t, self.profile, self.R)
+
+    def step(self, *, use_graph: bool = True) -> torch.Tensor:
+        """Run one decode step on the engine's static buffers (q, k_new,
+        v_new -> out).  The first step after prefill makes the initial
+        selection for every head."""
+        rerank = self.is_rerank_step()
+        if not self.selected:
+            self._launch_step(rerank, force_due=True)
+            self.selected = True
+        elif use_graph:
+            g = self._graphs.get(rerank)
+            if g is None:
+                g = self._capture(rerank)
+            g.replay()
+        else:
+            self._launch_step(rerank, force_due=False)
+        self.t += 1
+        self.seq_host = [s + 1 for s in self.seq_host]
+        return self.out
+
+    def _capture(self, rerank: bool) -> torch.cuda.CUDAGraph:
+        # stream capture records the launches without executing them, so the
+        # engine state is untouched; workspaces were sized by the eager first step
+        torch.cuda.synchronize(self.device)
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                self._launch_step(rerank, force_due=False)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        torch.cuda.synchronize(self.device)
+        self._graphs[rerank] = g
+        return g
+
+    def launches_per_step(self, t: int) -> int:
+        """Library kernel launches in the step graph for step t: per layer an
+        append and an attention, a scoring launch for every layer with a due
+        head, and the step advance."""
+        rerank = self.is_rerank_step(t)
+        scored = sum(not self._layer_skippable(l, rerank) for l in range(self.L))
+        return 2 * self.L + scored + 1
+
+    # -- host-buffer API (end-to-end path) -------------------------------------------
+
+    def step_host(self, q_host: torch.Tensor, k_host: torch.Tensor, v_host: torch.Tensor,
+                  out_host: torch.Tensor) -> None:
+        """One step from pinned host inputs to a pinned host output: H2D of
+        q/k/v, the step, D2H of the attention outputs, all on the current
+        stream (asynchronous; the caller synchronises)."""
+        self.q.copy_(q_host, non_blocking=True)
+        self.k_new.copy_(k_host, non_blocking=True)
+        self.v_new.copy_(v_host, non_blocking=True)
+        self.step()
+        out_host.copy_(self.out, non_blocking=True)
+
+    # -- accounting ------------------------------------------------------------------
+
+    def attended_pages(self) -> torch.Tensor:
+        """[B, L, H] pages each head attends at the upcoming step (after its
+        selection): n_sel + pages appended since the head's last rerank."""
+        st = self.store
+        n_tok = st.seq_len.long() + 1
+        n_pages = (n_tok + PAGE_SIZE - 1) // PAGE_SIZE
+        last = torch.gather(st.sel.long(), 3, (st.n_sel.long() - 1).clamp(min=0).unsqueeze(-1))[..., 0]
+        last = torch.where(st.n_sel > 0, last, torch.full_like(last, -1))
+        app = (n_pages[:, None, None] - 1 - last).clamp(min=0)
+        return st.n_sel.long() + app
+
+    def attention_bytes(self, layer: int) -> int:
+        """Algorithmic HBM bytes of one fc_sparse_decode launch:
+        K+V of the attended pages (the partial last page by its tokens) + the
+        table and selection entries read + q and o."""
+        st = self.store
+        e = st.kv_pool.element_size()
+        att = self.attended_pages()[:, layer]                      # [B, H]
+        n_tok = st.seq_len.long() + 1
+        last_fill = ((n_tok - 1) % PAGE_SIZE + 1)[:, None]          # tokens in the last page
+        kv = ((att - 1) * PAGE_SIZE + last_fill) * 2 * self.D * e
+        meta = att * 8                                              # table + sel entries
+        qo = 2 * self.G * self.D * e
+        return int((kv + meta + qo).sum().item())
+
+    def scoring_bytes(self, layer: int, t: int) -> int:
+        """Algorithmic bytes of fc_score_select at step t for one layer: the
+        summaries of every scored page (all but the pinned last) + q."""
+        st = self.store
+        e = st.summaries.element_size()
+        due = [self.profile.is_unstable(HeadId(layer, h)) or t % self.R == 0 for h in range(self.H)]
+        n_pages = (st.seq_len.long() + 1 + PAGE_SIZE - 1) // PAGE_SIZE
+        per_head = ((n_pages - 1) * 2 * self.D * e + self.G * self.D * e)
+        return int(per_head.sum().item()) * sum(due)

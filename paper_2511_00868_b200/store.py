@@ -1,0 +1,225 @@
+"""KVStore: the GPU-resident, batched state of the FlexiCache hot path.
+
+One ``KVStore`` holds, for ``batch_cap`` request rows × L layers × H KV heads:
+
+* the physical KV pool ``[n_blocks, 2, ps, d]`` (block 0 = null block) —
+  ``PhysicalPool`` (blocktable.py:28-94) with its LIFO free list kept on the
+  device (``free_stack``/``free_top``);
+* the dense logical→physical table ``[B, L, H, N_cap]`` int32 —
+  ``BlockTable`` (blocktable.py:109-440);
+* the per-page key min/max summaries ``[B, L, H, N_cap, 2, d]`` —
+  ``MinMaxCache`` (scoring.py:114-139);
+* the current page selection per head ``[B, L, H, sel_cap]`` + count —
+  ``TopKSet`` (scoring.py:142-161);
+* ``seq_len[B]``, the decode step counter and a sticky device error word.
+
+All buffers are torch tensors; the C-ABI library (``_lib``) only receives
+their device pointers.  Every method is asynchronous on the current CUDA
+stream except ``check_errors`` and the host readbacks.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+
+from . import _lib
+from .errors import ConsistencyError, PoolExhausted
+
+PAGE_SIZE = 16
+_DTYPES = {torch.bfloat16: _lib.FC_BF16, torch.float32: _lib.FC_F32}
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class KVStore:
+    def __init__(self, *, batch_cap: int, layers: int, kv_heads: int, group: int,
+                 head_dim: int, pages_cap: int, n_blocks: int, sel_cap: int,
+                 dtype: torch.dtype = torch.bfloat16, device="cuda"):
+        if dtype not in _DTYPES:
+            raise ValueError("dtype must be torch.bfloat16 or torch.float32")
+        if n_blocks < 2:
+            raise ValueError("pool needs at least one real block beyond the null block")
+        self.lib = _lib.load()
+        self.device = torch.device(device)
+        if self.device.type != "cuda" or not torch.cuda.is_available():
+            raise RuntimeError("KVStore needs a CUDA device (B200, sm_100a); no CPU fallback")
+        self.B, self.L, self.H, self.G = batch_cap, layers, kv_heads, group
+        self.D, self.PS, self.NCAP, self.SELCAP = head_dim, PAGE_SIZE, pages_cap, sel_cap
+        self.dtype, self.n_blocks = dtype, n_blocks
+        dev = self.device
+        self.kv_pool = torch.zeros((n_blocks, 2, PAGE_SIZE, head_dim), dtype=dtype, device=dev)
+        self.summaries = torch.zeros((batch_cap, layers, kv_heads, pages_cap, 2, head_dim),
+                                     dtype=dtype, device=dev)
+        self.table = torch.zeros((batch_cap, layers, kv_heads, pages_cap), dtype=torch.int32, device=dev)
+        self.seq_len = torch.zeros(batch_cap, dtype=torch.int32, device=dev)
+        self.sel = torch.zeros((batch_cap, layers, kv_heads, sel_cap), dtype=torch.int32, device=dev)
+        self.n_sel = torch.zeros((batch_cap, layers, kv_heads), dtype=torch.int32, device=dev)
+        # fresh pool pops 1, 2, 3, ... (blocktable.py:38-39)
+        self.free_stack = torch.arange(n_blocks - 1, 0, -1, dtype=torch.int32, device=dev)
+        self.free_stack = torch.cat([self.free_stack, torch.zeros(1, dtype=torch.int32, device=dev)])
+        self.free_top = torch.tensor([n_blocks - 1], dtype=torch.int32, device=dev)
+        self.step = torch.ones(1, dtype=torch.int32, device=dev)
+        self.error_word = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._c = _lib.FcStore(
+            batch_cap, layers, kv_heads, group, head_dim, PAGE_SIZE, pages_cap, sel_cap,
+            _DTYPES[dtype], n_blocks,
+            self.kv_pool.data_ptr(), self.summaries.data_ptr(), self.table.data_ptr(),
+            self.seq_len.data_ptr(), self.sel.data_ptr(), self.n_sel.data_ptr(),
+            self.free_stack.data_ptr(), self.free_top.data_ptr(), self.step.data_ptr(),
+            self.error_word.data_ptr())
+        self.cptr = ctypes.addressof(self._c)
+        # scoring workspace: scores [B*H, N_cap] fp32 + per-head counters
+        self.scores = torch.full((batch_cap * kv_heads, pages_cap), float("-inf"),
+                                 dtype=torch.float32, device=dev)
+        self.score_counters = torch.zeros(batch_cap * kv_heads, dtype=torch.int32, device=dev)
+        self._attn_ws = torch.zeros(0, dtype=torch.uint8, device=dev)
+        self._rerank_ws = None
+
+    # -- misc ------------------------------------------------------------------
+
+    @property
+    def page_bytes(self) -> int:
+        return 2 * PAGE_SIZE * self.D * self.kv_pool.element_size()
+
+    def stream(self) -> int:
+        return _stream(self.device)
+
+    def check_errors(self) -> None:
+        """Synchronise and raise the reference exception for any sticky
+        device error bit (then clear it)."""
+        bits = int(self.error_word.item()) & 0xFFFFFFFF
+        if not bits:
+            return
+        self.error_word.zero_()
+        if bits & _lib.FC_ERR_POOL_EXHAUSTED:
+            raise PoolExhausted(f"fast pool exhausted ({self.n_blocks - 1} blocks)")
+        if bits & (_lib.FC_ERR_NULL_READ | _lib.FC_ERR_DOUBLE_EVICT):
+            raise ConsistencyError(
+                "residency violation: read of the null block / double eviction "
+                f"(device error bits {bits:#x})")
+        if bits & _lib.FC_ERR_NULL_WRITE:
+            raise ConsistencyError("append into a page with no physical block")
+        raise ValueError(f"capacity exceeded (device error bits {bits:#x})")
+
+    def free_count(self) -> int:
+        return int(self.free_top.item())
+
+    # -- allocation / steps ------------------------------------------------------
+
+    def alloc_pages(self, row: int, first_page: int, n_pages: int) -> None:
+        _lib.check(self.lib.fc_alloc_pages(self.cptr, row, first_page, n_pages, self.stream()),
+                   "fc_alloc_pages")
+
+    def step_advance(self, batch: int) -> None:
+        _lib.check(self.lib.fc_step_advance(self.cptr, batch, self.stream()), "fc_step_advance")
+
+    def evict_pages(self, pages: torch.Tensor) -> None:
+        """pages: int32 [n, 4] (row, layer, head, logical) on the device."""
+        pages = pages.to(self.device, torch.int32).contiguous()
+        _lib.check(self.lib.fc_evict_pages(self.cptr, pages.data_ptr(), pages.shape[0], self.stream()),
+                   "fc_evict_pages")
+
+    # -- (1) KV writes -------------------------------------------------------------
+
+    def prefill(self, row: int, layer: int, k: torch.Tensor, v: torch.Tensor) -> None:
+        """k, v: [H, T, d] in the store dtype, on the device."""
+        k = k.to(self.device, self.dtype).contiguous()
+        v = v.to(self.device, self.dtype).contiguous()
+        if k.shape != v.shape or k.dim() != 3 or k.shape[0] != self.H or k.shape[2] != self.D:
+            raise ValueError("k and v must both be [H, T, d]")
+        _lib.check(self.lib.fc_kv_prefill(self.cptr, row, layer, k.data_ptr(), v.data_ptr(),
+                                          k.shape[1], self.stream()), "fc_kv_prefill")
+
+    def append(self, layer: int, k_new: torch.Tensor, v_new: torch.Tensor, batch: int) -> None:
+        """k_new, v_new: [batch, H, d] contiguous in the store dtype."""
+        _lib.check(self.lib.fc_kv_append(self.cptr, layer, k_new.data_ptr(), v_new.data_ptr(),
+                                         batch, self.stream()), "fc_kv_append")
+
+    def gather(self, row: int, layer: int, head: int, n_pages: int):
+        """Logical K/V [n_pages*ps, d] of one head (un-swizzled readback)."""
+        k = torch.empty((n_pages * PAGE_SIZE, self.D), dtype=self.dtype, device=self.device)
+        v = torch.empty_like(k)
+        _lib.check(self.lib.fc_kv_gather(self.cptr, row, layer, head, n_pages, k.data_ptr(),
+                                         v.data_ptr(), self.stream()), "fc_kv_gather")
+        return k, v
+
+    # -- (2) scoring / selection -----------------------------------------------------
+
+    def score_select(self, layer: int, q: torch.Tensor, unstable: torch.Tensor, period: int,
+                     topk: int, batch: int, *, force_due: bool = False, extra_tokens: int = 1) -> None:
+        _lib.check(self.lib.fc_score_select(
+            self.cptr, layer, q.data_ptr(), unstable.data_ptr(), period, int(force_due), topk,
+            extra_tokens, self.scores.data_ptr(), self.score_counters.data_ptr(), batch,
+            self.stream()), "fc_score_select")
+
+    def score_pages(self, layer: int, q: torch.Tensor, batch: int, *, extra_tokens: int = 0) -> None:
+        _lib.check(self.lib.fc_score_pages(self.cptr, layer, q.data_ptr(), extra_tokens,
+                                           self.scores.data_ptr(), batch, self.stream()),
+                   "fc_score_pages")
+
+    # -- (3) attention -------------------------------------------------------------
+
+    def choose_pages_per_split(self, batch: int, max_pages: int) -> int:
+        """Pages per CTA so the grid covers ~4 CTAs per SM (148 SMs)."""
+        total = max(1, batch * self.H * max_pages)
+        pps = math.ceil(total / (148 * 4))
+        pps = max(4, min(256, pps))
+        return min(pps, max(1, max_pages))
+
+    def attn_workspace(self, batch: int, max_pages: int, pps: int) -> torch.Tensor:
+        need = self.lib.fc_sparse_decode_workspace_size(self.cptr, batch, max_pages, pps)
+        if self._attn_ws.numel() < need:
+            self._attn_ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
+        return self._attn_ws
+
+    def sparse_decode(self, layer: int, q: torch.Tensor, out: torch.Tensor, batch: int, *,
+                      max_pages: int, pps: int | None = None, lse: torch.Tensor | None = None,
+                      scale: float | None = None, extra_tokens: int = 1,
+                      attend_appended: bool = True) -> None:
+        if pps is None:
+            pps = self.choose_pages_per_split(batch, max_pages)
+        ws = self.attn_workspace(batch, max_pages, pps)
+        scale = 1.0 / math.sqrt(self.D) if scale is None else scale
+        _lib.check(self.lib.fc_sparse_decode(
+            self.cptr, layer, q.data_ptr(), out.data_ptr(), _ptr(lse), scale, extra_tokens,
+            int(attend_appended), max_pages, pps, ws.data_ptr(), ws.numel(), batch, self.stream()),
+            "fc_sparse_decode")
+
+    # -- (4) rerank / tiers ------------------------------------------------------------
+
+    def rerank_workspace(self) -> torch.Tensor:
+        if self._rerank_ws is None:
+            n = self.lib.fc_rerank_workspace_size(self.cptr)
+            self._rerank_ws = torch.zeros(n, dtype=torch.uint8, device=self.device)
+        return self._rerank_ws
+
+    def rerank_recycle(self, layer: int, old_sel: torch.Tensor, n_old: torch.Tensor,
+                       unstable: torch.Tensor, period: int, copies: torch.Tensor,
+                       n_copies: torch.Tensor, batch: int, *, force_due: bool = False,
+                       old_has_tail: bool = True, extra_tokens: int = 1,
+                       slow_resident: torch.Tensor | None = None) -> None:
+        ws = self.rerank_workspace()
+        _lib.check(self.lib.fc_rerank_recycle(
+            self.cptr, layer, old_sel.data_ptr(), n_old.data_ptr(), unstable.data_ptr(), period,
+            int(force_due), int(old_has_tail), extra_tokens, _ptr(slow_resident),
+            copies.data_ptr(), copies.shape[0], n_copies.data_ptr(), ws.data_ptr(), batch,
+            self.stream()), "fc_rerank_recycle")
+
+    def fetch_pages(self, layer: int, host_pages: torch.Tensor, copies: torch.Tensor,
+                    n_copies: torch.Tensor) -> None:
+        _lib.check(self.lib.fc_fetch_pages(self.cptr, layer, host_pages.data_ptr(), copies.data_ptr(),
+                                           n_copies.data_ptr(), copies.shape[0], self.stream()),
+                   "fc_fetch_pages")
+
+    def offload_pages(self, host_pages: torch.Tensor, pages: torch.Tensor) -> None:
+        _lib.check(self.lib.fc_offload_pages(self.cptr, host_pages.data_ptr(), pages.data_ptr(),
+                                             pages.shape[0], self.stream()), "fc_offload_pages")
