@@ -265,8 +265,8 @@ def run_ours(args, cfg):
     for l in range(L):
         a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        eng.store.sparse_decode(l, eng.q[l], eng.out[l], B, max_pages=eng.att_bound, pps=eng.pps,
-                                extra_tokens=1)
+        eng.store.sparse_decode(l, eng.q[l], eng.out[l], B, max_pages=eng.att_bound, extra_tokens=1,
+                                attend_appended=False)
         b_.record(stream)
         durs.append((a, b_))
     torch.cuda.synchronize(dev)

@@ -98,7 +98,10 @@ int fc_alloc_pages(const fc_store *s, int row, int first_page, int n_pages,
  * length starts a page get that page for every (layer, head), popped in
  * (row, layer, head) order — BlockTable.allocate_page_all_heads
  * (blocktable.py:248-263) as driven by simulator._append_token
- * (simulator.py:455-466).  Advances *step. */
+ * (simulator.py:455-466) — and the page joins every head's current
+ * selection (n_sel > 0): the page being written is always attended, as
+ * the simulator's "resident ∪ appended" (simulator.py:463-466,512), so a
+ * selection row is always the complete attended set.  Advances *step. */
 int fc_step_advance(const fc_store *s, int batch, void *stream);
 
 /* ---- (1) KV append + per-page min/max summaries ------------------------ */
@@ -162,18 +165,25 @@ int fc_select_topk(const float *scores, int stride, const int32_t *n_valid,
  * — sparse_decode / dense_decode (attention.py:76-111) with the stable-head
  * rule "selection at the last rerank plus pages appended since"
  * (simulator.py:416-420,512).  attend_appended = 0 attends exactly
- * sel[0..n_sel) (the per-call reference sparse_decode contract).  softmax scale = scale (1/sqrt(d) in the
- * reference, attention.py:69).  out: [batch][H*G][d] store dtype;
- * lse: optional [batch][H*G] fp32 natural-log sum-exp.  Split-K over pages
- * (`pages_per_split`), combine fused in the last CTA of each head.
- * `max_pages` bounds the attended pages of any head (grid size). */
+ * sel[0..n_sel) (the per-call reference sparse_decode contract).
+ * softmax scale = scale (1/sqrt(d) in the reference, attention.py:69).
+ * Fused append: when k_new/v_new ([batch][H][d], store dtype) are given
+ * (decode, extra_tokens = 1), the CTA that stages a head's last page writes
+ * the new token into it and folds the key into the page summary
+ * (update_minmax, scoring.py:59-69) — fc_kv_append in the same launch.
+ * out: [batch][H*G][d] store dtype; lse: optional [batch][H*G] fp32
+ * natural-log sum-exp.  The concatenated page lists of all heads are cut into
+ * equal ranges, one per CTA (n_ctas = 0: one full wave, 2 per SM); heads
+ * spanning several CTAs are combined by the last CTA to finish them.
+ * `max_pages` bounds the attended pages of any head (grid sizing). */
 size_t fc_sparse_decode_workspace_size(const fc_store *s, int batch,
-                                       int max_pages, int pages_per_split);
-int fc_sparse_decode(const fc_store *s, int layer, const void *q, void *out,
+                                       int max_pages, int n_ctas);
+int fc_sparse_decode(const fc_store *s, int layer, const void *q,
+                     const void *k_new, const void *v_new, void *out,
                      float *lse, float scale, int extra_tokens,
-                     int attend_appended, int max_pages,
-                     int pages_per_split, void *workspace, size_t ws_bytes,
-                     int batch, void *stream);
+                     int attend_appended, int max_pages, int n_ctas,
+                     void *workspace, size_t ws_bytes, int batch,
+                     void *stream);
 
 /* ---- (4) stable-head rerank: recycle + tier copies ---------------------- */
 

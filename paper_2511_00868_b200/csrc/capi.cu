@@ -60,6 +60,11 @@ extern "C" {
 const char *fc_version(void) { return "flexicache-b200 0.1 sm_100a"; }
 const char *fc_last_error(void) { return g_last_error; }
 
+/* profiling hook (not part of the ABI): per-CTA globaltimer trace of the
+ * attention kernel into a device buffer [grid][4] u64, or null to disable */
+int fc_debug_attn_trace(void *device_buf) { return cuda_status(set_attn_trace(device_buf)); }
+int fc_debug_score_trace(void *device_buf) { return cuda_status(set_score_trace(device_buf)); }
+
 int fc_alloc_pages(const fc_store *s, int row, int first_page, int n_pages, void *stream) {
     FC_CHECK(check_store(s));
     if (row < 0 || row >= s->batch_cap) return invalid("row out of range");
@@ -123,7 +128,7 @@ int fc_score_select(const fc_store *s, int layer, const void *q, const uint8_t *
     if (topk > s->sel_cap) return FC_E_CAPACITY;
     if (extra_tokens < 0 || extra_tokens > 1) return invalid("extra_tokens must be 0 or 1");
     if (!q || !unstable || !scores_out || !counters) return invalid("null buffer");
-    if ((size_t)s->pages_cap * 4 > 200 * 1024) return FC_E_CAPACITY;
+    if (s->pages_cap > 8192) return FC_E_CAPACITY;  /* 128k-token heads (block_select keys <= 32*256) */
     if (batch == 0) return FC_OK;
     return cuda_status(launch_score(make_view(s), s->dtype, layer, q, unstable, period, force_due, topk,
                                     extra_tokens, scores_out, counters, 1, batch, (cudaStream_t)stream));
@@ -146,44 +151,50 @@ int fc_select_topk(const float *scores, int stride, const int32_t *n_valid, int 
                    int32_t *sel_out, int32_t *n_out, void *stream) {
     if (topk < 1) return invalid("k must be >= 1");
     if (stride < 1 || n_heads < 0) return invalid("bad stride / n_heads");
-    if ((size_t)stride * 4 > 200 * 1024) return FC_E_CAPACITY;
+    if (stride > 8192) return FC_E_CAPACITY;
     if (!scores || !n_valid || !sel_out || !n_out) return invalid("null buffer");
     if (n_heads == 0) return FC_OK;
     return cuda_status(launch_select(scores, stride, n_valid, n_heads, topk, pin_last, sel_out, n_out,
                                      (cudaStream_t)stream));
 }
 
-size_t fc_sparse_decode_workspace_size(const fc_store *s, int batch, int max_pages, int pages_per_split) {
-    if (check_store(s) != FC_OK || pages_per_split < 1) return 0;
-    const int max_splits = (max_pages + pages_per_split - 1) / pages_per_split;
-    return attn_workspace_bytes(make_view(s), batch, max_splits < 1 ? 1 : max_splits);
+size_t fc_sparse_decode_workspace_size(const fc_store *s, int batch, int max_pages, int n_ctas) {
+    if (check_store(s) != FC_OK || max_pages < 1 || n_ctas < 0) return 0;
+    const StoreView v = make_view(s);
+    return attn_workspace_bytes(v, batch, attn_grid(v, s->dtype, batch, max_pages, n_ctas));
 }
 
-int fc_sparse_decode(const fc_store *s, int layer, const void *q, void *out, float *lse, float scale,
-                     int extra_tokens, int attend_appended, int max_pages, int pages_per_split, void *workspace, size_t ws_bytes,
-                     int batch, void *stream) {
+int fc_sparse_decode(const fc_store *s, int layer, const void *q, const void *k_new, const void *v_new,
+                     void *out, float *lse, float scale, int extra_tokens, int attend_appended,
+                     int max_pages, int n_ctas, void *workspace, size_t ws_bytes, int batch,
+                     void *stream) {
     FC_CHECK(check_store(s));
     if (layer < 0 || layer >= s->layers) return invalid("layer out of range");
     if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
+    if (batch * s->kv_heads > 2048) return FC_E_CAPACITY;
     if (!q || !out || !workspace) return invalid("null buffer");
-    if (pages_per_split < 1 || pages_per_split > 256) return invalid("pages_per_split must be in 1..256");
+    if ((k_new == nullptr) != (v_new == nullptr)) return invalid("k_new and v_new go together");
+    if (k_new && extra_tokens != 1) return invalid("fused append needs extra_tokens = 1");
+    if (n_ctas < 0) return invalid("n_ctas must be >= 0 (0 = one full wave)");
     if (max_pages < 1) return invalid("max_pages must be >= 1");
     if (!(scale > 0.f) || !std::isfinite(scale)) return invalid("scale must be positive");
     if (extra_tokens < 0 || extra_tokens > 1) return invalid("extra_tokens must be 0 or 1");
-    const int max_splits = (max_pages + pages_per_split - 1) / pages_per_split;
     const StoreView v = make_view(s);
-    const size_t need = attn_workspace_bytes(v, batch, max_splits);
+    const int grid = attn_grid(v, s->dtype, batch, max_pages, n_ctas);
+    const size_t need = attn_workspace_bytes(v, batch, grid);
     if (ws_bytes < need) return FC_E_CAPACITY;
     if (batch == 0) return FC_OK;
     const size_t heads = (size_t)s->batch_cap * s->kv_heads;
+    const size_t parts = heads + (size_t)grid * 4;  // partial ids head + global warp (4 warps/CTA)
     AttnArgs a;
-    a.layer = layer; a.q = q; a.out = out; a.lse = lse;
+    a.layer = layer; a.q = q; a.k_new = k_new; a.v_new = v_new; a.out = out; a.lse = lse;
     a.scale_log2 = scale * 1.4426950408889634f;
-    a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.pps = pages_per_split; a.max_splits = max_splits;
+    a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.max_splits = grid;
     char *w = (char *)workspace;
-    a.counters = (int32_t *)w;
-    a.part_ml = (float *)(w + heads * sizeof(int32_t));
-    a.part_o = a.part_ml + heads * max_splits * s->group * 2;
+    a.plan = (int32_t *)w;
+    a.part_m = (float *)(w + ((2 * heads * sizeof(int32_t) + 255) & ~(size_t)255));
+    a.part_l = a.part_m + parts * 16;
+    a.part_o = a.part_l + parts * 16;
     return cuda_status(launch_attn(v, s->dtype, a, batch, (cudaStream_t)stream));
 }
 

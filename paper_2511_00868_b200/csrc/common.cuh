@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <utility>
 
 #include "../../include/flexicache_b200.h"
 
@@ -125,6 +126,33 @@ FC_DEVINL void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0
 }
 
 // ---------------------------------------------------------------------------
+// programmatic dependent launch (PDL): griddepcontrol PTX
+
+// Wait until the grids this one depends on have completed and their memory
+// is visible (no-op when launched without the PDL attribute).
+FC_DEVINL void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Allow the dependent grid to be scheduled now (it still waits for our completion).
+FC_DEVINL void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+// Launch with cudaLaunchAttributeProgrammaticStreamSerialization so that the
+// kernel's launch overlaps the tail of the previous kernel on the stream.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// ---------------------------------------------------------------------------
 // misc
 
 FC_DEVINL float warp_max(float v) {
@@ -149,6 +177,10 @@ FC_DEVINL uint32_t score_key(float f) {
     uint32_t u = __float_as_uint(f);
     if (u == 0x80000000u) u = 0u;
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+FC_DEVINL float key_to_float(uint32_t k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
 }  // namespace fc

@@ -68,8 +68,19 @@ __global__ void step_advance_kernel(StoreView s, int batch) {
             const int r = rows_needing[e / LH];
             const int lh = e % LH;
             const int page = (s.seq_len[r] + 1) / s.PS;  // seq_len not yet written
-            s.table[s.table_off(s.hix(r, lh / s.H, lh % s.H), page)] =
-                s.free_stack[top - 1 - e];
+            const int hx = s.hix(r, lh / s.H, lh % s.H);
+            s.table[s.table_off(hx, page)] = s.free_stack[top - 1 - e];
+            // the new page joins the head's selection: it is attended from now
+            // on (appended pages, simulator.py:463-466,512; pinned at reranks)
+            const int n = s.n_sel[hx];
+            if (n > 0) {
+                if (n < s.SELCAP) {
+                    s.sel[(int64_t)hx * s.SELCAP + n] = page;
+                    s.n_sel[hx] = n + 1;
+                } else {
+                    set_error(s.err, FC_ERR_SEL_CAP);
+                }
+            }
         }
     }
     __syncthreads();

@@ -6,15 +6,17 @@ namespace fc {
 struct AttnArgs {
     int layer;
     const void *q;
+    const void *k_new;    // fused append: [batch][H][D] or null
+    const void *v_new;
     void *out;
     float *lse;
     float scale_log2;
     int extra_tokens;
     int attend_appended;
-    int pps;
     int max_splits;
-    int32_t *counters;
-    float *part_ml;
+    int32_t *plan;        // [batch*H][2] first/last warp of each split head (-1: none)
+    float *part_m;        // [parts][16]
+    float *part_l;        // [parts][16]
     float *part_o;
 };
 
@@ -30,6 +32,9 @@ cudaError_t launch_select(const float *, int, const int32_t *, int, int, int, in
                           cudaStream_t);
 cudaError_t launch_attn(const StoreView &, int, const AttnArgs &, int, cudaStream_t);
 size_t attn_workspace_bytes(const StoreView &, int, int);
+cudaError_t set_attn_trace(void *);
+cudaError_t set_score_trace(void *);
+int attn_grid(const StoreView &, int, int, int, int);
 size_t rerank_workspace_bytes(const StoreView &);
 cudaError_t launch_rerank(const StoreView &, int, const int32_t *, const int32_t *, const uint8_t *, int,
                           int, int, int, const uint8_t *, int32_t *, int, int32_t *, void *, int, cudaStream_t);

@@ -13,87 +13,248 @@
 // with w = [sum_g q_g⁻ | sum_g q_g⁺]: scoring costs one pass over the
 // summaries regardless of G and is HBM-bound (2d*e bytes per page).
 //
-// Selection is a block-wide 4-pass 8-bit radix select on an orderable 32-bit
-// key of the fp32 score (-0.0 == +0.0), ties resolved by lowest page index,
-// fused into the last CTA to finish scoring a head (threadfence reduction).
+// Selection is a block-wide exact threshold search (2 key bits per round) on
+// an orderable 32-bit key of the fp32 score (-0.0 == +0.0), ties resolved by
+// lowest page index, fused into the last CTA to finish scoring a head
+// (threadfence reduction).
 #include "store.cuh"
 #include <cub/block/block_scan.cuh>
 
 namespace fc {
+
+// Optional per-CTA timeline for profiling (see fc_debug_attn_trace): [grid][4]
+__device__ unsigned long long *g_score_trace = nullptr;
+FC_DEVINL unsigned long long gtimer_s() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 constexpr int kScoreThreads = 256;
 constexpr int kRoundsPerIter = 8;   // pages per lane-slot per iteration (MLP)
 
 // ---------------------------------------------------------------------------
 // block-wide exact top-K over keys[0..n) in shared memory.
-// Selects the kprime largest (key desc, index asc) and writes their indices in
-// ascending order to out[0..kprime).  Requires kprime < n.
+//
+// Radix select, MSB digit first, three block-wide passes of 11/11/10 bits on
+// an orderable 32-bit key.  Keys live in registers (thread t owns indices
+// t + k*NT, so warp w's k-th keys are exactly bit-word w + k*NT/32 of the
+// index space).  Each pass: a 2048-bin shared histogram (each warp folds the
+// lanes sharing lane 0's digit into one atomic — real scores crowd into few
+// top-digit bins), one block scan over the bins, the digit holding the
+// kprime-th key.  T = the kprime-th largest key; every key > T is taken plus
+// the lowest-index keys == T up to kprime — select_topk's (score desc, index
+// asc) order (scoring.py:186).  Selection bits are built per 32-index word
+// with ballots and emitted in ascending order after one scan of word counts.
+// 0 < kprime < n <= 32*NT.
+constexpr int kSelBins = 2048;
 
-template <int NT>
-__device__ void block_select(const uint32_t *keys, int n, int kprime, int32_t *out) {
+template <int NT, int KPT>
+__device__ void block_select_kpt(const uint32_t *keys, int n, int kprime, int32_t *out) {
     using Scan = cub::BlockScan<int, NT>;
+    constexpr int BPT = kSelBins / NT;  // bins per thread
+    constexpr int NWORDS = NT * KPT / 32;
     __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ int hist[256];
-    __shared__ uint32_t s_prefix;
-    __shared__ int s_remaining;
-    const int tid = threadIdx.x;
-    uint32_t prefix = 0, mask = 0;
-    int remaining = kprime;
-    for (int shift = 24; shift >= 0; shift -= 8) {
-        for (int i = tid; i < 256; i += NT) hist[i] = 0;
+    __shared__ int hist[kSelBins];
+    __shared__ uint32_t gt_bits[NWORDS], eq_bits[NWORDS];
+    __shared__ int s_digit, s_above;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    uint32_t kv[KPT];
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+        const int i = tid + k * NT;
+        kv[k] = i < n ? keys[i] : 0u;  // key 0 never beats a real key (scores are not NaN)
+    }
+#ifdef FC_SEL_PROFILE
+    long long tp[12]; int np_ = 0; tp[np_++] = clock64();
+#define FC_SEL_STAMP() tp[np_++] = clock64()
+#else
+#define FC_SEL_STAMP()
+#endif
+    __shared__ uint32_t s_kmin, s_kmax, s_T;
+    __shared__ int s_rem, s_ncand, s_done;
+    __shared__ uint32_t cand_key[32];
+    __shared__ int cand_idx[32];
+    // ---- fast path: one pass of 2048 linear bins over [min key, max key]; the
+    // crossing bin of a continuous score distribution holds a handful of keys,
+    // ranked exactly by one warp.  Otherwise (ties / skew) the radix passes run.
+    {
+        uint32_t lo_k = 0xffffffffu, hi_k = 0u;
+#pragma unroll
+        for (int k = 0; k < KPT; ++k)
+            if (tid + k * NT < n) { lo_k = min(lo_k, kv[k]); hi_k = max(hi_k, kv[k]); }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo_k = min(lo_k, __shfl_xor_sync(0xffffffffu, lo_k, o));
+            hi_k = max(hi_k, __shfl_xor_sync(0xffffffffu, hi_k, o));
+        }
+        for (int i = tid; i < kSelBins; i += NT) hist[i] = 0;
+        if (tid == 0) { s_kmin = 0xffffffffu; s_kmax = 0u; s_ncand = 0; s_done = 0; }
         __syncthreads();
-        for (int i = tid; i < n; i += NT) {
-            const uint32_t k = keys[i];
-            if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1);
+        if (lane == 0) { atomicMin(&s_kmin, lo_k); atomicMax(&s_kmax, hi_k); }
+        __syncthreads();
+        // bins linear in the score VALUE (monotone in the key): robust to a few
+        // outliers, unlike linear bins in key space
+        const float fmin = key_to_float(s_kmin), fmax = key_to_float(s_kmax);
+        const float scale = fmax > fmin ? (float)kSelBins / (fmax - fmin) : 0.f;
+        auto lbin = [&](uint32_t key) {
+            const float b = (key_to_float(key) - fmin) * scale;
+            return b >= (float)(kSelBins - 1) ? kSelBins - 1 : (int)b;
+        };
+#pragma unroll
+        for (int k = 0; k < KPT; ++k)
+            if (tid + k * NT < n) atomicAdd(&hist[lbin(kv[k])], 1);
+        __syncthreads();
+        int loc[BPT], sum = 0;
+#pragma unroll
+        for (int j = 0; j < BPT; ++j) {
+            loc[j] = hist[kSelBins - 1 - (tid * BPT + j)];
+            sum += loc[j];
+        }
+        int before, tot;
+        Scan(scan_tmp).ExclusiveSum(sum, before, tot);
+        int run = before;
+#pragma unroll
+        for (int j = 0; j < BPT; ++j) {
+            if (run < kprime && run + loc[j] >= kprime) {
+                s_digit = kSelBins - 1 - (tid * BPT + j);
+                s_above = run;
+            }
+            run += loc[j];
         }
         __syncthreads();
-        // suffix count from the high digit down: cnt_ge(d) = sum_{d' >= d} hist[d']
-        // thread t handles digit 255 - t (NT >= 256)
-        const int digit = 255 - tid;
-        const int c = (tid < 256) ? hist[digit] : 0;
-        int incl, total;
-        Scan(scan_tmp).InclusiveSum(c, incl, total);
-        if (tid < 256) {
-            const int above = incl - c;  // keys with a larger digit
-            if (above < remaining && incl >= remaining) {
-                s_prefix = prefix | ((uint32_t)digit << shift);
-                s_remaining = remaining - above;
+        const int B = s_digit;
+        if (hist[B] <= 32) {
+#pragma unroll
+            for (int k = 0; k < KPT; ++k)
+                if (tid + k * NT < n && lbin(kv[k]) == B) {
+                    const int slot = atomicAdd(&s_ncand, 1);
+                    cand_key[slot] = kv[k];
+                    cand_idx[slot] = tid + k * NT;
+                }
+            __syncthreads();
+            if (tid < 32) {
+                const int c = s_ncand, need = kprime - s_above;  // 1 <= need <= c
+                const uint32_t myk = lane < c ? cand_key[lane] : 0u;
+                const int myi = lane < c ? cand_idx[lane] : 0x7fffffff;
+                int rank = 0, gt = 0;
+                for (int j = 0; j < c; ++j) {
+                    const uint32_t kj = __shfl_sync(0xffffffffu, myk, j);
+                    const int ij = __shfl_sync(0xffffffffu, myi, j);
+                    rank += (kj > myk) || (kj == myk && ij < myi);
+                    gt += kj > myk;
+                }
+                if (lane < c && rank == need - 1) {  // the kprime-th key overall
+                    s_T = myk;
+                    s_rem = need - gt;                 // keys == T still to take
+                    s_done = 1;
+                }
             }
         }
         __syncthreads();
-        prefix = s_prefix;
-        remaining = s_remaining;
-        mask |= 255u << shift;
+    }
+    uint32_t prefix = 0, mask = 0;
+    int remaining = kprime;
+    if (s_done) {
+        prefix = s_T;
+        remaining = s_rem;
+    }
+#pragma unroll 1
+    for (int pass = 0; pass < 3 && !s_done; ++pass) {
+        const int shift = pass == 0 ? 21 : pass == 1 ? 10 : 0;
+        const uint32_t dmask = pass == 2 ? 0x3ffu : 0x7ffu;
+        for (int i = tid; i < kSelBins; i += NT) hist[i] = 0;
         __syncthreads();
-    }
-    // prefix is the kprime-th largest key; take every larger key and the
-    // `remaining` lowest-index keys equal to it.
-    const uint32_t T = prefix;
-    const int per = (n + NT - 1) / NT;
-    const int lo = min(n, tid * per), hi = min(n, lo + per);
-    int eq_local = 0, gt_local = 0;
-    for (int i = lo; i < hi; ++i) {
-        const uint32_t k = keys[i];
-        eq_local += (k == T);
-        gt_local += (k > T);
-    }
-    int eq_before, dummy;
-    Scan(scan_tmp).ExclusiveSum(eq_local, eq_before, dummy);
-    __syncthreads();
-    const int take_eq = max(0, min(eq_local, remaining - eq_before));
-    int pos, total_sel;
-    Scan(scan_tmp).ExclusiveSum(gt_local + take_eq, pos, total_sel);
-    int eq_seen = 0;
-    for (int i = lo; i < hi; ++i) {
-        const uint32_t k = keys[i];
-        bool take = k > T;
-        if (k == T) {
-            take = eq_seen < take_eq;
-            ++eq_seen;
+        FC_SEL_STAMP();
+        {
+            // the warp's dominant digit (lane 0's first key) is counted in a
+            // register across all KPT keys: one atomic per warp for it, so the
+            // crowded top-digit bin sees 8 atomics, not one per key
+            const bool v0 = tid < n && (kv[0] & mask) == prefix;
+            const int dom = __shfl_sync(0xffffffffu, v0 ? (int)((kv[0] >> shift) & dmask) : -1, 0);
+            int dom_cnt = 0;
+#pragma unroll
+            for (int k = 0; k < KPT; ++k) {
+                const bool valid = (tid + k * NT) < n && (kv[k] & mask) == prefix;
+                const int d = valid ? (int)((kv[k] >> shift) & dmask) : -1;
+                dom_cnt += __popc(__ballot_sync(0xffffffffu, valid && d == dom));
+                if (valid && d != dom) atomicAdd(&hist[d], 1);
+            }
+            if (lane == 0 && dom_cnt) atomicAdd(&hist[dom], dom_cnt);
         }
-        if (take) out[pos++] = i;
+        __syncthreads();
+        FC_SEL_STAMP();
+        int loc[BPT], sum = 0;  // descending digits: thread t owns [2047-BPT*t .. 2047-BPT*t-BPT+1]
+#pragma unroll
+        for (int j = 0; j < BPT; ++j) {
+            loc[j] = hist[kSelBins - 1 - (tid * BPT + j)];
+            sum += loc[j];
+        }
+        int before, tot;
+        Scan(scan_tmp).ExclusiveSum(sum, before, tot);
+        int run = before;
+#pragma unroll
+        for (int j = 0; j < BPT; ++j) {
+            if (run < remaining && run + loc[j] >= remaining) {
+                s_digit = kSelBins - 1 - (tid * BPT + j);
+                s_above = run;
+            }
+            run += loc[j];
+        }
+        __syncthreads();
+        prefix |= (uint32_t)s_digit << shift;
+        mask |= dmask << shift;
+        remaining -= s_above;
+        __syncthreads();  // s_digit / hist reuse
+        FC_SEL_STAMP();
+    }
+    const uint32_t T = prefix;
+    // selection bit-words: warp w's k-th keys are indices (w + k*NT/32)*32 + lane
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+        const bool inr = (tid + k * NT) < n;
+        const unsigned g = __ballot_sync(0xffffffffu, inr && kv[k] > T);
+        const unsigned e = __ballot_sync(0xffffffffu, inr && kv[k] == T);
+        if (lane == 0) {
+            gt_bits[wid + k * (NT / 32)] = g;
+            eq_bits[wid + k * (NT / 32)] = e;
+        }
     }
     __syncthreads();
+    // thread t < NWORDS owns bit-word t (indices 32t .. 32t+31, ascending)
+    static_assert(NWORDS <= NT, "one word per thread");
+    const uint32_t eqw = tid < NWORDS ? eq_bits[tid] : 0u;
+    const int eq_cnt = __popc(eqw);
+    int eq_before, dummy;
+    Scan(scan_tmp).ExclusiveSum(eq_cnt, eq_before, dummy);
+    __syncthreads();
+    int take = max(0, min(eq_cnt, remaining - eq_before));  // lowest-index equal keys
+    uint32_t e = eqw, kept = 0;
+    while (take > 0 && e) {
+        const uint32_t low = e & (~e + 1u);
+        kept |= low;
+        e ^= low;
+        --take;
+    }
+    uint32_t selw = (tid < NWORDS ? gt_bits[tid] : 0u) | kept;
+    int pos, total_sel;
+    Scan(scan_tmp).ExclusiveSum(__popc(selw), pos, total_sel);
+    while (selw) {
+        const int bit = __ffs(selw) - 1;
+        out[pos++] = tid * 32 + bit;
+        selw &= selw - 1;
+    }
+    __syncthreads();
+    FC_SEL_STAMP();
+#ifdef FC_SEL_PROFILE
+    if (tid == 0) for (int k = 1; k < np_; ++k) printf("phase %d: %lld\n", k, tp[k] - tp[k - 1]);
+#endif
+}
+
+template <int NT>
+__device__ void block_select(const uint32_t *keys, int n, int kprime, int32_t *out) {
+    if (n <= NT * 8) block_select_kpt<NT, 8>(keys, n, kprime, out);
+    else block_select_kpt<NT, 32>(keys, n, kprime, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -208,67 +369,132 @@ __device__ void load_group_coeffs(const StoreView &s, const T *q, int b, int h, 
     }
 }
 
-// grid (chunks, batch*H), block kScoreThreads.  do_select = 0: score pages
-// [0, n_pages) of every head; do_select = 1: score [0, n_pages-1) of due heads
-// and select (last page pinned).
+// One wave of CTAs over the concatenation of every scored head's candidate
+// pages (all pages for do_select = 0; pages [0, n_pages-1) of due heads with
+// n_pages > topk for do_select = 1, the last page being pinned).  Each CTA
+// takes an equal contiguous range and walks it head segment by head segment;
+// for do_select the last CTA to finish a head (threadfence reduction) runs
+// the exact selection.  Heads whose budget covers every page are selected
+// directly by CTA 0 (all pages).
 template <typename T, int D>
 __global__ void __launch_bounds__(kScoreThreads)
 score_select_kernel(StoreView s, int layer, const T *__restrict__ q,
                     const uint8_t *__restrict__ unstable, int period, int force_due,
                     int topk, int extra_tokens, float *scores, int32_t *counters,
-                    int do_select, int chunk_pages) {
-    extern __shared__ uint32_t dyn_keys[];
+                    int do_select, int n_heads) {
+    extern __shared__ uint32_t dyn[];  // keys [NCAP] (do_select) | prefix [n_heads+1]
     __shared__ float w[2 * D];
-    __shared__ int s_last;
-    const int bh = blockIdx.y;
-    const int b = bh / s.H, h = bh % s.H;
-    if (do_select) {
-        const bool due = force_due || unstable[layer * s.H + h] || (*s.step % period == 0);
-        if (!due) return;
-    }
-    const int n_tok = s.seq_len[b] + extra_tokens;
-    if (n_tok <= 0) return;
-    const int n_pages = (n_tok + s.PS - 1) / s.PS;
-    const int hx = s.hix(b, layer, h);
-    if (do_select && n_pages <= topk) {  // budget covers every page
-        if (blockIdx.x == 0) {
-            for (int i = threadIdx.x; i < n_pages; i += blockDim.x)
-                s.sel[(int64_t)hx * s.SELCAP + i] = i;
-            if (threadIdx.x == 0) s.n_sel[hx] = n_pages;
+    __shared__ int s_last, s_wsum[kScoreThreads / 32];
+    griddep_launch_dependents();
+    griddep_wait();
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    unsigned long long *trace = g_score_trace;
+    if (trace && tid == 0) trace[blockIdx.x * 4] = gtimer_s();
+    uint32_t *keys = dyn;
+    int *prefix = reinterpret_cast<int *>(dyn + (do_select ? s.NCAP : 0));
+    const int step = *s.step;
+
+    // ---- candidate counts and prefix over heads
+    {
+        int carry = 0;
+        for (int c0 = 0; c0 < n_heads; c0 += blockDim.x) {
+            const int bh = c0 + tid;
+            int cnt = 0;
+            if (bh < n_heads) {
+                const int b = bh / s.H, h = bh % s.H;
+                const int n_tok = s.seq_len[b] + extra_tokens;
+                const int n_pages = n_tok > 0 ? (n_tok + s.PS - 1) / s.PS : 0;
+                if (!do_select) {
+                    cnt = n_pages;
+                } else if (force_due || unstable[layer * s.H + h] || step % period == 0) {
+                    if (n_pages > topk) {
+                        cnt = n_pages - 1;
+                    } else if (blockIdx.x == 0 && n_pages > 0) {  // budget covers every page
+                        const int hx = s.hix(b, layer, h);
+                        for (int i = 0; i < n_pages; ++i) s.sel[(int64_t)hx * s.SELCAP + i] = i;
+                        s.n_sel[hx] = n_pages;
+                    }
+                }
+            }
+            int x = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) s_wsum[wid] = x;
+            __syncthreads();
+            int before = carry, total = 0;
+            for (int ww = 0; ww < kScoreThreads / 32; ++ww) {
+                if (ww < wid) before += s_wsum[ww];
+                total += s_wsum[ww];
+            }
+            if (bh < n_heads) prefix[bh] = before + x - cnt;
+            carry += total;
+            __syncthreads();
         }
-        return;
+        if (tid == 0) prefix[n_heads] = carry;
+        __syncthreads();
     }
-    const int n_cand = do_select ? n_pages - 1 : n_pages;
-    const int n_chunks = (n_cand + chunk_pages - 1) / chunk_pages;
-    if ((int)blockIdx.x >= n_chunks) return;
-    const int p0 = blockIdx.x * chunk_pages;
-    const int p1 = min(n_cand, p0 + chunk_pages);
-    load_group_coeffs<T>(s, q, b, h, w);
-    __syncthreads();
-    float *row = scores + (int64_t)bh * s.NCAP;
-    score_range<T, D>(s, hx, p0, p1, w, row);
-    if (!do_select) return;
-    if (blockIdx.x == 0 && threadIdx.x == 0) row[n_pages - 1] = -INFINITY;  // pinned
-    // last CTA of this head performs the selection
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const int ticket = atomicAdd(&counters[bh], 1);
-        s_last = (ticket == n_chunks - 1);
-        if (s_last) counters[bh] = 0;
+    const int total = prefix[n_heads];
+    if (total == 0) return;
+    using Gm = ScoreGeom<T, D>;
+    constexpr int ALIGN = (kScoreThreads / 32) * Gm::kPagesPerIter;  // one iteration of every warp
+    int P = (total + gridDim.x - 1) / gridDim.x;
+    P = ((P + ALIGN - 1) / ALIGN) * ALIGN;
+    const int start = blockIdx.x * P;
+    if (start >= total) return;
+    const int end = min(total, start + P);
+
+    int pos = start;
+    while (pos < end) {
+        int lo = 0, hi = n_heads - 1;  // head containing pos (last with prefix <= pos)
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (prefix[mid] <= pos) lo = mid; else hi = mid - 1;
+        }
+        const int bh = lo;
+        const int h_beg = prefix[bh], h_end = prefix[bh + 1];
+        const int seg_end = min(end, h_end);
+        const int b = bh / s.H, h = bh % s.H;
+        const int hx = s.hix(b, layer, h);
+        __syncthreads();  // w reuse
+        load_group_coeffs<T>(s, q, b, h, w);
+        __syncthreads();
+        float *row = scores + (int64_t)bh * s.NCAP;
+        score_range<T, D>(s, hx, pos - h_beg, seg_end - h_beg, w, row);
+        pos = seg_end;
+        if (!do_select) continue;
+        // ---- the last CTA of this head selects
+        const int first_c = h_beg / P, last_c = (h_end - 1) / P;
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            const int ticket = atomicAdd(&counters[bh], 1);
+            s_last = (ticket == last_c - first_c);
+            if (s_last) {
+                counters[bh] = 0;
+                __threadfence();
+            }
+        }
+        __syncthreads();
+        if (trace && tid == 0) trace[blockIdx.x * 4 + 1] = gtimer_s();
+        if (!s_last) continue;
+        const int n_cand = h_end - h_beg;
+        const int n_pages = n_cand + 1;
+        for (int i = tid; i < n_cand; i += blockDim.x) keys[i] = score_key(__ldcg(row + i));
+        if (tid == 0) row[n_pages - 1] = -INFINITY;  // pinned page: not scored
+        __syncthreads();
+        const int kprime = topk - 1;  // n_pages > topk, so kprime < n_cand
+        int32_t *out = s.sel + (int64_t)hx * s.SELCAP;
+        if (kprime > 0) block_select<kScoreThreads>(keys, n_cand, kprime, out);
+        if (tid == 0) {
+            out[kprime] = n_pages - 1;
+            s.n_sel[hx] = topk;
+            if (trace) trace[blockIdx.x * 4 + 2] = gtimer_s();
+        }
     }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    for (int i = threadIdx.x; i < n_cand; i += blockDim.x) dyn_keys[i] = score_key(__ldcg(row + i));
-    __syncthreads();
-    const int kprime = topk - 1;  // n_pages > topk here, so kprime < n_cand
-    int32_t *out = s.sel + (int64_t)hx * s.SELCAP;
-    if (kprime > 0) block_select<kScoreThreads>(dyn_keys, n_cand, kprime, out);
-    if (threadIdx.x == 0) {
-        out[kprime] = n_pages - 1;
-        s.n_sel[hx] = topk;
-    }
+    if (trace && tid == 0) trace[blockIdx.x * 4 + 3] = gtimer_s();
 }
 
 // standalone select over caller scores: grid n_heads, block kScoreThreads
@@ -304,24 +530,27 @@ select_topk_kernel(const float *scores, int stride, const int32_t *n_valid, int 
 // ---------------------------------------------------------------------------
 // launchers
 
-static int score_chunk_pages(int n_pages_max) {
-    (void)n_pages_max;
-    return 256;
-}
-
 template <typename T, int D>
 static cudaError_t launch_score_t(const StoreView &s, int layer, const void *q,
                                   const uint8_t *unstable, int period, int force_due, int topk,
                                   int extra, float *scores, int32_t *counters, int do_select,
                                   int batch, cudaStream_t st) {
-    const int chunk = score_chunk_pages(s.NCAP);
-    dim3 grid((s.NCAP + chunk - 1) / chunk, batch * s.H);
-    const size_t smem = do_select ? (size_t)s.NCAP * sizeof(uint32_t) : 0;
+    const int n_heads = batch * s.H;
+    const size_t smem = (do_select ? (size_t)s.NCAP * sizeof(uint32_t) : 0) + (size_t)(n_heads + 1) * sizeof(int);
     auto kern = score_select_kernel<T, D>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, kScoreThreads, smem, st>>>(s, layer, (const T *)q, unstable, period, force_due,
-                                            topk, extra, scores, counters, do_select, chunk);
-    return cudaGetLastError();
+    static size_t cached_smem = (size_t)-1;
+    static int grid = 0;
+    if (cached_smem != smem) {  // one full wave at the occupancy this smem allows
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        int occ = 0, dev = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kScoreThreads, smem);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        grid = (occ < 1 ? 1 : occ) * sms;
+        cached_smem = smem;
+    }
+    return launch_pdl(kern, dim3(grid), dim3(kScoreThreads), smem, st, s, layer, (const T *)q, unstable,
+                      period, force_due, topk, extra, scores, counters, do_select, n_heads);
 }
 
 cudaError_t launch_score(const StoreView &s, int dtype, int layer, const void *q,
@@ -338,12 +567,19 @@ cudaError_t launch_score(const StoreView &s, int dtype, int layer, const void *q
     return launch_score_t<float, 64>(s, layer, q, unstable, period, force_due, topk, extra, scores, counters, do_select, batch, st);
 }
 
+cudaError_t set_score_trace(void *p) {
+    return cudaMemcpyToSymbol(g_score_trace, &p, sizeof(p));
+}
+
 cudaError_t launch_select(const float *scores, int stride, const int32_t *n_valid, int n_heads,
                           int topk, int pin_last, int32_t *sel_out, int32_t *n_out,
                           cudaStream_t st) {
     const size_t smem = (size_t)stride * sizeof(uint32_t);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static bool configured = false;
+    if (!configured) {  // keys up to 8192 (32 KiB) on top of ~12 KiB of static histogram
+        cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        configured = true;
+    }
     select_topk_kernel<<<n_heads, kScoreThreads, smem, st>>>(scores, stride, n_valid, topk, pin_last,
                                                             sel_out, n_out);
     return cudaGetLastError();

@@ -5,19 +5,20 @@ per head in Python (attention.sparsity_error, attention.py:150-159) and
 schedules in its simulator (simulator._decode_step / _append_token / _rerank,
 simulator.py:410-547).  One decode step over L layers is, per layer:
 
-  1. fc_kv_append      write the new token's k/v into its page and fold the
-                       key into that page's min/max summary   (subsystem 1)
-  2. fc_score_select   for due heads only (unstable every step, stable at
+  1. fc_score_select   for due heads only (unstable every step, stable at
                        t % R == 0; layers with no due head are skipped —
                        layer_scoring_skippable, scoring.py:205-209): group
                        page scores + exact top-K with the last page pinned
                        (subsystem 2)
-  3. fc_sparse_decode  GQA split-K attention over sel ∪ pages appended since
-                       the head's last rerank, combine fused  (subsystem 3)
+  2. fc_sparse_decode  GQA split-K attention over sel ∪ pages appended since
+                       the head's last rerank, combine fused (subsystem 3),
+                       with the append fused in: the CTA staging a head's
+                       last page writes the new token's k/v into it and folds
+                       the key into the page's min/max summary (subsystem 1)
 
 then fc_step_advance (seq_len += 1; new pages allocated from the device free
 list).  Steps are replayed from CUDA graphs (one for rerank steps, one for
-plain steps) so the 3·L+1 launches cost no host time.
+plain steps) so the <= 2·L+1 launches cost no host time.
 """
 
 from __future__ import annotations
@@ -55,7 +56,6 @@ class DecodeEngine:
         self.selected = False     # initial selection done (first step forces all heads due)
         self.seq_host = [0] * batch
         self.att_bound = min(pages_cap, topk_pages + self.sel_slack)
-        self.pps = self.store.choose_pages_per_split(batch, self.att_bound)
         # static step buffers (CUDA-graph inputs/outputs)
         Hq = kv_heads * group
         self.q = torch.zeros((layers, batch, Hq, head_dim), dtype=dtype, device=self.device)
@@ -96,12 +96,12 @@ class DecodeEngine:
     def _launch_step(self, rerank: bool, force_due: bool) -> None:
         st = self.store
         for layer in range(self.L):
-            st.append(layer, self.k_new[layer], self.v_new[layer], self.B)
             if force_due or not self._layer_skippable(layer, rerank):
                 st.score_select(layer, self.q[layer], self.unstable, self.R, self.K, self.B,
                                 force_due=force_due, extra_tokens=1)
             st.sparse_decode(layer, self.q[layer], self.out[layer], self.B,
-                             max_pages=self.att_bound, pps=self.pps, extra_tokens=1)
+                             max_pages=self.att_bound, extra_tokens=1, attend_appended=False,
+                             k_new=self.k_new[layer], v_new=self.v_new[layer])
         st.step_advance(self.B)
 
     def _layer_skippable(self, layer: int, rerank: bool) -> bool:
@@ -145,11 +145,11 @@ class DecodeEngine:
 
     def launches_per_step(self, t: int) -> int:
         """Library kernel launches in the step graph for step t: per layer an
-        append and an attention, a scoring launch for every layer with a due
-        head, and the step advance."""
+        attention launch (append fused), a scoring launch for every layer with
+        a due head, and the step advance."""
         rerank = self.is_rerank_step(t)
         scored = sum(not self._layer_skippable(l, rerank) for l in range(self.L))
-        return 2 * self.L + scored + 1
+        return self.L + scored + 1
 
     # -- host-buffer API (end-to-end path) -------------------------------------------
 

@@ -168,31 +168,24 @@ class KVStore:
 
     # -- (3) attention -------------------------------------------------------------
 
-    def choose_pages_per_split(self, batch: int, max_pages: int) -> int:
-        """Pages per CTA so the grid covers ~4 CTAs per SM (148 SMs)."""
-        total = max(1, batch * self.H * max_pages)
-        pps = math.ceil(total / (148 * 4))
-        pps = max(4, min(256, pps))
-        return min(pps, max(1, max_pages))
-
-    def attn_workspace(self, batch: int, max_pages: int, pps: int) -> torch.Tensor:
-        need = self.lib.fc_sparse_decode_workspace_size(self.cptr, batch, max_pages, pps)
+    def attn_workspace(self, batch: int, max_pages: int, n_ctas: int = 0) -> torch.Tensor:
+        need = self.lib.fc_sparse_decode_workspace_size(self.cptr, batch, max_pages, n_ctas)
         if self._attn_ws.numel() < need:
             self._attn_ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
         return self._attn_ws
 
     def sparse_decode(self, layer: int, q: torch.Tensor, out: torch.Tensor, batch: int, *,
-                      max_pages: int, pps: int | None = None, lse: torch.Tensor | None = None,
+                      max_pages: int, n_ctas: int = 0, lse: torch.Tensor | None = None,
                       scale: float | None = None, extra_tokens: int = 1,
-                      attend_appended: bool = True) -> None:
-        if pps is None:
-            pps = self.choose_pages_per_split(batch, max_pages)
-        ws = self.attn_workspace(batch, max_pages, pps)
+                      attend_appended: bool = True, k_new: torch.Tensor | None = None,
+                      v_new: torch.Tensor | None = None) -> None:
+        """Split-K paged attention; with k_new/v_new the decode append is fused."""
+        ws = self.attn_workspace(batch, max_pages, n_ctas)
         scale = 1.0 / math.sqrt(self.D) if scale is None else scale
         _lib.check(self.lib.fc_sparse_decode(
-            self.cptr, layer, q.data_ptr(), out.data_ptr(), _ptr(lse), scale, extra_tokens,
-            int(attend_appended), max_pages, pps, ws.data_ptr(), ws.numel(), batch, self.stream()),
-            "fc_sparse_decode")
+            self.cptr, layer, q.data_ptr(), _ptr(k_new), _ptr(v_new), out.data_ptr(), _ptr(lse),
+            scale, extra_tokens, int(attend_appended), max_pages, n_ctas, ws.data_ptr(),
+            ws.numel(), batch, self.stream()), "fc_sparse_decode")
 
     # -- (4) rerank / tiers ------------------------------------------------------------
 

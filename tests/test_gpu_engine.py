@@ -77,7 +77,9 @@ def run_engine_vs_oracle(*, B, L, H, G, D, T0, steps, K, R, frac, dtype, seed, u
                     assert np.array_equal(summ[b, l, h, :n_pages, 0], mins)
                     assert np.array_equal(summ[b, l, h, :n_pages, 1], maxs)
                     due = first or unstable[l, h] or t % R == 0
-                    gsel = tuple(sel[b, l, h, :n_sel[b, l, h]].tolist())
+                    # the selection row also holds the page the next token opens
+                    # (fc_step_advance appends it); this step attended pages < n_pages
+                    gsel = tuple(p for p in sel[b, l, h, :n_sel[b, l, h]].tolist() if p < n_pages)
                     qs = q[l, b, h * G:(h + 1) * G]
                     if due:
                         # (2) selection: oracle select on oracle scores, tie band
