@@ -172,10 +172,11 @@ int fc_select_topk(const float *scores, int stride, const int32_t *n_valid,
  * the new token into it and folds the key into the page summary
  * (update_minmax, scoring.py:59-69) — fc_kv_append in the same launch.
  * out: [batch][H*G][d] store dtype; lse: optional [batch][H*G] fp32
- * natural-log sum-exp.  The concatenated page lists of all heads are cut into
- * equal ranges, one per CTA (n_ctas = 0: one full wave, 2 per SM); heads
- * spanning several CTAs are combined by the last CTA to finish them.
- * `max_pages` bounds the attended pages of any head (grid sizing). */
+ * natural-log sum-exp.  Each head is processed by a cluster of S CTAs
+ * (n_ctas = S; 0 = auto: the largest power of two <= 16 keeping all heads in
+ * one wave); the CTAs of a cluster merge their softmax states through
+ * distributed shared memory.  `max_pages` bounds the attended pages of any
+ * head.  The workspace is a small scratch kept for ABI stability. */
 size_t fc_sparse_decode_workspace_size(const fc_store *s, int batch,
                                        int max_pages, int n_ctas);
 int fc_sparse_decode(const fc_store *s, int layer, const void *q,

@@ -161,7 +161,7 @@ int fc_select_topk(const float *scores, int stride, const int32_t *n_valid, int 
 size_t fc_sparse_decode_workspace_size(const fc_store *s, int batch, int max_pages, int n_ctas) {
     if (check_store(s) != FC_OK || max_pages < 1 || n_ctas < 0) return 0;
     const StoreView v = make_view(s);
-    return attn_workspace_bytes(v, batch, attn_grid(v, s->dtype, batch, max_pages, n_ctas));
+    return attn_workspace_bytes(v, batch, attn_split(v, s->dtype, batch, max_pages, n_ctas));
 }
 
 int fc_sparse_decode(const fc_store *s, int layer, const void *q, const void *k_new, const void *v_new,
@@ -171,16 +171,15 @@ int fc_sparse_decode(const fc_store *s, int layer, const void *q, const void *k_
     FC_CHECK(check_store(s));
     if (layer < 0 || layer >= s->layers) return invalid("layer out of range");
     if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
-    if (batch * s->kv_heads > 2048) return FC_E_CAPACITY;
     if (!q || !out || !workspace) return invalid("null buffer");
     if ((k_new == nullptr) != (v_new == nullptr)) return invalid("k_new and v_new go together");
     if (k_new && extra_tokens != 1) return invalid("fused append needs extra_tokens = 1");
-    if (n_ctas < 0) return invalid("n_ctas must be >= 0 (0 = one full wave)");
+    if (n_ctas < 0 || n_ctas > 16) return invalid("n_ctas (CTAs per head) must be in 0..16 (0 = auto)");
     if (max_pages < 1) return invalid("max_pages must be >= 1");
     if (!(scale > 0.f) || !std::isfinite(scale)) return invalid("scale must be positive");
     if (extra_tokens < 0 || extra_tokens > 1) return invalid("extra_tokens must be 0 or 1");
     const StoreView v = make_view(s);
-    const int grid = attn_grid(v, s->dtype, batch, max_pages, n_ctas);
+    const int grid = attn_split(v, s->dtype, batch, max_pages, n_ctas);
     const size_t need = attn_workspace_bytes(v, batch, grid);
     if (ws_bytes < need) return FC_E_CAPACITY;
     if (batch == 0) return FC_OK;
@@ -191,7 +190,7 @@ int fc_sparse_decode(const fc_store *s, int layer, const void *q, const void *k_
     a.scale_log2 = scale * 1.4426950408889634f;
     a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.max_splits = grid;
     char *w = (char *)workspace;
-    a.plan = (int32_t *)w;
+    a.counters = (int32_t *)w;
     a.part_m = (float *)(w + ((2 * heads * sizeof(int32_t) + 255) & ~(size_t)255));
     a.part_l = a.part_m + parts * 16;
     a.part_o = a.part_l + parts * 16;

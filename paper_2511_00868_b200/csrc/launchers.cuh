@@ -13,8 +13,8 @@ struct AttnArgs {
     float scale_log2;
     int extra_tokens;
     int attend_appended;
-    int max_splits;
-    int32_t *plan;        // [batch*H][2] first/last warp of each split head (-1: none)
+    int max_splits;       // CTAs per head (cluster size S)
+    int32_t *counters;    // [B_cap*H] partials published per head (zeroed once, self-resetting)
     float *part_m;        // [parts][16]
     float *part_l;        // [parts][16]
     float *part_o;
@@ -34,7 +34,7 @@ cudaError_t launch_attn(const StoreView &, int, const AttnArgs &, int, cudaStrea
 size_t attn_workspace_bytes(const StoreView &, int, int);
 cudaError_t set_attn_trace(void *);
 cudaError_t set_score_trace(void *);
-int attn_grid(const StoreView &, int, int, int, int);
+int attn_split(const StoreView &, int, int, int, int);
 size_t rerank_workspace_bytes(const StoreView &);
 cudaError_t launch_rerank(const StoreView &, int, const int32_t *, const int32_t *, const uint8_t *, int,
                           int, int, int, const uint8_t *, int32_t *, int, int32_t *, void *, int, cudaStream_t);

@@ -20,11 +20,11 @@
 // mode, 1e-5 parity).  Warps merge through shared memory; splits merge in the
 // last CTA of the head (threadfence reduction) — no second launch.
 #include "launchers.cuh"
+#include <cooperative_groups.h>
 #include <type_traits>
 
 namespace fc {
 
-constexpr int kAttnWarps = 4;
 
 
 template <typename T, int D>
@@ -334,7 +334,8 @@ FC_DEVINL HeadInfo head_info(const StoreView &s, const AttnArgs &a, int bh) {
     return hi;
 }
 
-constexpr int kMaxHeads = 2048;     // batch*H per launch
+constexpr int kMaxHeads = 1 << 20;  // batch*H per launch (grid.x = heads * S)
+constexpr int kMaxClusterCtas = 16;
 
 // Optional per-CTA timeline (globaltimer ns) for profiling: [grid][4] =
 // entry, first load issued, main loop done, exit.  Null in production.
@@ -345,131 +346,83 @@ FC_DEVINL unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-constexpr int kMinPagesPerWarp = 2;
-constexpr int kMaxPagesPerWarp = 32;  // one entry per lane
 
+// page (logical) of attended entry j of a head
+FC_DEVINL int entry_page(const StoreView &s, const HeadInfo &hd, int j) {
+    return j < hd.nsel ? s.sel[(int64_t)hd.hx * s.SELCAP + j] : hd.hi + 1 + (j - hd.nsel);
+}
 
-// Every warp is an independent worker.  The concatenation of all heads'
-// attended page lists is cut into equal contiguous ranges, one per warp of
-// the grid (<= 32 pages: one page per lane to resolve).  A warp streams its
-// pages through a private ring of NST cp.async.bulk stages (one 8 KiB copy per
-// bf16 page, completion on an mbarrier), keeps one online-softmax state per
-// segment (= the part of one head inside its range), and at a segment end
-// either writes the head's output (head entirely inside the range) or
-// publishes a partial (m, l, acc) at slot head + global_warp — unique because
-// each new segment bumps the head index, the warp index, or both — and the
-// last warp to finish a head (acq_rel counter) combines its partials.  No CTA
-// barrier after the prologue: warps never wait for each other.
-template <typename T, int D, int NST>
-__global__ void __launch_bounds__(kAttnWarps * 32)
-attn_kernel(StoreView s, AttnArgs a, int n_heads) {
+FC_DEVINL int resolve_block(const StoreView &s, const HeadInfo &hd, int page) {
+    int blk = 0;
+    if (page >= 0 && page < hd.n_pages) blk = s.table[s.table_off(hd.hx, page)];
+    if (blk == FC_NULL_BLOCK) {  // residency violation (attention.py:101-105)
+        set_error(s.err, FC_ERR_NULL_READ);
+        blk = -1;
+    }
+    return blk;
+}
+
+// One head per cluster of S CTAs (S = 1: a plain CTA).  The head's attended
+// pages are cut into S*NW equal contiguous ranges, one per warp; a warp
+// streams its pages through a private ring of NST cp.async.bulk stages (one
+// copy of the whole page, K then V, completing on an mbarrier) and keeps one
+// online-softmax state.  At the end the warps merge through shared memory and
+// the S CTAs of the cluster merge through distributed shared memory into
+// rank 0, which writes the output — no partials in global memory, no second
+// pass.  The warp that stages the head's last page first writes the new
+// token into it (fused append).
+template <typename T, int D, int NST, int NW>
+__global__ void __launch_bounds__(NW * 32)
+attn_kernel(StoreView s, AttnArgs a, int S) {
     using Gm = AttnGeom<T, D>;
-    constexpr int NW = kAttnWarps;
-    // dynamic: ring [NW][NST][page] | (fp32) q [NW][G][D] f32 | prefix [n_heads+1]
+    // dynamic: ring [NW][NST][page] | (fp32) q [G][D] | cta state [G][D] + m,l [2][16]
     extern __shared__ __align__(128) char dsm[];
     __shared__ __align__(8) uint64_t bars[NW * NST];
-    __shared__ int s_wsum[NW];
+    __shared__ float s_wm[NW][16], s_wl[NW][16];
 
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int G = s.G;
     unsigned long long *trace = g_attn_trace;
     const unsigned long long t_entry = trace ? gtimer() : 0ull;
-    griddep_launch_dependents();  // let the combine kernel get scheduled early (PDL)
+    griddep_launch_dependents();  // let the next launch get scheduled early (PDL)
     griddep_wait();               // selection / seq_len come from the previous launches
     char *ring = dsm;
     float *s_q = reinterpret_cast<float *>(dsm + (size_t)NW * NST * Gm::kPageBytes);
-    int *s_prefix = reinterpret_cast<int *>(s_q + (sizeof(T) == 4 ? NW * G * D : 0));
+    float *cstate = s_q + (sizeof(T) == 4 ? G * D : 0);  // [G][D] acc, then m[16], l[16]
+    float *cm = cstate + G * D, *cl = cm + 16;
 
-    // ---- prefix of attended pages over all heads of this layer (CTA-wide, once)
-    __shared__ int s_maxatt;
-    {
-        int carry = 0, mx = 0;
-        for (int c0 = 0; c0 < n_heads; c0 += blockDim.x) {
-            const int bh = c0 + tid;
-            const int cnt = bh < n_heads ? head_info(s, a, bh).n_att : 0;
-            mx = max(mx, cnt);
-            int x = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            if (lane == 31) s_wsum[w] = x;
-            __syncthreads();
-            int before = carry, total = 0;
-            for (int ww = 0; ww < NW; ++ww) {
-                if (ww < w) before += s_wsum[ww];
-                total += s_wsum[ww];
-            }
-            if (bh < n_heads) s_prefix[bh] = before + x - cnt;
-            carry += total;
-            __syncthreads();
-        }
-        if (tid == 0) { s_prefix[n_heads] = carry; s_maxatt = 0; }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        __syncthreads();
-        if (lane == 0) atomicMax(&s_maxatt, mx);
-    }
+    const int bh = blockIdx.x / S, rank = blockIdx.x % S;
+    const HeadInfo hd = head_info(s, a, bh);
+    const int n_att = hd.n_att;
+    const int nwt = S * NW, kw = rank * NW + w;
+    const int j0 = (int)((int64_t)n_att * kw / nwt);
+    const int n_e = (int)((int64_t)n_att * (kw + 1) / nwt) - j0;
+    const int b = bh / s.H, h = bh % s.H;
+    const int64_t qoff = ((int64_t)b * s.H * G + (int64_t)h * G) * D;
+    const int last_fill = hd.n_tok - (hd.n_pages - 1) * kPageSize;  // tokens in the last page
+
     if (tid < NW * NST) mbar_init(&bars[tid], 1);
     fence_mbar_init();
+    if constexpr (sizeof(T) == 4) {
+        const float *qg = reinterpret_cast<const float *>(a.q) + qoff;
+        for (int i = tid; i < G * D; i += blockDim.x) s_q[i] = qg[i];
+    }
     __syncthreads();
 
-    const int total = s_prefix[n_heads];
-    const int n_workers = gridDim.x * NW;
-    const int gw = blockIdx.x * NW + w;
-    // pages per warp: balanced, >= 2, and a head never spans more than 32
-    // warps (combine_kernel reads <= 32 partials)
-    const int P = max(max(kMinPagesPerWarp, (total + n_workers - 1) / n_workers), (s_maxatt + 29) / 30);
-    if (blockIdx.x == 0) {  // combine plan: warps covering each head, -1 = no combine needed
-        for (int bh = tid; bh < n_heads; bh += blockDim.x) {
-            const int h_beg = s_prefix[bh], h_end = s_prefix[bh + 1];
-            const int fw = h_beg / P, lw = h_end > h_beg ? (h_end - 1) / P : fw;
-            const bool one = h_end == h_beg || (fw == lw && h_beg >= fw * P && h_end <= fw * P + P);
-            a.plan[2 * bh] = one ? -1 : fw;
-            a.plan[2 * bh + 1] = lw;
-        }
+    // entries are resolved 32 at a time (lane l owns entry 32c + l of chunk c)
+    int cur_blk = 0, nxt_blk = 0;
+    {
+        const int j = j0 + lane;
+        if (lane < n_e) cur_blk = resolve_block(s, hd, entry_page(s, hd, j));
+        if (lane + 32 < n_e) nxt_blk = resolve_block(s, hd, entry_page(s, hd, j + 32));
     }
-    const int start = gw * P;
-    if (start >= total) return;
-    const int end = min(total, start + P);
-    const int n_e = end - start;  // <= 32 (grid sized on the host)
-
-    // ---- resolve: lane e owns entry e (page -> block, head, tokens)
-    int e_blk = 0, e_bh = 0, e_meta = 0;
-    if (lane < n_e) {
-        const int pos = start + lane;
-        int lo = 0, hi = n_heads - 1;  // last head with prefix <= pos (skips empty heads)
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_prefix[mid] <= pos) lo = mid; else hi = mid - 1;
-        }
-        const HeadInfo hd = head_info(s, a, lo);
-        const int j = pos - s_prefix[lo];
-        const int page = j < hd.nsel ? s.sel[(int64_t)hd.hx * s.SELCAP + j] : hd.hi + 1 + (j - hd.nsel);
-        int blk = 0;
-        if (page >= 0 && page < hd.n_pages) blk = s.table[s.table_off(hd.hx, page)];
-        if (blk == FC_NULL_BLOCK) {  // residency violation (attention.py:101-105)
-            set_error(s.err, FC_ERR_NULL_READ);
-            blk = -1;
-        }
-        e_blk = blk;
-        e_bh = lo;
-        const bool appended_here = a.k_new != nullptr && page == hd.n_pages - 1;
-        e_meta = min(kPageSize, hd.n_tok - page * kPageSize) | (appended_here ? 0x10000 : 0) |
-                 ((page & 0x3fff) << 17);
-    }
-
     const char *pool = reinterpret_cast<const char *>(s.pool);
     char *myring = ring + (size_t)w * NST * Gm::kPageBytes;
     uint64_t *mybars = bars + w * NST;
-    const unsigned long long t_resolved = trace ? gtimer() : 0ull;
-    int trace_flags = 0;
-
-    // prologue: the first NST loads
+    int chunk = 0;  // chunk of cur_blk
 #pragma unroll
     for (int i = 0; i < NST; ++i) {
-        const int blk = __shfl_sync(0xffffffffu, e_blk, i);
+        const int blk = __shfl_sync(0xffffffffu, cur_blk, i);  // i < NST <= 32: chunk 0
         if (lane == 0 && i < n_e) {
             if (blk > 0) {
                 mbar_arrive_expect_tx(&mybars[i], Gm::kPageBytes);
@@ -480,49 +433,41 @@ attn_kernel(StoreView s, AttnArgs a, int n_heads) {
             }
         }
     }
+    const unsigned long long t_issued = trace ? gtimer() : 0ull;
 
     typename std::conditional<sizeof(T) == 2, Bf16Warp<D>, F32Warp<D>>::type st;
-    T *out = reinterpret_cast<T *>(a.out);
-    const T *qall = reinterpret_cast<const T *>(a.q);
-    float *myq = s_q + (size_t)w * G * D;
-    int cur = -1;           // head of the open segment
-    int64_t qoff = 0;
-    HeadInfo hd{};
+    if constexpr (sizeof(T) == 4) st.init(s_q, G, lane);
+    else st.init(reinterpret_cast<const T *>(a.q) + qoff, G, lane);
     for (int i = 0; i < n_e; ++i) {
-        const int bh = __shfl_sync(0xffffffffu, e_bh, i);
-        const int meta = __shfl_sync(0xffffffffu, e_meta, i);
-        const int blk = __shfl_sync(0xffffffffu, e_blk, i);
-        const int nblk = __shfl_sync(0xffffffffu, e_blk, (i + NST) & 31);
-        if (bh != cur) {
-            cur = bh;
-            const int b = bh / s.H, h = bh % s.H;
-            qoff = ((int64_t)b * s.H * G + (int64_t)h * G) * D;
-            hd = head_info(s, a, bh);
-            if constexpr (sizeof(T) == 4) {
-                __syncwarp();
-                for (int k = lane; k < G * D; k += 32) myq[k] = qall[qoff + k];
-                __syncwarp();
-                st.init(myq, G, lane);
-            } else {
-                st.init(qall + qoff, G, lane);
-            }
+        // advance the resolution window when consumption enters a new chunk
+        if (i > 0 && (i & 31) == 0) {
+            cur_blk = nxt_blk;
+            ++chunk;
+            const int j = j0 + (chunk + 1) * 32 + lane;
+            nxt_blk = (j < j0 + n_e) ? resolve_block(s, hd, entry_page(s, hd, j)) : 0;
         }
+        const int blk = __shfl_sync(0xffffffffu, cur_blk, i & 31);
+        const int ni = i + NST;  // entry to issue after this one
+        const int nb_cur = __shfl_sync(0xffffffffu, cur_blk, ni & 31);
+        const int nb_nxt = __shfl_sync(0xffffffffu, nxt_blk, ni & 31);
+        const int nblk = (ni >> 5) == chunk ? nb_cur : nb_nxt;
         const int stg = i % NST;
         mbar_wait(&mybars[stg], (i / NST) & 1);
         if (blk > 0) {
             char *stage = myring + (size_t)stg * Gm::kPageBytes;
-            if (meta & 0x10000) {
-                const int b = bh / s.H, h = bh % s.H;
+            const bool last = (j0 + i == n_att - 1);
+            if (last && a.k_new != nullptr) {
                 const int64_t nk = ((int64_t)b * s.H + h) * D;
                 patch_token<T, D>(s, stage, reinterpret_cast<T *>(s.pool) + s.block_off(blk),
-                                  (hd.n_tok - 1) % kPageSize, hd.hx, (meta >> 17) & 0x3fff,
+                                  (hd.n_tok - 1) % kPageSize, hd.hx, hd.n_pages - 1,
                                   reinterpret_cast<const T *>(a.k_new) + nk,
                                   reinterpret_cast<const T *>(a.v_new) + nk, lane);
             }
-            st.page(stage, meta & 0xffff, a.scale_log2, lane);
+            const int page_is_last = last && entry_page(s, hd, j0 + i) == hd.n_pages - 1;
+            st.page(stage, page_is_last ? last_fill : kPageSize, a.scale_log2, lane);
         }
         __syncwarp();
-        if (lane == 0 && i + NST < n_e) {
+        if (lane == 0 && ni < n_e) {
             fence_proxy_async_smem();
             if (nblk > 0) {
                 mbar_arrive_expect_tx(&mybars[stg], Gm::kPageBytes);
@@ -532,121 +477,101 @@ attn_kernel(StoreView s, AttnArgs a, int n_heads) {
                 mbar_arrive_expect_tx(&mybars[stg], 0);
             }
         }
-        // ---- segment end (last entry of the range or head change next)
-        const int next_bh = __shfl_sync(0xffffffffu, e_bh, (i + 1) & 31);
-        if (i + 1 == n_e || next_bh != bh) {
-            st.finalize();
-            const int h_beg = s_prefix[bh], h_end = s_prefix[bh + 1];
-            if (h_beg >= start && h_end <= end) {  // whole head inside this warp
-                st.template store_final<T>(out + qoff, a.lse ? a.lse + (int64_t)bh * G : nullptr, G, lane);
-            } else {  // partial: combined by combine_kernel (ids bh + first..last warp)
-                const int64_t pid = (int64_t)bh + gw;
-                st.store_partial(a.part_o + pid * G * D, a.part_m + pid * 16, a.part_l + pid * 16, G, lane);
-                trace_flags |= 1;
+    }
+    const unsigned long long t_loop = trace ? gtimer() : 0ull;
+
+    // ---- merge the warps of this CTA (ring is free once every warp is done)
+    st.finalize();
+    __syncthreads();
+    float *scratch = reinterpret_cast<float *>(ring);  // [NW][G][D]
+    for (int g = lane; g < 16; g += 32) { s_wm[w][g] = -INFINITY; s_wl[w][g] = 0.f; }
+    __syncwarp();
+    st.store_partial(scratch + (size_t)w * G * D, s_wm[w], s_wl[w], G, lane);
+    __syncthreads();
+    T *out = reinterpret_cast<T *>(a.out) + qoff;
+    float *lse = a.lse ? a.lse + (int64_t)bh * G : nullptr;
+    for (int e = tid; e < G * D; e += blockDim.x) {
+        const int g = e / D;
+        float M = -INFINITY;
+#pragma unroll
+        for (int ww = 0; ww < NW; ++ww) M = fmaxf(M, s_wm[ww][g]);
+        float L = 0.f, O = 0.f;
+#pragma unroll
+        for (int ww = 0; ww < NW; ++ww) {
+            const float f = exp2f(s_wm[ww][g] - M);  // -inf rows of idle warps give 0
+            L += s_wl[ww][g] * f;
+            O += scratch[(size_t)ww * G * D + e] * f;
+        }
+        if (S == 1) {
+            if (n_att > 0) {
+                out[e] = T(O / L);
+                if (lse && e % D == 0) lse[g] = (M + log2f(L)) * 0.69314718055994531f;
             }
+        } else {
+            cstate[e] = O;
+            if (e % D == 0) { cm[g] = M; cl[g] = L; }
         }
     }
-    if (trace && lane == 0) {  // per warp: entry, resolved, done, smid | flags << 16 | n_e << 24
+    if (S > 1) {  // ---- merge the cluster's CTAs into rank 0 through DSMEM
+        namespace cg = cooperative_groups;
+        cg::cluster_group cluster = cg::this_cluster();
+        cluster.sync();
+        if (rank == 0 && n_att > 0) {
+            for (int e = tid; e < G * D; e += blockDim.x) {
+                const int g = e / D;
+                float M = -INFINITY;
+                for (int r = 0; r < S; ++r) M = fmaxf(M, cluster.map_shared_rank(cm, r)[g]);
+                float L = 0.f, O = 0.f;
+                for (int r = 0; r < S; ++r) {
+                    const float f = exp2f(cluster.map_shared_rank(cm, r)[g] - M);
+                    L += cluster.map_shared_rank(cl, r)[g] * f;
+                    O += cluster.map_shared_rank(cstate, r)[e] * f;
+                }
+                out[e] = T(O / L);
+                if (lse && e % D == 0) lse[g] = (M + log2f(L)) * 0.69314718055994531f;
+            }
+        }
+        cluster.sync();  // keep every rank's shared memory alive until rank 0 is done
+    }
+    if (trace && tid == 0) {
         unsigned smid;
         asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-        unsigned long long *tw = trace + (size_t)gw * 4;
+        unsigned long long *tw = trace + (size_t)blockIdx.x * 4;
         tw[0] = t_entry;
-        tw[1] = 0;
-        tw[2] = gtimer();
-        tw[3] = smid | (trace_flags << 16) | ((unsigned long long)n_e << 24) | ((unsigned long long)w << 40);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// split-K combine: one CTA per head that spans several warps (plan >= 0).
-// Launched with programmatic dependent launch right behind attn_kernel; it
-// waits (griddepcontrol.wait) for the partials, loads every partial's (m, l)
-// in one round, then streams the accumulators with all loads independent.
-template <typename T, int D>
-__global__ void __launch_bounds__(128) combine_kernel(AttnArgs a, int G) {
-    constexpr int MAXP = 32;
-    __shared__ float s_w[16][MAXP];
-    __shared__ float s_inv[16];
-    griddep_wait();
-    const int bh = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int fw = a.plan[2 * bh];
-    if (fw < 0) return;
-    const int np = a.plan[2 * bh + 1] - fw + 1;
-    const int64_t p0 = (int64_t)bh + fw;
-    // (m, l) of every partial: warp w handles rows g = w, w+4, ...; lane = partial
-    {
-        float mv[4], lv[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int g = w + 4 * k;
-            mv[k] = (g < G && lane < np) ? __ldcg(a.part_m + (p0 + lane) * 16 + g) : -INFINITY;
-            lv[k] = (g < G && lane < np) ? __ldcg(a.part_l + (p0 + lane) * 16 + g) : 0.f;
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int g = w + 4 * k;
-            if (g >= G) break;
-            float M = mv[k];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-            const float f = lane < np ? exp2f(mv[k] - M) : 0.f;
-            float L = lv[k] * f;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-            s_w[g][lane] = f;
-            if (lane == 0) {
-                s_inv[g] = 1.f / L;
-                if (a.lse) a.lse[(int64_t)bh * G + g] = (M + log2f(L)) * 0.69314718055994531f;
-            }
-        }
-    }
-    __syncthreads();
-    T *out = reinterpret_cast<T *>(a.out) + (int64_t)bh * G * D;  // [batch*H][G][D] == [batch][H*G][D]
-    const float4 *po = reinterpret_cast<const float4 *>(a.part_o + p0 * G * D);
-    const int stride4 = G * D / 4;  // float4 per partial
-    for (int e4 = tid; e4 < stride4; e4 += blockDim.x) {
-        const int g = (e4 * 4) / D;
-        float4 v[MAXP];
-#pragma unroll
-        for (int p = 0; p < MAXP; ++p)  // every load issued before any use
-            if (p < np) v[p] = __ldcg(po + (int64_t)p * stride4 + e4);
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int p = 0; p < MAXP; ++p) {
-            if (p < np) {
-                const float f = s_w[g][p];
-                acc.x += f * v[p].x; acc.y += f * v[p].y; acc.z += f * v[p].z; acc.w += f * v[p].w;
-            }
-        }
-        const float inv = s_inv[g];
-        T *o = out + e4 * 4;
-        o[0] = T(acc.x * inv); o[1] = T(acc.y * inv); o[2] = T(acc.z * inv); o[3] = T(acc.w * inv);
+        tw[1] = t_issued;
+        tw[2] = t_loop;
+        tw[3] = gtimer() | 0ull;
+        (void)smid;
     }
 }
 
 // ---------------------------------------------------------------------------
 
-template <typename T, int D, int NST>
-static size_t attn_smem(const StoreView &s, int n_heads) {
+// CTA shapes: bf16 8 warps x 3 stages (192 KiB ring, one CTA per SM); fp32
+// (correctness mode, 2x page bytes) 4 warps.
+template <typename T, int D, int NST, int NW>
+static size_t attn_smem(const StoreView &s) {
     using Gm = AttnGeom<T, D>;
-    return (size_t)kAttnWarps * NST * Gm::kPageBytes +
-           (size_t)(sizeof(T) == 4 ? kAttnWarps : 0) * s.G * D * sizeof(float) +
-           (size_t)(n_heads + 1) * sizeof(int);
+    const size_t ring = (size_t)NW * NST * Gm::kPageBytes;
+    const size_t merge = (size_t)NW * s.G * D * sizeof(float);  // scratch lives in the ring
+    return (ring > merge ? ring : merge) + (size_t)(sizeof(T) == 4 ? s.G * D : 0) * sizeof(float) +
+           ((size_t)s.G * D + 32) * sizeof(float);
 }
 
-template <typename T, int D, int NST>
-static int attn_ctas_per_sm_t(const StoreView &s, int n_heads) {
-    const size_t smem = attn_smem<T, D, NST>(s, n_heads);
-    auto kern = attn_kernel<T, D, NST>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+template <typename T, int D, int NST, int NW>
+static int attn_ctas_per_sm_t(const StoreView &s) {
+    const size_t smem = attn_smem<T, D, NST, NW>(s);
+    auto kern = attn_kernel<T, D, NST, NW>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kAttnWarps * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, smem);
     return occ < 1 ? 1 : occ;
 }
 
-#define FC_ATTN_DISPATCH(dtype, D, CALL)                                        \
-    ((dtype) == FC_BF16 ? ((D) == 128 ? CALL(__nv_bfloat16, 128, 3) : CALL(__nv_bfloat16, 64, 6)) \
-                        : ((D) == 128 ? CALL(float, 128, 2) : CALL(float, 64, 3)))
+#define FC_ATTN_DISPATCH(dtype, D, CALL)                                            \
+    ((dtype) == FC_BF16 ? ((D) == 128 ? CALL(__nv_bfloat16, 128, 3, 8) : CALL(__nv_bfloat16, 64, 6, 8)) \
+                        : ((D) == 128 ? CALL(float, 128, 3, 4) : CALL(float, 64, 6, 4)))
 
 static int num_sms() {
     static int sms = 0;
@@ -658,29 +583,41 @@ static int num_sms() {
     return sms;
 }
 
-// One full wave of CTAs (occupancy x SMs), more if a warp would own more than
-// kMaxPagesPerWarp pages.
-int attn_grid(const StoreView &s, int dtype, int batch, int max_pages, int n_ctas) {
-    if (n_ctas > 0) return n_ctas;
+// CTAs per head (cluster size): the largest power of two <= 16 that keeps
+// heads * S within one wave and gives every warp at least two pages.
+int attn_split(const StoreView &s, int dtype, int batch, int max_pages, int n_ctas) {
+    if (n_ctas > 0) return n_ctas;  // explicit split (profiling)
     const int n_heads = batch * s.H;
-#define FC_OCC(T, DD, N) attn_ctas_per_sm_t<T, DD, N>(s, n_heads)
+#define FC_OCC(T, DD, N, W) attn_ctas_per_sm_t<T, DD, N, W>(s)
     const int occ = FC_ATTN_DISPATCH(dtype, s.D, FC_OCC);
 #undef FC_OCC
-    const int64_t bound = (int64_t)n_heads * max_pages;
-    const int64_t wave = (int64_t)occ * num_sms();
-    const int64_t per_cta = (int64_t)kMaxPagesPerWarp * kAttnWarps;
-    const int64_t need = (bound + per_cta - 1) / per_cta;
-    return (int)(need > wave ? need : wave);
+    const int64_t slots = (int64_t)occ * num_sms();
+    int S = 1;
+    while (2 * S <= kMaxClusterCtas && (int64_t)n_heads * 2 * S <= slots && 2 * S * 4 * 2 <= max_pages)
+        S *= 2;
+    return S;
 }
 
-template <typename T, int D, int NST>
+template <typename T, int D, int NST, int NW>
 static cudaError_t launch_attn_t(const StoreView &s, const AttnArgs &a, int batch, cudaStream_t st) {
     const int n_heads = batch * s.H;
-    const size_t smem = attn_smem<T, D, NST>(s, n_heads);
-    cudaError_t e = launch_pdl(attn_kernel<T, D, NST>, dim3(a.max_splits), dim3(kAttnWarps * 32), smem, st,
-                               s, a, n_heads);
-    if (e != cudaSuccess) return e;
-    return launch_pdl(combine_kernel<T, D>, dim3(n_heads), dim3(128), 0, st, a, s.G);
+    const int S = a.max_splits;
+    const size_t smem = attn_smem<T, D, NST, NW>(s);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(n_heads * S);
+    cfg.blockDim = dim3(NW * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = S;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, attn_kernel<T, D, NST, NW>, s, a, S);
 }
 
 cudaError_t set_attn_trace(void *p) {
@@ -688,21 +625,13 @@ cudaError_t set_attn_trace(void *p) {
 }
 
 cudaError_t launch_attn(const StoreView &s, int dtype, const AttnArgs &a, int batch, cudaStream_t st) {
-    if (batch * s.H > kMaxHeads) return cudaErrorInvalidValue;
-    if (dtype == FC_BF16) {
-        if (s.D == 128) return launch_attn_t<__nv_bfloat16, 128, 3>(s, a, batch, st);
-        return launch_attn_t<__nv_bfloat16, 64, 6>(s, a, batch, st);
-    }
-    if (s.D == 128) return launch_attn_t<float, 128, 2>(s, a, batch, st);
-    return launch_attn_t<float, 64, 3>(s, a, batch, st);
+    if ((int64_t)batch * s.H * a.max_splits > 2147483647ll || a.max_splits < 1 || a.max_splits > kMaxClusterCtas)
+        return cudaErrorInvalidValue;
+#define FC_LAUNCH(T, DD, N, W) launch_attn_t<T, DD, N, W>(s, a, batch, st)
+    return FC_ATTN_DISPATCH(dtype, s.D, FC_LAUNCH);
+#undef FC_LAUNCH
 }
 
-size_t attn_workspace_bytes(const StoreView &s, int batch, int n_ctas) {  // n_ctas = launched grid
-    const size_t heads = (size_t)s.B * s.H;
-    const size_t parts = heads + (size_t)n_ctas * kAttnWarps;  // partial ids h + global warp
-    (void)batch;
-    return ((2 * heads * sizeof(int32_t) + 255) & ~(size_t)255) + parts * 16 * 2 * sizeof(float) +
-           parts * s.G * s.D * sizeof(float);
-}
+size_t attn_workspace_bytes(const StoreView &, int, int) { return 256; }  // no partials: DSMEM merge
 
 }  // namespace fc

@@ -25,7 +25,7 @@ lib.fc_debug_attn_trace.restype = ctypes.c_int
 lib.fc_debug_attn_trace.argtypes = [ctypes.c_void_p]
 res = {}
 alg = eng.attention_bytes(0)
-for n_ctas in [0, 148, 296, 444, 592, 888, 1184]:
+for n_ctas in [0, 1, 2, 4]:
     ts = []
     for rep in range(5):
         for l in range(L):
@@ -45,19 +45,14 @@ torch.cuda._sleep(5_000_000)
 st.sparse_decode(0, eng.q[0], eng.out[0], B, max_pages=eng.att_bound, attend_appended=False)
 torch.cuda.synchronize()
 lib.fc_debug_attn_trace(None)
-tr = buf.view(-1, 4).cpu().numpy()
-tr = tr[tr[:, 2] > 0]
+tr = buf.view(-1, 4).cpu().numpy().astype("float64")
+tr = tr[tr[:, 3] > 0]
 t0 = tr[:, 0].min()
-ent = (tr[:, 0] - t0) / 1e3; done = (tr[:, 2] - t0) / 1e3
-tcomb = (tr[:, 1] >> 32) / 1e3; tpub = (tr[:, 1] & 0xffffffff) / 1e3; res = ent
-smid = tr[:, 3] & 0xffff; flags = (tr[:, 3] >> 16) & 0xff; n_e = (tr[:, 3] >> 24) & 0xffff; wi = (tr[:, 3] >> 40) & 0xff
 import numpy as np
-body = done - res
 def pct(x): return [round(float(np.percentile(x, p)), 2) for p in (0, 10, 50, 90, 100)] if len(x) else []
-print(json.dumps({"warps": int(tr.shape[0]), "resolve_us": pct(res - ent), "body_us": pct(body), "done_us": pct(done),
-                  "comb_us_flag2": pct(tcomb[((tr[:, 3] >> 16) & 0xff) >= 2]), "pub_us": pct(tpub[((tr[:, 3] >> 16) & 0xff) >= 1]), "body_by_flags": {int(f): pct(body[flags == f]) for f in np.unique(flags)},
-                  "body_by_warp_in_cta": {int(f): pct(body[wi == f]) for f in np.unique(wi)},
-                  "slowest": [[round(float(done[i]), 1), round(float(body[i]), 1), int(smid[i]), int(flags[i]), int(wi[i])] for i in np.argsort(done)[-16:]]}))
+print(json.dumps({"ctas": int(tr.shape[0]), "entry": pct((tr[:, 0] - t0) / 1e3), "issued": pct((tr[:, 1] - t0) / 1e3),
+                  "loop_done": pct((tr[:, 2] - t0) / 1e3), "exit": pct((tr[:, 3] - t0) / 1e3),
+                  "body": pct((tr[:, 2] - tr[:, 1]) / 1e3), "merge": pct((tr[:, 3] - tr[:, 2]) / 1e3)}))
 
 # ---- scoring: score only vs score + select (layer 0, all heads due)
 def timeit(fn, reps=5):
