@@ -1,0 +1,105 @@
+"""Two-tier page placement — the reference's ``tierkv.tiering`` semantics
+(tiering.py:42-184) with real data movement.
+
+The slow tier is pinned host memory ``[B, L, H, N_cap, page]`` (same in-page
+layout as the HBM pool); pages move with zero-copy UVA kernels
+(fc_offload_pages: HBM -> host, fc_fetch_pages: host -> HBM over a copy list
+produced by fc_rerank_recycle), on whatever stream the caller uses (a side
+stream overlapped with decode, ordered by CUDA events).  The write-once
+offload ledger, stable-only rule and capacity check follow the reference:
+every full page of a stable head is written exactly once (tiering.py:99-157),
+unstable heads never offload or reload (:146-148, :164-166).  The
+latency/bandwidth cost model (tiering.py:29-39) is replaced by measurement.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from .config import HeadId
+from .errors import AdmissionError, ConsistencyError
+from .store import PAGE_SIZE, KVStore
+
+
+def promoted_delta(old_topk, new_topk) -> tuple:
+    """Pages entering the selection, i.e. the ones that need a reload (tiering.py:42-46)."""
+    old = {int(p) for p in getattr(old_topk, "pages", old_topk)}
+    new = {int(p) for p in getattr(new_topk, "pages", new_topk)}
+    return tuple(sorted(new - old))
+
+
+class TierStore:
+    """Pinned-host slow tier + write-once ledger for one KVStore."""
+
+    def __init__(self, store: KVStore, profile, capacity_bytes: int | None = None):
+        self.store = store
+        self.profile = profile
+        self.page_bytes = store.page_bytes
+        cap_pages = store.B * store.L * store.H * store.NCAP
+        self.capacity_bytes = cap_pages * self.page_bytes if capacity_bytes is None else capacity_bytes
+        # [B, L, H, N, 2, ps, d] in the pool's element type, pinned
+        self.host = torch.empty((store.B, store.L, store.H, store.NCAP, 2, PAGE_SIZE, store.D),
+                                dtype=store.dtype, pin_memory=True)
+        self.slow_resident = torch.zeros((store.B, store.L, store.H, store.NCAP), dtype=torch.uint8,
+                                         device=store.device)
+        self._counts: dict = {}
+        self.slow_bytes_used = 0
+        self.stable = tuple(profile.stable)
+
+    def _record(self, row: int, head: HeadId, pages) -> list:
+        counts = self._counts.setdefault((row, HeadId(*head)), {})
+        out = []
+        for p in pages:
+            p = int(p)
+            if counts.get(p, 0):
+                raise ConsistencyError(f"page {p} of {head} offloaded twice for request row {row}")
+            counts[p] = 1
+            out.append(p)
+        n_bytes = len(out) * self.page_bytes
+        if self.slow_bytes_used + n_bytes > self.capacity_bytes:
+            raise AdmissionError(f"slow tier capacity exceeded: {self.slow_bytes_used + n_bytes} "
+                                 f"> {self.capacity_bytes}")
+        self.slow_bytes_used += n_bytes
+        return out
+
+    def _offload(self, entries) -> int:
+        if not entries:
+            return 0
+        t = torch.tensor(entries, dtype=torch.int32).reshape(-1, 4).to(self.store.device)
+        self.store.offload_pages(self.host, t)
+        r, l, h, p = t.long().unbind(1)
+        self.slow_resident[r, l, h, p] = 1
+        return t.shape[0] * self.page_bytes
+
+    def offload_after_prefill(self, row: int, full_pages: int) -> int:
+        """One background copy of every full stable-head page (tiering.py:122-139)."""
+        if full_pages < 0:
+            raise ValueError("full_pages must be non-negative")
+        for head in self.stable:
+            if self._counts.get((row, head)):
+                raise ConsistencyError(f"request row {row} already ran its post-prefill offload")
+        entries = []
+        for head in self.stable:
+            for p in self._record(row, head, range(full_pages)):
+                entries += [row, head.layer, head.head, p]
+        return self._offload(entries)
+
+    def incremental_offload(self, row: int, head: HeadId, page: int, *, page_full: bool = True) -> int:
+        """Copy one page that just became full (tiering.py:141-157)."""
+        head = HeadId(*head)
+        if self.profile.is_unstable(head):
+            raise ConsistencyError(f"{head} is unstable; its pages are never offloaded")
+        if not page_full:
+            raise ConsistencyError(f"page {page} is not full; offload refused")
+        self._record(row, head, [page])
+        return self._offload([row, head.layer, head.head, int(page)])
+
+    def reload(self, layer: int, copies: torch.Tensor, n_copies: torch.Tensor) -> None:
+        """Fetch promoted pages (copy list from fc_rerank_recycle) host -> HBM."""
+        self.store.fetch_pages(layer, self.host, copies, n_copies)
+
+    def offload_counts(self, row: int, head: HeadId) -> dict:
+        return dict(self._counts.get((row, HeadId(*head)), {}))
+
+    def slow_pages(self, row: int, head: HeadId) -> set:
+        return set(self._counts.get((row, HeadId(*head)), {}))
