@@ -47,6 +47,7 @@ extern "C" {
 #define FC_ERR_PAGES_CAP        8u  /* logical page beyond pages_cap                 */
 #define FC_ERR_SEL_CAP         16u  /* selection longer than sel_cap                 */
 #define FC_ERR_DOUBLE_EVICT    32u  /* ConsistencyError   (blocktable.py:319-322)    */
+#define FC_ERR_WRITE_TWICE     64u  /* ConsistencyError   (tiering.py:105-110 ledger) */
 
 #define FC_NULL_BLOCK 0             /* blocktable.py:25 */
 
@@ -229,6 +230,22 @@ int fc_fetch_pages(const fc_store *s, int layer, const void *host_pages,
  * (TierStore._record write-once ledger, tiering.py:99-157). */
 int fc_offload_pages(const fc_store *s, void *host_pages, const int32_t *pages,
                      int n_pages, void *stream);
+
+/* Per-step incremental offload of stable heads (tiering.py:141-157, driven
+ * as simulator._append_token, simulator.py:467-477): for rows [0, batch)
+ * whose seq_len is a positive multiple of ps (the page seq_len/ps - 1 just
+ * filled), copy that page of every stable (layer, head) to the pinned host
+ * tier and set slow_resident[row][l][h][page]; a page already marked sets
+ * FC_ERR_WRITE_TWICE (write-once ledger).  Run after fc_step_advance. */
+int fc_offload_filled(const fc_store *s, void *host_pages, const uint8_t *unstable,
+                      uint8_t *slow_resident, int batch, void *stream);
+
+/* After the post-prefill offload: release every page of every stable head of
+ * rows [0, batch) that is not in its current selection (the offload_done
+ * eviction, simulator.py:389-408).  Blocks return to the free list in an
+ * unspecified order (naming is canonical-equivalent). */
+int fc_evict_unselected(const fc_store *s, const uint8_t *unstable, int batch,
+                        void *stream);
 
 /* Evict (set to the null block and release) logical pages listed in
  * pages [n][4] = (row, layer, head, logical page) — evict_many

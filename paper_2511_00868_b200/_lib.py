@@ -26,6 +26,7 @@ FC_ERR_NULL_WRITE = 4
 FC_ERR_PAGES_CAP = 8
 FC_ERR_SEL_CAP = 16
 FC_ERR_DOUBLE_EVICT = 32
+FC_ERR_WRITE_TWICE = 64
 
 _p = ctypes.c_void_p
 _i = ctypes.c_int
@@ -67,6 +68,8 @@ _SIGNATURES = {
     "fc_fetch_pages": (_i, [_p, _i, _p, _p, _p, _i, _p]),
     "fc_offload_pages": (_i, [_p, _p, _p, _i, _p]),
     "fc_evict_pages": (_i, [_p, _p, _i, _p]),
+    "fc_offload_filled": (_i, [_p, _p, _p, _p, _i, _p]),
+    "fc_evict_unselected": (_i, [_p, _p, _i, _p]),
 }
 
 _lib = None

@@ -239,6 +239,24 @@ int fc_offload_pages(const fc_store *s, void *host_pages, const int32_t *pages, 
     return cuda_status(launch_offload(make_view(s), host_pages, pages, n_pages, pb, (cudaStream_t)stream));
 }
 
+int fc_offload_filled(const fc_store *s, void *host_pages, const uint8_t *unstable, uint8_t *slow_resident,
+                      int batch, void *stream) {
+    FC_CHECK(check_store(s));
+    if (!host_pages || !unstable) return invalid("null buffer");
+    if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
+    if (batch == 0) return FC_OK;
+    const int pb = 2 * s->page_size * s->head_dim * (s->dtype == FC_BF16 ? 2 : 4);
+    return cuda_status(launch_offload_filled(make_view(s), host_pages, unstable, slow_resident, batch, pb,
+                                             (cudaStream_t)stream));
+}
+
+int fc_evict_unselected(const fc_store *s, const uint8_t *unstable, int batch, void *stream) {
+    FC_CHECK(check_store(s));
+    if (!unstable) return invalid("null buffer");
+    if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
+    return cuda_status(launch_evict_unselected(make_view(s), unstable, batch, 0, (cudaStream_t)stream));
+}
+
 int fc_evict_pages(const fc_store *s, const int32_t *pages, int n_pages, void *stream) {
     FC_CHECK(check_store(s));
     if (!pages) return invalid("null buffer");

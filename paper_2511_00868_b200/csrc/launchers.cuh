@@ -41,5 +41,7 @@ cudaError_t launch_rerank(const StoreView &, int, const int32_t *, const int32_t
 cudaError_t launch_fetch(const StoreView &, int, const void *, const int32_t *, const int32_t *, int, int,
                          cudaStream_t);
 cudaError_t launch_offload(const StoreView &, void *, const int32_t *, int, int, cudaStream_t);
+cudaError_t launch_offload_filled(const StoreView &, void *, const uint8_t *, uint8_t *, int, int, cudaStream_t);
+cudaError_t launch_evict_unselected(const StoreView &, const uint8_t *, int, int, cudaStream_t);
 
 }  // namespace fc

@@ -251,6 +251,66 @@ offload_kernel(StoreView s, char *host_pages, const int32_t *pages, int n, int p
     }
 }
 
+
+// per-step incremental offload: grid-stride over (row, layer, head)
+__global__ void __launch_bounds__(kCopyThreads)
+offload_filled_kernel(StoreView s, char *host_pages, const uint8_t *unstable, uint8_t *slow_resident,
+                      int batch, int page_bytes) {
+    const int LH = s.L * s.H;
+    for (int u = blockIdx.x; u < batch * LH; u += gridDim.x) {
+        const int b = u / LH, lh = u % LH;
+        if (unstable[lh]) continue;
+        const int len = s.seq_len[b];
+        if (len <= 0 || len % s.PS != 0) continue;
+        const int page = len / s.PS - 1;
+        const int64_t off = s.table_off(s.hix(b, lh / s.H, lh % s.H), page);
+        const int blk = s.table[off];
+        if (blk == FC_NULL_BLOCK) {
+            if (threadIdx.x == 0) set_error(s.err, FC_ERR_NULL_READ);
+            continue;
+        }
+        if (slow_resident && slow_resident[off]) {
+            if (threadIdx.x == 0) set_error(s.err, FC_ERR_WRITE_TWICE);
+            continue;
+        }
+        copy_page(reinterpret_cast<uint4 *>(host_pages + off * page_bytes),
+                  reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(s.pool) +
+                                                  (int64_t)blk * page_bytes),
+                  page_bytes / 16);
+        __syncthreads();
+        if (threadIdx.x == 0 && slow_resident) slow_resident[off] = 1;
+    }
+}
+
+// release every non-selected page of stable heads: one CTA per (row, layer, head)
+__global__ void __launch_bounds__(256)
+evict_unselected_kernel(StoreView s, const uint8_t *unstable, int batch, int extra_tokens) {
+    const int LH = s.L * s.H;
+    const int u = blockIdx.x;
+    if (u >= batch * LH) return;
+    const int b = u / LH, lh = u % LH;
+    if (unstable[lh]) return;
+    const int hx = s.hix(b, lh / s.H, lh % s.H);
+    const int n_pages = (s.seq_len[b] + extra_tokens + s.PS - 1) / s.PS;
+    const int nsel = s.n_sel[hx];
+    const int32_t *sel = s.sel + (int64_t)hx * s.SELCAP;
+    int32_t *trow = s.table + s.table_off(hx, 0);
+    for (int p = threadIdx.x; p < n_pages; p += blockDim.x) {
+        // sel is ascending: binary search
+        int lo = 0, hi = nsel;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (sel[mid] < p) lo = mid + 1; else hi = mid;
+        }
+        if (lo < nsel && sel[lo] == p) continue;
+        const int blk = trow[p];
+        if (blk == FC_NULL_BLOCK) continue;
+        trow[p] = FC_NULL_BLOCK;
+        const int slot = atomicAdd(s.free_top, 1);
+        s.free_stack[slot] = blk;
+    }
+}
+
 // ---------------------------------------------------------------------------
 
 size_t rerank_workspace_bytes(const StoreView &s) {
@@ -275,6 +335,21 @@ cudaError_t launch_fetch(const StoreView &s, int layer, const void *host_pages, 
     const int grid = max(1, min(max_copies, 148 * 8));
     fetch_kernel<<<grid, kCopyThreads, 0, st>>>(s, layer, (const char *)host_pages, copies, n_copies,
                                                 max_copies, page_bytes);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_offload_filled(const StoreView &s, void *host_pages, const uint8_t *unstable,
+                                  uint8_t *slow_resident, int batch, int page_bytes, cudaStream_t st) {
+    const int grid = max(1, min(batch * s.L * s.H, 148 * 8));
+    offload_filled_kernel<<<grid, kCopyThreads, 0, st>>>(s, (char *)host_pages, unstable, slow_resident,
+                                                          batch, page_bytes);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_evict_unselected(const StoreView &s, const uint8_t *unstable, int batch, int extra,
+                                    cudaStream_t st) {
+    if (batch * s.L * s.H == 0) return cudaSuccess;
+    evict_unselected_kernel<<<batch * s.L * s.H, 256, 0, st>>>(s, unstable, batch, extra);
     return cudaGetLastError();
 }
 

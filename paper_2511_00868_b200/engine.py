@@ -37,7 +37,7 @@ class DecodeEngine:
     def __init__(self, *, batch: int, layers: int, kv_heads: int, group: int, head_dim: int,
                  ctx_cap_tokens: int, topk_pages: int, rerank_period: int,
                  profile: HeadProfile, dtype=torch.bfloat16, device="cuda",
-                 n_blocks: int | None = None):
+                 n_blocks: int | None = None, tiering: bool = False):
         if profile.n_layers != layers or profile.n_heads_per_layer != kv_heads:
             raise ValueError("profile grid does not match (layers, kv_heads)")
         self.B, self.L, self.H, self.G, self.D = batch, layers, kv_heads, group, head_dim
@@ -63,6 +63,21 @@ class DecodeEngine:
         self.v_new = torch.zeros_like(self.k_new)
         self.out = torch.zeros_like(self.q)
         self._graphs: dict[bool, torch.cuda.CUDAGraph] = {}
+        # two-tier mode (subsystem 4): stable heads keep only their selection in
+        # HBM; every full page lives once in the pinned host tier
+        self.tiering = tiering
+        self.tier = None
+        if tiering:
+            from .tiering import TierStore
+            self.tier = TierStore(self.store, profile)
+            st = self.store
+            self.old_sel = torch.zeros((batch, kv_heads, st.SELCAP), dtype=torch.int32, device=self.device)
+            self.n_old = torch.zeros((batch, kv_heads), dtype=torch.int32, device=self.device)
+            self.copies = torch.zeros((batch * kv_heads * st.SELCAP, 4), dtype=torch.int32, device=self.device)
+            self.n_copies = torch.zeros(1, dtype=torch.int32, device=self.device)
+            self.fetched_pages = torch.zeros(1, dtype=torch.int64, device=self.device)
+            self._stable_layers = [l for l in range(layers)
+                                   if any(not profile.is_unstable(HeadId(l, h)) for h in range(kv_heads))]
 
     # -- prefill ----------------------------------------------------------------
 
@@ -95,14 +110,28 @@ class DecodeEngine:
 
     def _launch_step(self, rerank: bool, force_due: bool) -> None:
         st = self.store
+        tiered_rerank = self.tiering and rerank and not force_due
         for layer in range(self.L):
+            recycle = tiered_rerank and layer in self._stable_layers
+            if recycle:  # resident set of stable heads = their current selection
+                self.old_sel.copy_(st.sel[:, layer])
+                self.n_old.copy_(st.n_sel[:, layer])
+                self.n_copies.zero_()
             if force_due or not self._layer_skippable(layer, rerank):
                 st.score_select(layer, self.q[layer], self.unstable, self.R, self.K, self.B,
                                 force_due=force_due, extra_tokens=1)
+            if recycle:  # fused diff/recycle, then fetch the promoted pages over PCIe
+                st.rerank_recycle(layer, self.old_sel, self.n_old, self.unstable, self.R, self.copies,
+                                  self.n_copies, self.B, old_has_tail=False, extra_tokens=1,
+                                  slow_resident=self.tier.slow_resident)
+                self.tier.reload(layer, self.copies, self.n_copies)
+                self.fetched_pages.add_(self.n_copies)
             st.sparse_decode(layer, self.q[layer], self.out[layer], self.B,
                              max_pages=self.att_bound, extra_tokens=1, attend_appended=False,
                              k_new=self.k_new[layer], v_new=self.v_new[layer])
         st.step_advance(self.B)
+        if self.tiering:  # write-once offload of the page that just filled
+            st.offload_filled(self.tier.host, self.unstable, self.tier.slow_resident, self.B)
 
     def _layer_skippable(self, layer: int, rerank: bool) -> bool:
         # a representative step of the same kind: R (rerank) or 1 (plain, R > 1)
@@ -115,7 +144,12 @@ class DecodeEngine:
         selection for every head."""
         rerank = self.is_rerank_step()
         if not self.selected:
+            if self.tiering:  # post-prefill offload of every full stable-head page
+                for b in range(self.B):
+                    self.tier.offload_after_prefill(b, self.seq_host[b] // PAGE_SIZE)
             self._launch_step(rerank, force_due=True)
+            if self.tiering:  # keep only the selection of stable heads in HBM
+                self.store.evict_unselected(self.unstable, self.B)
             self.selected = True
         elif use_graph:
             g = self._graphs.get(rerank)
@@ -149,7 +183,10 @@ class DecodeEngine:
         a due head, and the step advance."""
         rerank = self.is_rerank_step(t)
         scored = sum(not self._layer_skippable(l, rerank) for l in range(self.L))
-        return self.L + scored + 1
+        n = self.L + scored + 1
+        if self.tiering:
+            n += 1 + (2 * len(self._stable_layers) if rerank else 0)
+        return n
 
     # -- host-buffer API (end-to-end path) -------------------------------------------
 

@@ -102,6 +102,8 @@ class KVStore:
         self.error_word.zero_()
         if bits & _lib.FC_ERR_POOL_EXHAUSTED:
             raise PoolExhausted(f"fast pool exhausted ({self.n_blocks - 1} blocks)")
+        if bits & _lib.FC_ERR_WRITE_TWICE:
+            raise ConsistencyError("page offloaded twice (write-once ledger, tiering.py:105-110)")
         if bits & (_lib.FC_ERR_NULL_READ | _lib.FC_ERR_DOUBLE_EVICT):
             raise ConsistencyError(
                 "residency violation: read of the null block / double eviction "
@@ -212,6 +214,16 @@ class KVStore:
         _lib.check(self.lib.fc_fetch_pages(self.cptr, layer, host_pages.data_ptr(), copies.data_ptr(),
                                            n_copies.data_ptr(), copies.shape[0], self.stream()),
                    "fc_fetch_pages")
+
+    def offload_filled(self, host_pages: torch.Tensor, unstable: torch.Tensor,
+                       slow_resident: torch.Tensor | None, batch: int) -> None:
+        _lib.check(self.lib.fc_offload_filled(self.cptr, host_pages.data_ptr(), unstable.data_ptr(),
+                                              _ptr(slow_resident), batch, self.stream()),
+                   "fc_offload_filled")
+
+    def evict_unselected(self, unstable: torch.Tensor, batch: int) -> None:
+        _lib.check(self.lib.fc_evict_unselected(self.cptr, unstable.data_ptr(), batch, self.stream()),
+                   "fc_evict_unselected")
 
     def offload_pages(self, host_pages: torch.Tensor, pages: torch.Tensor) -> None:
         _lib.check(self.lib.fc_offload_pages(self.cptr, host_pages.data_ptr(), pages.data_ptr(),

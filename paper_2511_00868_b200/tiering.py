@@ -63,9 +63,9 @@ class TierStore:
         return out
 
     def _offload(self, entries) -> int:
-        if not entries:
+        if len(entries) == 0:
             return 0
-        t = torch.tensor(entries, dtype=torch.int32).reshape(-1, 4).to(self.store.device)
+        t = torch.as_tensor(entries, dtype=torch.int32).reshape(-1, 4).to(self.store.device)
         self.store.offload_pages(self.host, t)
         r, l, h, p = t.long().unbind(1)
         self.slow_resident[r, l, h, p] = 1
@@ -78,11 +78,15 @@ class TierStore:
         for head in self.stable:
             if self._counts.get((row, head)):
                 raise ConsistencyError(f"request row {row} already ran its post-prefill offload")
-        entries = []
+        import numpy as np
+        blocks = []
         for head in self.stable:
-            for p in self._record(row, head, range(full_pages)):
-                entries += [row, head.layer, head.head, p]
-        return self._offload(entries)
+            pages = np.asarray(self._record(row, head, range(full_pages)), dtype=np.int32)
+            if pages.size:
+                e = np.empty((pages.size, 4), dtype=np.int32)
+                e[:, 0], e[:, 1], e[:, 2], e[:, 3] = row, head.layer, head.head, pages
+                blocks.append(e)
+        return self._offload(np.concatenate(blocks) if blocks else [])
 
     def incremental_offload(self, row: int, head: HeadId, page: int, *, page_full: bool = True) -> int:
         """Copy one page that just became full (tiering.py:141-157)."""

@@ -25,7 +25,7 @@ def _round(x, dtype):
 
 
 def run_engine_vs_oracle(*, B, L, H, G, D, T0, steps, K, R, frac, dtype, seed, use_graph,
-                         ragged=False):
+                         ragged=False, tiering=False):
     from paper_2511_00868_b200.engine import DecodeEngine
     from paper_2511_00868_b200.stability import HeadProfile
     rng = np.random.default_rng(seed)
@@ -33,7 +33,7 @@ def run_engine_vs_oracle(*, B, L, H, G, D, T0, steps, K, R, frac, dtype, seed, u
     unstable = prof.mask()
     eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D,
                        ctx_cap_tokens=T0 + steps + 64, topk_pages=K, rerank_period=R,
-                       profile=prof, dtype=dtype)
+                       profile=prof, dtype=dtype, tiering=tiering)
     dev = eng.device
     lens = [T0 + (17 * b if ragged else 0) for b in range(B)]
     keys = {}
@@ -64,6 +64,7 @@ def run_engine_vs_oracle(*, B, L, H, G, D, T0, steps, K, R, frac, dtype, seed, u
         n_sel = eng.store.n_sel.cpu().numpy()
         out = eng.out.double().cpu().numpy()
         summ = eng.store.summaries.double().cpu().numpy()
+        table = eng.store.table.cpu().numpy()
         for b in range(B):
             for l in range(L):
                 for h in range(H):
@@ -91,6 +92,12 @@ def run_engine_vs_oracle(*, B, L, H, G, D, T0, steps, K, R, frac, dtype, seed, u
                             for p in set(gsel) ^ set(osel):
                                 assert abs(osc[p] - kth) <= band, (b, l, h, p)
                             tie_mismatch += 1
+                    if tiering and not unstable[l, h]:
+                        # stable heads keep exactly their selection in HBM
+                        # (boundary residency check, simulator.py:526-531)
+                        n_alloc = O.pages_for_tokens(n_tok + 1, PS)
+                        resident = tuple(np.flatnonzero(table[b, l, h, :n_alloc]).tolist())
+                        assert resident == tuple(sel[b, l, h, :n_sel[b, l, h]].tolist()), (step, b, l, h)
                     # (3) attention over the GPU's attended set
                     pages = O.attended_pages(gsel, n_pages)
                     want = O.gqa_sparse_decode(qs, kk, vv, PS, pages)
@@ -135,3 +142,15 @@ def test_page_table_injective_and_conserving():
     live = table[table != 0]
     assert np.unique(live).size == live.size            # check_injective (blocktable.py:389-392)
     assert st.free_count() + live.size + 1 == st.n_blocks  # check_conservation (:394-400)
+
+
+def test_engine_tiered_rerank_fetch_matches_oracle():
+    """Two-tier mode: stable heads hold only their selection in HBM; reranks
+    recycle blocks and fetch promoted pages from pinned host memory; pages
+    filled during decode are offloaded once.  Attention after every fetch
+    must still equal the oracle (fetched K/V are the written K/V)."""
+    worst, ties, eng = run_engine_vs_oracle(B=2, L=2, H=4, G=4, D=128, T0=400, steps=24, K=6,
+                                            R=4, frac=0.5, dtype=torch.bfloat16, seed=10,
+                                            use_graph=True, tiering=True)
+    assert int(eng.fetched_pages.item()) > 0
+    eng.store.check_errors()
