@@ -239,15 +239,21 @@ def run_ours(args, cfg):
     barrier(world)
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local) as clk:
+        torch.cuda._sleep(50_000_000)  # ~25 ms of GPU work queued first: the host runs ahead
         e0.record(stream)
+        step_ev[0].record(stream)
         for i in range(args.steps):
             feed(i)
             eng.step()
+            step_ev[i + 1].record(stream)
         e1.record(stream)
         torch.cuda.synchronize(dev)
     barrier(world)
     ms = e0.elapsed_time(e1)
+    per_step = sorted(step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps))
+    step_stats = {"p50_ms": per_step[len(per_step) // 2], "min_ms": per_step[0], "max_ms": per_step[-1]}
     ms = max_over_ranks(ms, world)
     eng.store.check_errors()
     value = world * B * args.steps / (ms / 1e3)
@@ -327,6 +333,7 @@ def run_ours(args, cfg):
                    "parallelism": f"request-parallel x{world}",
                    "l2": "inputs larger than L2 (5+ GiB touched per step vs 126 MB L2)"},
         "gpu_launches": launches,
+        "step_ms": step_stats,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "kernel": "fc_sparse_decode (attn_kernel)",
                      "peak_source": peak_src, "avg_launch_us": att_avg_s * 1e6,

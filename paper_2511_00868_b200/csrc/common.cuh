@@ -103,6 +103,11 @@ FC_DEVINL void bulk_g2s(void *smem_dst, const void *gmem_src, uint32_t bytes, ui
         ::"r"(smem_u32(smem_dst)), "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
+// L2 prefetch of a global range (no shared memory, no completion tracking)
+FC_DEVINL void bulk_prefetch_l2(const void *gmem_src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem_src), "r"(bytes) : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // ldmatrix / mma.sync (bf16 -> fp32) — legacy tensor path (SASS HMMA).
 

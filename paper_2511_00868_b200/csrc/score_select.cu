@@ -31,7 +31,13 @@ FC_DEVINL unsigned long long gtimer_s() {
 }
 
 constexpr int kScoreThreads = 256;
-constexpr int kRoundsPerIter = 8;   // pages per lane-slot per iteration (MLP)
+#ifndef FC_SCORE_ROUNDS
+#define FC_SCORE_ROUNDS 16
+#endif
+#ifndef FC_SCORE_MINBLOCKS
+#define FC_SCORE_MINBLOCKS 2
+#endif
+constexpr int kRoundsPerIter = FC_SCORE_ROUNDS;   // pages per lane-slot per iteration (MLP)
 
 // ---------------------------------------------------------------------------
 // block-wide exact top-K over keys[0..n) in shared memory.
@@ -329,11 +335,14 @@ __device__ void score_range(const StoreView &s, int hx, int p0, int p1, const fl
             }
             v[r] = acc;
         }
-        // transpose-reduce 8 values over LPP lanes: 3 halving steps then plain
-        // butterflies; afterwards lane bits select which round it holds.
+        // transpose-reduce R values over LPP lanes: log2(R) halving steps, then
+        // plain butterflies over the LPP/R lanes that share a round; lane bits
+        // then select which round a lane holds.
+        static_assert(LPP >= kRoundsPerIter, "rounds per iteration exceed lanes per page");
+        constexpr int NSTEP = kRoundsPerIter == 16 ? 4 : kRoundsPerIter == 8 ? 3 : kRoundsPerIter == 4 ? 2 : 1;
         int ridx = 0;
 #pragma unroll
-        for (int step = 0, dist = LPP / 2, cnt = kRoundsPerIter / 2; step < 3;
+        for (int step = 0, dist = LPP / 2, cnt = kRoundsPerIter / 2; step < NSTEP;
              ++step, dist >>= 1, cnt >>= 1) {
             const bool upper = (lane & dist) != 0;
 #pragma unroll
@@ -345,9 +354,9 @@ __device__ void score_range(const StoreView &s, int hx, int p0, int p1, const fl
             if (upper) ridx += cnt;
         }
 #pragma unroll
-        for (int dist = LPP / 16; dist > 0; dist >>= 1)
+        for (int dist = LPP / kRoundsPerIter / 2; dist > 0; dist >>= 1)
             v[0] += __shfl_xor_sync(0xffffffffu, v[0], dist);
-        if ((cl & (LPP / 8 - 1)) == 0) {
+        if ((cl & (LPP / kRoundsPerIter - 1)) == 0) {
             const int p = it0 + ridx * Gm::kPagesPerSlot + sub;
             if (p < p1) scores_row[p] = v[0];
         }
@@ -377,7 +386,7 @@ __device__ void load_group_coeffs(const StoreView &s, const T *q, int b, int h, 
 // the exact selection.  Heads whose budget covers every page are selected
 // directly by CTA 0 (all pages).
 template <typename T, int D>
-__global__ void __launch_bounds__(kScoreThreads)
+__global__ void __launch_bounds__(kScoreThreads, FC_SCORE_MINBLOCKS)
 score_select_kernel(StoreView s, int layer, const T *__restrict__ q,
                     const uint8_t *__restrict__ unstable, int period, int force_due,
                     int topk, int extra_tokens, float *scores, int32_t *counters,

@@ -334,7 +334,6 @@ FC_DEVINL HeadInfo head_info(const StoreView &s, const AttnArgs &a, int bh) {
     return hi;
 }
 
-constexpr int kMaxHeads = 1 << 20;  // batch*H per launch (grid.x = heads * S)
 constexpr int kMaxClusterCtas = 16;
 
 // Optional per-CTA timeline (globaltimer ns) for profiling: [grid][4] =
@@ -345,6 +344,20 @@ FC_DEVINL unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
+}
+
+// one page as FC_PAGE_SPLIT bulk copies on the same mbarrier (tx counted once)
+#ifndef FC_PAGE_SPLIT
+#define FC_PAGE_SPLIT 1
+#endif
+#ifndef FC_L2_PREFETCH
+#define FC_L2_PREFETCH 0   // pages ahead of the ring warmed into L2 (0 = off)
+#endif
+FC_DEVINL void bulk_page(char *dst, const char *src, uint32_t bytes, uint64_t *bar) {
+    constexpr int NS = FC_PAGE_SPLIT;
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+        bulk_g2s(dst + k * (bytes / NS), src + k * (bytes / NS), bytes / NS, bar);
 }
 
 // page (logical) of attended entry j of a head
@@ -426,11 +439,18 @@ attn_kernel(StoreView s, AttnArgs a, int S) {
         if (lane == 0 && i < n_e) {
             if (blk > 0) {
                 mbar_arrive_expect_tx(&mybars[i], Gm::kPageBytes);
-                bulk_g2s(myring + (size_t)i * Gm::kPageBytes, pool + (int64_t)blk * Gm::kPageBytes,
-                         Gm::kPageBytes, &mybars[i]);
+                bulk_page(myring + (size_t)i * Gm::kPageBytes, pool + (int64_t)blk * Gm::kPageBytes,
+                          Gm::kPageBytes, &mybars[i]);
             } else {
                 mbar_arrive_expect_tx(&mybars[i], 0);
             }
+        }
+    }
+    if constexpr (FC_L2_PREFETCH > 0) {
+#pragma unroll
+        for (int i = NST; i < NST + FC_L2_PREFETCH; ++i) {
+            const int pblk = __shfl_sync(0xffffffffu, i < 32 ? cur_blk : nxt_blk, i & 31);
+            if (lane == 0 && i < n_e && pblk > 0) bulk_prefetch_l2(pool + (int64_t)pblk * Gm::kPageBytes, Gm::kPageBytes);
         }
     }
     const unsigned long long t_issued = trace ? gtimer() : 0ull;
@@ -467,12 +487,20 @@ attn_kernel(StoreView s, AttnArgs a, int S) {
             st.page(stage, page_is_last ? last_fill : kPageSize, a.scale_log2, lane);
         }
         __syncwarp();
+        if constexpr (FC_L2_PREFETCH > 0) {
+            const int pi = ni + FC_L2_PREFETCH;  // within the current or next 32-entry chunk
+            const int pb_cur = __shfl_sync(0xffffffffu, cur_blk, pi & 31);
+            const int pb_nxt = __shfl_sync(0xffffffffu, nxt_blk, pi & 31);
+            const int pblk = (pi >> 5) == chunk ? pb_cur : ((pi >> 5) == chunk + 1 ? pb_nxt : 0);
+            if (lane == 0 && pi < n_e && pblk > 0)
+                bulk_prefetch_l2(pool + (int64_t)pblk * Gm::kPageBytes, Gm::kPageBytes);
+        }
         if (lane == 0 && ni < n_e) {
             fence_proxy_async_smem();
             if (nblk > 0) {
                 mbar_arrive_expect_tx(&mybars[stg], Gm::kPageBytes);
-                bulk_g2s(myring + (size_t)stg * Gm::kPageBytes, pool + (int64_t)nblk * Gm::kPageBytes,
-                         Gm::kPageBytes, &mybars[stg]);
+                bulk_page(myring + (size_t)stg * Gm::kPageBytes, pool + (int64_t)nblk * Gm::kPageBytes,
+                          Gm::kPageBytes, &mybars[stg]);
             } else {
                 mbar_arrive_expect_tx(&mybars[stg], 0);
             }

@@ -90,3 +90,13 @@ sel_rows = tr[:, 2] > 0
 sel_start = sc_done[sel_rows]; sel_end = (tr[sel_rows, 2] - t0) / 1e3
 print(json.dumps({"score_ctas": int(tr.shape[0]), "entry": pct(ent), "scoring_done": pct(sc_done), "exit": pct(fin),
                   "n_selectors": int(sel_rows.sum()), "select_us": pct(sel_end - sel_start), "select_end": pct(sel_end)}))
+
+# ---- access-pattern probe: contiguous selections vs the top-K (scattered) ones
+sel_bak, nsel_bak = st.sel.clone(), st.n_sel.clone()
+n_att = int(st.n_sel[0, 0, 0].item())
+contig = torch.arange(n_att, dtype=torch.int32, device=dev)
+st.sel[:, 0, :, :n_att] = contig
+t_contig = timeit(lambda: st.sparse_decode(0, eng.q[0], eng.out[0], B, max_pages=eng.att_bound, attend_appended=False))
+st.sel.copy_(sel_bak); st.n_sel.copy_(nsel_bak)
+t_sparse = timeit(lambda: st.sparse_decode(0, eng.q[0], eng.out[0], B, max_pages=eng.att_bound, attend_appended=False))
+print(json.dumps({"attn_contiguous_pages_us": t_contig, "attn_topk_pages_us": t_sparse, "n_att": n_att}))
