@@ -136,11 +136,14 @@ int fc_kv_gather(const fc_store *s, int row, int layer, int head, int n_pages,
  * seq_len to count the token being appended this step.
  * q: [batch][H*G][d] (store dtype).  scores_out: [B_cap*H][pages_cap] fp32
  * workspace that receives the scores (pinned page = -inf).  counters:
- * [B_cap*H] int32, zero-initialised once by the caller. */
+ * [B_cap*H] int32, zero-initialised once by the caller.  kv_prefetch = 1:
+ * the previous launch on the stream does not write this layer's summaries,
+ * selections or seq_len, so the launch plans its range and warms L2 before
+ * waiting for it (programmatic dependent launch); only q is waited for. */
 size_t fc_score_select_workspace_size(const fc_store *s);
 int fc_score_select(const fc_store *s, int layer, const void *q,
                     const uint8_t *unstable, int period, int force_due,
-                    int topk, int extra_tokens, float *scores_out,
+                    int topk, int extra_tokens, int kv_prefetch, float *scores_out,
                     int32_t *counters, int batch, void *stream);
 
 /* Score only (no selection): scores_out[(row*H+h)*pages_cap + p] for pages
@@ -177,13 +180,18 @@ int fc_select_topk(const float *scores, int stride, const int32_t *n_valid,
  * (n_ctas = S; 0 = auto: the largest power of two <= 16 keeping all heads in
  * one wave); the CTAs of a cluster merge their softmax states through
  * distributed shared memory.  `max_pages` bounds the attended pages of any
- * head.  The workspace is a small scratch kept for ABI stability. */
+ * head.  The workspace is a small scratch kept for ABI stability.
+ * kv_prefetch = 1 lets the launch resolve pages and start their loads before
+ * the previous kernel on the stream completes (programmatic dependent
+ * launch); only q and k_new/v_new are waited for.  Valid when no kernel
+ * between this layer's last selection/table update and this call is still
+ * writing them (e.g. layers without a scoring launch this step). */
 size_t fc_sparse_decode_workspace_size(const fc_store *s, int batch,
                                        int max_pages, int n_ctas);
 int fc_sparse_decode(const fc_store *s, int layer, const void *q,
                      const void *k_new, const void *v_new, void *out,
                      float *lse, float scale, int extra_tokens,
-                     int attend_appended, int max_pages, int n_ctas,
+                     int attend_appended, int kv_prefetch, int max_pages, int n_ctas,
                      void *workspace, size_t ws_bytes, int batch,
                      void *stream);
 

@@ -118,8 +118,8 @@ size_t fc_score_select_workspace_size(const fc_store *s) {
 }
 
 int fc_score_select(const fc_store *s, int layer, const void *q, const uint8_t *unstable, int period,
-                    int force_due, int topk, int extra_tokens, float *scores_out, int32_t *counters,
-                    int batch, void *stream) {
+                    int force_due, int topk, int extra_tokens, int kv_prefetch, float *scores_out,
+                    int32_t *counters, int batch, void *stream) {
     FC_CHECK(check_store(s));
     if (layer < 0 || layer >= s->layers) return invalid("layer out of range");
     if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
@@ -131,7 +131,8 @@ int fc_score_select(const fc_store *s, int layer, const void *q, const uint8_t *
     if (s->pages_cap > 8192) return FC_E_CAPACITY;  /* 128k-token heads (block_select keys <= 32*256) */
     if (batch == 0) return FC_OK;
     return cuda_status(launch_score(make_view(s), s->dtype, layer, q, unstable, period, force_due, topk,
-                                    extra_tokens, scores_out, counters, 1, batch, (cudaStream_t)stream));
+                                    extra_tokens, scores_out, counters, 1, batch, kv_prefetch ? 1 : 0,
+                                    (cudaStream_t)stream));
 }
 
 int fc_score_pages(const fc_store *s, int layer, const void *q, int extra_tokens, float *scores_out, int batch,
@@ -144,7 +145,7 @@ int fc_score_pages(const fc_store *s, int layer, const void *q, int extra_tokens
     if (batch == 0) return FC_OK;
     static uint8_t *dummy = nullptr;  // never dereferenced when do_select == 0
     return cuda_status(launch_score(make_view(s), s->dtype, layer, q, dummy, 1, 0, 1, extra_tokens, scores_out,
-                                    nullptr, 0, batch, (cudaStream_t)stream));
+                                    nullptr, 0, batch, 0, (cudaStream_t)stream));
 }
 
 int fc_select_topk(const float *scores, int stride, const int32_t *n_valid, int n_heads, int topk, int pin_last,
@@ -166,8 +167,8 @@ size_t fc_sparse_decode_workspace_size(const fc_store *s, int batch, int max_pag
 
 int fc_sparse_decode(const fc_store *s, int layer, const void *q, const void *k_new, const void *v_new,
                      void *out, float *lse, float scale, int extra_tokens, int attend_appended,
-                     int max_pages, int n_ctas, void *workspace, size_t ws_bytes, int batch,
-                     void *stream) {
+                     int kv_prefetch, int max_pages, int n_ctas, void *workspace, size_t ws_bytes,
+                     int batch, void *stream) {
     FC_CHECK(check_store(s));
     if (layer < 0 || layer >= s->layers) return invalid("layer out of range");
     if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
@@ -189,6 +190,7 @@ int fc_sparse_decode(const fc_store *s, int layer, const void *q, const void *k_
     a.layer = layer; a.q = q; a.k_new = k_new; a.v_new = v_new; a.out = out; a.lse = lse;
     a.scale_log2 = scale * 1.4426950408889634f;
     a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.max_splits = grid;
+    a.kv_prefetch = kv_prefetch ? 1 : 0;
     char *w = (char *)workspace;
     a.counters = (int32_t *)w;
     a.part_m = (float *)(w + ((2 * heads * sizeof(int32_t) + 255) & ~(size_t)255));

@@ -13,6 +13,7 @@ struct AttnArgs {
     float scale_log2;
     int extra_tokens;
     int attend_appended;
+    int kv_prefetch;      // stage KV pages before the previous launch completes
     int max_splits;       // CTAs per head (cluster size S)
     int32_t *counters;    // [B_cap*H] partials published per head (zeroed once, self-resetting)
     float *part_m;        // [parts][16]
@@ -27,7 +28,7 @@ cudaError_t launch_prefill(const StoreView &, int, int, int, const void *, const
 cudaError_t launch_append(const StoreView &, int, int, const void *, const void *, int, cudaStream_t);
 cudaError_t launch_gather(const StoreView &, int, int, int, int, int, void *, void *, cudaStream_t);
 cudaError_t launch_score(const StoreView &, int, int, const void *, const uint8_t *, int, int, int, int,
-                         float *, int32_t *, int, int, cudaStream_t);
+                         float *, int32_t *, int, int, int, cudaStream_t);
 cudaError_t launch_select(const float *, int, const int32_t *, int, int, int, int32_t *, int32_t *,
                           cudaStream_t);
 cudaError_t launch_attn(const StoreView &, int, const AttnArgs &, int, cudaStream_t);

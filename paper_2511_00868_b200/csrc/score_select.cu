@@ -390,12 +390,14 @@ __global__ void __launch_bounds__(kScoreThreads, FC_SCORE_MINBLOCKS)
 score_select_kernel(StoreView s, int layer, const T *__restrict__ q,
                     const uint8_t *__restrict__ unstable, int period, int force_due,
                     int topk, int extra_tokens, float *scores, int32_t *counters,
-                    int do_select, int n_heads) {
+                    int do_select, int n_heads, int kv_prefetch) {
     extern __shared__ uint32_t dyn[];  // keys [NCAP] (do_select) | prefix [n_heads+1]
     __shared__ float w[2 * D];
     __shared__ int s_last, s_wsum[kScoreThreads / 32];
     griddep_launch_dependents();
-    griddep_wait();
+    // kv_prefetch: the previous launch does not write this layer's summaries,
+    // selection or seq_len — plan the range and warm L2 before waiting for q
+    if (!kv_prefetch) griddep_wait();
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     unsigned long long *trace = g_score_trace;
     if (trace && tid == 0) trace[blockIdx.x * 4] = gtimer_s();
@@ -452,8 +454,28 @@ score_select_kernel(StoreView s, int layer, const T *__restrict__ q,
     int P = (total + gridDim.x - 1) / gridDim.x;
     P = ((P + ALIGN - 1) / ALIGN) * ALIGN;
     const int start = blockIdx.x * P;
-    if (start >= total) return;
+    if (start >= total) {
+        if (kv_prefetch) griddep_wait();
+        return;
+    }
     const int end = min(total, start + P);
+    if (kv_prefetch) {
+        // warm L2 with the first 64 KiB of this CTA's summaries, then wait for q
+        int lo = 0, hi = n_heads - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (prefix[mid] <= start) lo = mid; else hi = mid - 1;
+        }
+        const int hx0 = s.hix(lo / s.H, layer, lo % s.H);
+        const int p0 = start - prefix[lo];
+        const int np = min(min(end, prefix[lo + 1]) - start, 65536 / ScoreGeom<T, D>::kRecBytes);
+        const char *base = reinterpret_cast<const char *>(s.summ) +
+                           ((int64_t)hx0 * s.NCAP + p0) * ScoreGeom<T, D>::kRecBytes;
+        const int bytes = np * ScoreGeom<T, D>::kRecBytes;
+        for (int off = tid * 4096; off < bytes; off += blockDim.x * 4096)
+            bulk_prefetch_l2(base + off, (uint32_t)min(4096, bytes - off));
+        griddep_wait();
+    }
 
     int pos = start;
     while (pos < end) {
@@ -543,7 +565,7 @@ template <typename T, int D>
 static cudaError_t launch_score_t(const StoreView &s, int layer, const void *q,
                                   const uint8_t *unstable, int period, int force_due, int topk,
                                   int extra, float *scores, int32_t *counters, int do_select,
-                                  int batch, cudaStream_t st) {
+                                  int batch, int kv_prefetch, cudaStream_t st) {
     const int n_heads = batch * s.H;
     const size_t smem = (do_select ? (size_t)s.NCAP * sizeof(uint32_t) : 0) + (size_t)(n_heads + 1) * sizeof(int);
     auto kern = score_select_kernel<T, D>;
@@ -559,21 +581,21 @@ static cudaError_t launch_score_t(const StoreView &s, int layer, const void *q,
         cached_smem = smem;
     }
     return launch_pdl(kern, dim3(grid), dim3(kScoreThreads), smem, st, s, layer, (const T *)q, unstable,
-                      period, force_due, topk, extra, scores, counters, do_select, n_heads);
+                      period, force_due, topk, extra, scores, counters, do_select, n_heads, kv_prefetch);
 }
 
 cudaError_t launch_score(const StoreView &s, int dtype, int layer, const void *q,
                          const uint8_t *unstable, int period, int force_due, int topk, int extra,
                          float *scores, int32_t *counters, int do_select, int batch,
-                         cudaStream_t st) {
+                         int kv_prefetch, cudaStream_t st) {
     if (dtype == FC_BF16) {
         if (s.D == 128)
-            return launch_score_t<__nv_bfloat16, 128>(s, layer, q, unstable, period, force_due, topk, extra, scores, counters, do_select, batch, st);
-        return launch_score_t<__nv_bfloat16, 64>(s, layer, q, unstable, period, force_due, topk, extra, scores, counters, do_select, batch, st);
+            return launch_score_t<__nv_bfloat16, 128>(s, layer, q, unstable, period, force_due, topk, extra, scores, counters, do_select, batch, kv_prefetch, st);
+        return launch_score_t<__nv_bfloat16, 64>(s, layer, q, unstable, period, force_due, topk, extra, scores, counters, do_select, batch, kv_prefetch, st);
     }
     if (s.D == 128)
-        return launch_score_t<float, 128>(s, layer, q, unstable, period, force_due, topk, extra, scores, counters, do_select, batch, st);
-    return launch_score_t<float, 64>(s, layer, q, unstable, period, force_due, topk, extra, scores, counters, do_select, batch, st);
+        return launch_score_t<float, 128>(s, layer, q, unstable, period, force_due, topk, extra, scores, counters, do_select, batch, kv_prefetch, st);
+    return launch_score_t<float, 64>(s, layer, q, unstable, period, force_due, topk, extra, scores, counters, do_select, batch, kv_prefetch, st);
 }
 
 cudaError_t set_score_trace(void *p) {

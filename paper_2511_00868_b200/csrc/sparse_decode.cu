@@ -74,15 +74,27 @@ struct Bf16Warp {
         // S = Q Kᵀ over 16 tokens: two n-tiles of 8 tokens
         float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
         {
+            // two accumulator chains per n-tile (even / odd k-steps) halve the
+            // dependent-HMMA latency of the page
+            float s2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
             const int t = (mi >> 1) * 8 + ri;
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) {
                 const int c = 2 * kk + (mi & 1);
                 uint32_t b0, b1, b2, b3;
                 ldsm_x4(kb + t * RB + ((c ^ (t & 7)) << 4), b0, b1, b2, b3);
-                mma_bf16_16816(s[0], qa[kk], b0, b1);
-                mma_bf16_16816(s[1], qa[kk], b2, b3);
+                if (kk & 1) {
+                    mma_bf16_16816(s2[0], qa[kk], b0, b1);
+                    mma_bf16_16816(s2[1], qa[kk], b2, b3);
+                } else {
+                    mma_bf16_16816(s[0], qa[kk], b0, b1);
+                    mma_bf16_16816(s[1], qa[kk], b2, b3);
+                }
             }
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) s[j][e] += s2[j][e];
         }
         // online softmax; C-frag: s[j][0..1] row r0, s[j][2..3] row r1,
         // token j*8 + (lane&3)*2 + {0,1}
@@ -398,7 +410,11 @@ attn_kernel(StoreView s, AttnArgs a, int S) {
     unsigned long long *trace = g_attn_trace;
     const unsigned long long t_entry = trace ? gtimer() : 0ull;
     griddep_launch_dependents();  // let the next launch get scheduled early (PDL)
-    griddep_wait();               // selection / seq_len come from the previous launches
+    // Without kv_prefetch the selection / table / seq_len may come from the
+    // previous launch: wait for it.  With kv_prefetch the caller guarantees
+    // they do not, so pages are resolved and their loads issued while the
+    // previous kernel drains; only q and the new token wait.
+    if (!a.kv_prefetch) griddep_wait();
     char *ring = dsm;
     float *s_q = reinterpret_cast<float *>(dsm + (size_t)NW * NST * Gm::kPageBytes);
     float *cstate = s_q + (sizeof(T) == 4 ? G * D : 0);  // [G][D] acc, then m[16], l[16]
@@ -416,10 +432,6 @@ attn_kernel(StoreView s, AttnArgs a, int S) {
 
     if (tid < NW * NST) mbar_init(&bars[tid], 1);
     fence_mbar_init();
-    if constexpr (sizeof(T) == 4) {
-        const float *qg = reinterpret_cast<const float *>(a.q) + qoff;
-        for (int i = tid; i < G * D; i += blockDim.x) s_q[i] = qg[i];
-    }
     __syncthreads();
 
     // entries are resolved 32 at a time (lane l owns entry 32c + l of chunk c)
@@ -455,6 +467,12 @@ attn_kernel(StoreView s, AttnArgs a, int S) {
     }
     const unsigned long long t_issued = trace ? gtimer() : 0ull;
 
+    if (a.kv_prefetch) griddep_wait();  // q and the new token come from the previous launch
+    if constexpr (sizeof(T) == 4) {
+        const float *qg = reinterpret_cast<const float *>(a.q) + qoff;
+        for (int i = tid; i < G * D; i += blockDim.x) s_q[i] = qg[i];
+        __syncthreads();
+    }
     typename std::conditional<sizeof(T) == 2, Bf16Warp<D>, F32Warp<D>>::type st;
     if constexpr (sizeof(T) == 4) st.init(s_q, G, lane);
     else st.init(reinterpret_cast<const T *>(a.q) + qoff, G, lane);
@@ -597,8 +615,15 @@ static int attn_ctas_per_sm_t(const StoreView &s) {
     return occ < 1 ? 1 : occ;
 }
 
+#ifndef FC_ATTN_NW
+#define FC_ATTN_NW 8    // bf16 warps per CTA
+#endif
+#ifndef FC_ATTN_NST
+#define FC_ATTN_NST 3   // bf16 d=128 ring stages per warp (NW * NST * 8 KiB <= ~200 KiB)
+#endif
 #define FC_ATTN_DISPATCH(dtype, D, CALL)                                            \
-    ((dtype) == FC_BF16 ? ((D) == 128 ? CALL(__nv_bfloat16, 128, 3, 8) : CALL(__nv_bfloat16, 64, 6, 8)) \
+    ((dtype) == FC_BF16 ? ((D) == 128 ? CALL(__nv_bfloat16, 128, FC_ATTN_NST, FC_ATTN_NW)                \
+                                      : CALL(__nv_bfloat16, 64, 2 * FC_ATTN_NST, FC_ATTN_NW))            \
                         : ((D) == 128 ? CALL(float, 128, 3, 4) : CALL(float, 64, 6, 4)))
 
 static int num_sms() {

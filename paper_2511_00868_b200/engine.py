@@ -117,18 +117,25 @@ class DecodeEngine:
                 self.old_sel.copy_(st.sel[:, layer])
                 self.n_old.copy_(st.n_sel[:, layer])
                 self.n_copies.zero_()
-            if force_due or not self._layer_skippable(layer, rerank):
+            scored = force_due or not self._layer_skippable(layer, rerank)
+            if scored:
+                # the previous kernel (the last layer's attention) never writes this
+                # layer's summaries / selection: plan and warm L2 while it drains
                 st.score_select(layer, self.q[layer], self.unstable, self.R, self.K, self.B,
-                                force_due=force_due, extra_tokens=1)
+                                force_due=force_due, extra_tokens=1, kv_prefetch=layer > 0)
             if recycle:  # fused diff/recycle, then fetch the promoted pages over PCIe
                 st.rerank_recycle(layer, self.old_sel, self.n_old, self.unstable, self.R, self.copies,
                                   self.n_copies, self.B, old_has_tail=False, extra_tokens=1,
                                   slow_resident=self.tier.slow_resident)
                 self.tier.reload(layer, self.copies, self.n_copies)
                 self.fetched_pages.add_(self.n_copies)
+            # with no scoring / recycle launch in this layer, the previous kernel
+            # (the last layer's attention, or the step advance) does not touch
+            # this layer's selection, table or pages: stage KV while it drains
             st.sparse_decode(layer, self.q[layer], self.out[layer], self.B,
                              max_pages=self.att_bound, extra_tokens=1, attend_appended=False,
-                             k_new=self.k_new[layer], v_new=self.v_new[layer])
+                             k_new=self.k_new[layer], v_new=self.v_new[layer],
+                             kv_prefetch=not (scored or recycle))
         st.step_advance(self.B)
         if self.tiering:  # write-once offload of the page that just filled
             st.offload_filled(self.tier.host, self.unstable, self.tier.slow_resident, self.B)

@@ -157,11 +157,12 @@ class KVStore:
     # -- (2) scoring / selection -----------------------------------------------------
 
     def score_select(self, layer: int, q: torch.Tensor, unstable: torch.Tensor, period: int,
-                     topk: int, batch: int, *, force_due: bool = False, extra_tokens: int = 1) -> None:
+                     topk: int, batch: int, *, force_due: bool = False, extra_tokens: int = 1,
+                     kv_prefetch: bool = False) -> None:
         _lib.check(self.lib.fc_score_select(
             self.cptr, layer, q.data_ptr(), unstable.data_ptr(), period, int(force_due), topk,
-            extra_tokens, self.scores.data_ptr(), self.score_counters.data_ptr(), batch,
-            self.stream()), "fc_score_select")
+            extra_tokens, int(kv_prefetch), self.scores.data_ptr(), self.score_counters.data_ptr(),
+            batch, self.stream()), "fc_score_select")
 
     def score_pages(self, layer: int, q: torch.Tensor, batch: int, *, extra_tokens: int = 0) -> None:
         _lib.check(self.lib.fc_score_pages(self.cptr, layer, q.data_ptr(), extra_tokens,
@@ -180,13 +181,13 @@ class KVStore:
                       max_pages: int, n_ctas: int = 0, lse: torch.Tensor | None = None,
                       scale: float | None = None, extra_tokens: int = 1,
                       attend_appended: bool = True, k_new: torch.Tensor | None = None,
-                      v_new: torch.Tensor | None = None) -> None:
+                      v_new: torch.Tensor | None = None, kv_prefetch: bool = False) -> None:
         """Split-K paged attention; with k_new/v_new the decode append is fused."""
         ws = self.attn_workspace(batch, max_pages, n_ctas)
         scale = 1.0 / math.sqrt(self.D) if scale is None else scale
         _lib.check(self.lib.fc_sparse_decode(
             self.cptr, layer, q.data_ptr(), _ptr(k_new), _ptr(v_new), out.data_ptr(), _ptr(lse),
-            scale, extra_tokens, int(attend_appended), max_pages, n_ctas, ws.data_ptr(),
+            scale, extra_tokens, int(attend_appended), int(kv_prefetch), max_pages, n_ctas, ws.data_ptr(),
             ws.numel(), batch, self.stream()), "fc_sparse_decode")
 
     # -- (4) rerank / tiers ------------------------------------------------------------
