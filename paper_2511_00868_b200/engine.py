@@ -169,6 +169,13 @@ class DecodeEngine:
         self.seq_host = [s + 1 for s in self.seq_host]
         return self.out
 
+    def capture_graphs(self) -> None:
+        """Capture both step graphs now (rerank and plain), so no capture or
+        instantiation happens inside a timed region."""
+        for rerank in (False, True):
+            if rerank not in self._graphs:
+                self._capture(rerank)
+
     def _capture(self, rerank: bool) -> torch.cuda.CUDAGraph:
         # stream capture records the launches without executing them, so the
         # engine state is untouched; workspaces were sized by the eager first step
