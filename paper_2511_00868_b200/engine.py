@@ -215,6 +215,9 @@ class DecodeEngine:
         self.step()
         out_host.copy_(self.out, non_blocking=True)
 
+    def host_pipeline(self) -> "HostPipeline":
+        return HostPipeline(self)
+
     # -- accounting ------------------------------------------------------------------
 
     def attended_pages(self) -> torch.Tensor:
@@ -251,3 +254,55 @@ class DecodeEngine:
         n_pages = (st.seq_len.long() + 1 + PAGE_SIZE - 1) // PAGE_SIZE
         per_head = ((n_pages - 1) * 2 * self.D * e + self.G * self.D * e)
         return int(per_head.sum().item()) * sum(due)
+
+
+class HostPipeline:
+    """Decode steps fed from pinned host memory with the PCIe copies hidden:
+    step i's H2D inputs and step i-1's D2H outputs run on a copy stream while
+    the compute stream executes the step graph (double-buffered device
+    staging, ordered by CUDA events).  Every step still moves its own inputs
+    host->device and its outputs device->host."""
+
+    def __init__(self, eng: DecodeEngine):
+        self.eng = eng
+        dev = eng.device
+        self.copy = torch.cuda.Stream(dev)      # H2D of upcoming inputs
+        self.copy_out = torch.cuda.Stream(dev)  # D2H of finished outputs (separate queue:
+        self.main = torch.cuda.current_stream(dev)  # an H2D never waits behind a D2H)
+        self.q = [torch.empty_like(eng.q) for _ in range(2)]
+        self.k = [torch.empty_like(eng.k_new) for _ in range(2)]
+        self.v = [torch.empty_like(eng.v_new) for _ in range(2)]
+        self.o = [torch.empty_like(eng.out) for _ in range(2)]
+        self.ev_in = [torch.cuda.Event() for _ in range(2)]
+        self.ev_used = [torch.cuda.Event() for _ in range(2)]
+        self.ev_out = [torch.cuda.Event() for _ in range(2)]
+        for e in self.ev_used + self.ev_out:
+            e.record(self.main)
+        self.i = 0
+
+    def submit(self, q_host, k_host, v_host, out_host) -> None:
+        s = self.i % 2
+        with torch.cuda.stream(self.copy):
+            self.copy.wait_event(self.ev_used[s])  # step i-2 consumed this staging set
+            self.q[s].copy_(q_host, non_blocking=True)
+            self.k[s].copy_(k_host, non_blocking=True)
+            self.v[s].copy_(v_host, non_blocking=True)
+            self.ev_in[s].record(self.copy)
+        self.main.wait_event(self.ev_in[s])
+        self.eng.q.copy_(self.q[s])
+        self.eng.k_new.copy_(self.k[s])
+        self.eng.v_new.copy_(self.v[s])
+        self.eng.step()
+        self.main.wait_event(self.ev_out[s])  # step i-2's outputs left this buffer
+        self.o[s].copy_(self.eng.out)
+        self.ev_used[s].record(self.main)
+        with torch.cuda.stream(self.copy_out):
+            self.copy_out.wait_event(self.ev_used[s])
+            out_host.copy_(self.o[s], non_blocking=True)
+            self.ev_out[s].record(self.copy_out)
+        self.i += 1
+
+    def drain(self) -> None:
+        """Make the compute stream wait for every outstanding copy."""
+        self.main.wait_stream(self.copy)
+        self.main.wait_stream(self.copy_out)
