@@ -61,8 +61,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=CFG2["batch"])
     ap.add_argument("--ctx", type=int, default=CFG2["ctx"])
     ap.add_argument("--layers", type=int, default=CFG2["layers"])
-    ap.add_argument("--config", type=int, choices=[2, 3], default=2,
-                    help="2: the metric's config (default); 3: long generation with host offload")
+    ap.add_argument("--config", type=int, choices=[2, 3, 5], default=2,
+                    help="2: the metric's config (default); 3: long generation with host offload; "
+                         "5: Qwen2.5-7B-shaped, KV-head-sharded with an all-gather of outputs")
     return ap.parse_args()
 
 
@@ -504,6 +505,96 @@ def run_config3(args):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# config 5: Qwen2.5-7B-shaped GQA (28 q / 4 KV heads, d=128), 64k context,
+# batch 16, KV heads sharded over a head group with one all-gather of the
+# attention outputs per layer (NCCL over NVLink); leftover ranks replicate
+# requests (dist.head_shard_layout)
+
+CFG5 = dict(workload="config5: qwen2.5-7b-shaped decode, 28 layers, 28q/4kv, d=128, 64k ctx, batch 16, "
+                     "page 16, top-K 128 pages, R=16, u=0.25, KV-head-sharded + all-gather of outputs",
+            layers=28, kv_heads=4, group=7, head_dim=128, ctx=65536, batch=16, topk=128, period=16,
+            unstable_fraction=0.25)
+
+
+def run_config5(args):
+    import torch
+    rank, world, local = dist_setup(args.gpus)
+    from paper_2511_00868_b200 import dist as fdist
+    from paper_2511_00868_b200.engine import DecodeEngine
+    from paper_2511_00868_b200.stability import HeadProfile
+    from paper_2511_00868_b200.synthetic import device_normal
+    cfg = CFG5
+    dev = torch.device("cuda", local)
+    L, H, G, D = cfg["layers"], cfg["kv_heads"], cfg["group"], cfg["head_dim"]
+    T, K, R = cfg["ctx"], cfg["topk"], cfg["period"]
+    heads, rows, _ = fdist.head_shard_of(rank, world, H, cfg["batch"])
+    shards, replicas = fdist.head_shard_layout(world, H)
+    Hl, B = len(heads), len(rows)
+    full_prof = HeadProfile.first_n(L, H, cfg["unstable_fraction"], model_id="qwen2.5-7b-shaped")
+    prof = HeadProfile(model_id=full_prof.model_id, n_layers=L, n_heads_per_layer=Hl,
+                       fraction=full_prof.fraction,
+                       unstable=tuple((l, h - heads.start) for (l, h) in full_prof.unstable if h in heads))
+    group = fdist.HeadGroup(world, H)
+    out_full = torch.zeros((L, B, H * G, D), dtype=torch.bfloat16, device=dev)
+    holder = {}
+
+    def gather(layer):
+        group.gather(holder["eng"].out[layer], out_full[layer])
+
+    eng = DecodeEngine(batch=B, layers=L, kv_heads=Hl, group=G, head_dim=D,
+                       ctx_cap_tokens=T + 2 * (args.warmup + args.steps) + 32, topk_pages=K,
+                       rerank_period=R, profile=prof, dtype=torch.bfloat16, device=dev,
+                       after_layer=gather)
+    holder["eng"] = eng
+    srcs = [(device_normal((Hl, T, D), seed=100 * rank + 2 * i, device=dev),
+             device_normal((Hl, T, D), seed=100 * rank + 2 * i + 1, device=dev)) for i in range(2)]
+    for b in range(B):
+        for l in range(L):
+            k, v = srcs[(b + l) % 2]
+            eng.prefill_layer(b, l, k, v, alloc=(l == 0))
+    del srcs
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(5 + rank)
+
+    def feed():
+        eng.q.normal_(generator=gen)
+        eng.k_new.normal_(generator=gen)
+        eng.v_new.normal_(generator=gen)
+
+    feed()
+    eng.step()
+    for _ in range(args.warmup):
+        feed()
+        eng.step()
+    eng.capture_graphs()
+    torch.cuda.synchronize(dev)
+    eng.store.check_errors()
+    stream = torch.cuda.current_stream(dev)
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(20_000_000)
+    e0.record(stream)
+    for _ in range(args.steps):
+        feed()
+        eng.step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    ms = max_over_ranks(e0.elapsed_time(e1), world)
+    eng.store.check_errors()
+    if rank != 0:
+        return
+    total_tokens = cfg["batch"] * args.steps  # every request decodes one token per step
+    line = {"metric": METRIC, "value": total_tokens / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic N(0,1) KV and q/k/v", "config": {"workload": cfg["workload"],
+            "head_shards": shards, "request_replicas": replicas, "kv_heads_per_rank": Hl,
+            "requests_per_rank": B}}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     cfg = dict(CFG2)
@@ -512,6 +603,8 @@ def main():
         run_reference(args, cfg)
     elif args.config == 3:
         run_config3(args)
+    elif args.config == 5:
+        run_config5(args)
     else:
         run_ours(args, cfg)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:

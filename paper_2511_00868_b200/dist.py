@@ -68,3 +68,61 @@ def sum_over_ranks(x: float) -> float:
     t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# KV-head-sharded decode (config 5, SURVEY.md §8e option (i)):
+# the world is split into `n_head_shards`-rank head groups (each rank owns
+# H / n_head_shards KV heads of every layer) x `n_replicas` request replicas
+# (each replica group owns B / n_replicas request rows).  After each layer's
+# attention the head group all-gathers its outputs over NVLink — the path's
+# only exchange step; no softmax merge is needed because a query head's
+# attention is entirely local to the rank owning its KV head.
+
+def head_shard_layout(world: int, n_kv_heads: int) -> tuple[int, int]:
+    """(n_head_shards, n_replicas): the largest head split that divides both
+    the world and the KV heads; the rest of the world replicates requests."""
+    shards = 1
+    for s in range(1, world + 1):
+        if world % s == 0 and n_kv_heads % s == 0:
+            shards = s
+    return shards, world // shards
+
+
+def head_shard_of(rank: int, world: int, n_kv_heads: int, batch: int):
+    """This rank's (kv head range, request rows, head-group ranks)."""
+    shards, replicas = head_shard_layout(world, n_kv_heads)
+    replica, shard = divmod(rank, shards)
+    per = n_kv_heads // shards
+    heads = range(shard * per, (shard + 1) * per)
+    rows = shard_rows(batch, replica, replicas)
+    group = [replica * shards + s for s in range(shards)]
+    return heads, rows, group
+
+
+class HeadGroup:
+    """All-gather of per-shard attention outputs [B_r, Hq/shards, d] into the
+    full [B_r, Hq, d] (query heads in KV-head order) within a head group."""
+
+    def __init__(self, world: int, n_kv_heads: int):
+        self.shards, self.replicas = head_shard_layout(world, n_kv_heads)
+        self.group = None
+        if dist.is_initialized() and self.shards > 1:
+            groups = [dist.new_group([r * self.shards + s for s in range(self.shards)])
+                      for r in range(self.replicas)]  # every rank creates every group
+            self.group = groups[dist.get_rank() // self.shards]
+
+    def gather(self, local: torch.Tensor, out: torch.Tensor) -> None:
+        """local [B_r, Hq/shards, d] -> out [B_r, Hq, d]."""
+        if self.group is None:
+            out.copy_(local)
+            return
+        local = local.contiguous()
+        if dist.get_backend(self.group) == "nccl":  # one NCCL all-gather over NVLink
+            stacked = torch.empty((self.shards,) + tuple(local.shape), dtype=local.dtype, device=local.device)
+            dist.all_gather_into_tensor(stacked, local, group=self.group)
+        else:  # gloo (CPU tests)
+            parts = [torch.empty_like(local) for _ in range(self.shards)]
+            dist.all_gather(parts, local, group=self.group)
+            stacked = torch.stack(parts)
+        out.copy_(stacked.permute(1, 0, 2, 3).reshape(out.shape))

@@ -37,7 +37,7 @@ class DecodeEngine:
     def __init__(self, *, batch: int, layers: int, kv_heads: int, group: int, head_dim: int,
                  ctx_cap_tokens: int, topk_pages: int, rerank_period: int,
                  profile: HeadProfile, dtype=torch.bfloat16, device="cuda",
-                 n_blocks: int | None = None, tiering: bool = False):
+                 n_blocks: int | None = None, tiering: bool = False, after_layer=None):
         if profile.n_layers != layers or profile.n_heads_per_layer != kv_heads:
             raise ValueError("profile grid does not match (layers, kv_heads)")
         self.B, self.L, self.H, self.G, self.D = batch, layers, kv_heads, group, head_dim
@@ -63,6 +63,9 @@ class DecodeEngine:
         self.v_new = torch.zeros_like(self.k_new)
         self.out = torch.zeros_like(self.q)
         self._graphs: dict[bool, torch.cuda.CUDAGraph] = {}
+        # per-layer hook after the attention launch (e.g. the head-sharded
+        # all-gather of outputs, dist.HeadGroup); captured into the step graph
+        self.after_layer = after_layer
         # two-tier mode (subsystem 4): stable heads keep only their selection in
         # HBM; every full page lives once in the pinned host tier
         self.tiering = tiering
@@ -135,7 +138,9 @@ class DecodeEngine:
             st.sparse_decode(layer, self.q[layer], self.out[layer], self.B,
                              max_pages=self.att_bound, extra_tokens=1, attend_appended=False,
                              k_new=self.k_new[layer], v_new=self.v_new[layer],
-                             kv_prefetch=not (scored or recycle))
+                             kv_prefetch=not (scored or recycle) and self.after_layer is None)
+            if self.after_layer is not None:
+                self.after_layer(layer)
         st.step_advance(self.B)
         if self.tiering:  # write-once offload of the page that just filled
             st.offload_filled(self.tier.host, self.unstable, self.tier.slow_resident, self.B)

@@ -54,3 +54,56 @@ def test_shard_rows_partition(total, world):
     flat = [x for rr in rows for x in rr]
     assert flat == list(range(total))
     assert max(map(len, rows)) - min(map(len, rows)) <= 1
+
+
+def _head_worker(rank, world, port, q):
+    try:
+        _head_body(rank, world, port, q)
+    except Exception as exc:  # surface worker failures instead of a queue timeout
+        q.put((rank, "error", repr(exc), None, None))
+
+
+def _head_body(rank, world, port, q):
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    fdist.init(backend="gloo")
+    H, G, D, B = 4, 7, 8, 6
+    heads, rows, group = fdist.head_shard_of(rank, world, H, B)
+    hg = fdist.HeadGroup(world, H)
+    # each rank "computes" outputs of its query heads: value = global q-head index
+    local = torch.stack([torch.full((len(heads) * G, D), 0.0)] * len(rows))
+    for i, h in enumerate(heads):
+        for g in range(G):
+            local[:, i * G + g] = h * G + g
+    out = torch.empty((len(rows), H * G, D))
+    hg.gather(local, out)
+    q.put((rank, list(heads), list(rows), group, out[:, :, 0].tolist()))
+    torch.distributed.destroy_process_group()
+
+
+def test_head_sharded_all_gather_gloo():
+    """config 5 plumbing: 2 ranks x 2 KV heads each, all-gather reassembles
+    the query heads in KV-head order on every rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_head_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r, heads, rows, group, gathered in out:
+        assert heads != "error", rows
+        assert heads == ([0, 1] if r == 0 else [2, 3]) and rows == list(range(6)) and group == [0, 1]
+        for row in gathered:
+            assert row == [float(i) for i in range(28)]
+
+
+def test_head_shard_layout():
+    assert fdist.head_shard_layout(8, 4) == (4, 2)   # Qwen2.5-7B on 8 GPUs: 4-way heads x 2 replicas
+    assert fdist.head_shard_layout(8, 8) == (8, 1)
+    assert fdist.head_shard_layout(1, 4) == (1, 1)
+    heads, rows, group = fdist.head_shard_of(5, 8, 4, 16)
+    assert list(heads) == [1] and rows == range(8, 16) and group == [4, 5, 6, 7]
