@@ -184,18 +184,17 @@ int fc_sparse_decode(const fc_store *s, int layer, const void *q, const void *k_
     const size_t need = attn_workspace_bytes(v, batch, grid);
     if (ws_bytes < need) return FC_E_CAPACITY;
     if (batch == 0) return FC_OK;
-    const size_t heads = (size_t)s->batch_cap * s->kv_heads;
-    const size_t parts = heads + (size_t)grid * 4;  // partial ids head + global warp (4 warps/CTA)
     AttnArgs a;
     a.layer = layer; a.q = q; a.k_new = k_new; a.v_new = v_new; a.out = out; a.lse = lse;
     a.scale_log2 = scale * 1.4426950408889634f;
     a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.max_splits = grid;
     a.kv_prefetch = kv_prefetch ? 1 : 0;
     char *w = (char *)workspace;
+    const size_t n = grid < 0 ? (size_t)(-grid) : 0;
     a.counters = (int32_t *)w;
-    a.part_m = (float *)(w + ((2 * heads * sizeof(int32_t) + 255) & ~(size_t)255));
-    a.part_l = a.part_m + parts * 16;
-    a.part_o = a.part_l + parts * 16;
+    a.part_m = (float *)(w + ((n * sizeof(int32_t) + 255) & ~(size_t)255));
+    a.part_l = a.part_m + n * 16;
+    a.part_o = a.part_l + n * 16;
     return cuda_status(launch_attn(v, s->dtype, a, batch, (cudaStream_t)stream));
 }
 
