@@ -1,0 +1,101 @@
+"""Size-independent properties at the BASELINE context length (32k tokens,
+2049 pages per head, K = 128 pages), where the full float64 oracle would be
+too slow to run on every head:
+
+* selections: ascending, unique, in range, contain the page being written,
+  |sel| == K for due heads (plus the page opened by the step advance);
+* selection == select_topk over the GPU's own scores (exact) for the last
+  scored layer;
+* summaries of every touched page == min/max of the keys read back from the
+  paged pool (bit-exact);
+* attention of sampled heads == float64 oracle on the GPU's selection (bf16 2e-2);
+* the page table stays injective and conserving.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import flexicache_oracle as O  # noqa: E402
+
+PS = 16
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def test_fullsize_32k_properties():
+    from paper_2511_00868_b200.engine import DecodeEngine
+    from paper_2511_00868_b200.stability import HeadProfile
+    from paper_2511_00868_b200.synthetic import device_normal
+    B, L, H, G, D, T, K, R = 2, 2, 8, 4, 128, 32768, 128, 4
+    prof = HeadProfile.first_n(L, H, 0.5)  # layer 0 unstable, layer 1 stable
+    eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=T + 64,
+                       topk_pages=K, rerank_period=R, profile=prof)
+    for b in range(B):
+        for l in range(L):
+            eng.prefill_layer(b, l, device_normal((H, T, D), seed=10 * b + 2 * l),
+                              device_normal((H, T, D), seed=10 * b + 2 * l + 1), alloc=(l == 0))
+    st = eng.store
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(3)
+    for step in range(12):
+        t = eng.t
+        eng.q.normal_(generator=gen)
+        eng.k_new.normal_(generator=gen)
+        eng.v_new.normal_(generator=gen)
+        eng.step()
+        st.check_errors()
+        sel, n_sel = st.sel.cpu().numpy(), st.n_sel.cpu().numpy()
+        seq = st.seq_len.cpu().numpy()
+        for b in range(B):
+            n_tok = int(seq[b])                       # tokens after the step
+            n_pages = -(-n_tok // PS)
+            n_alloc = n_tok // PS + 1                 # includes the page the next token opens
+            for l in range(L):
+                for h in range(H):
+                    s = sel[b, l, h, :n_sel[b, l, h]]
+                    assert np.all(np.diff(s) > 0) and s[0] >= 0 and s[-1] < n_alloc
+                    assert n_pages - 1 in s            # the page written this step
+                    due = step == 0 or prof.is_unstable((l, h)) or t % R == 0
+                    if due:
+                        extra = 1 if n_alloc > n_pages else 0
+                        assert len(s) == K + extra
+        # selection == select_topk over the GPU scores (layer 1 was scored last on rerank steps)
+        if t % R == 0 or step == 0:
+            scores = st.scores.cpu().numpy()
+            for bh in (0, 5, 9, 15):
+                b, h = divmod(bh, H)
+                n_pages = -(-int(seq[b]) // PS)
+                row = scores[bh, :n_pages - 1].astype(np.float64)
+                want = O.select_topk_fast(np.append(row, 0.0), K, (n_pages - 1,))
+                got = tuple(x for x in sel[b, 1, h, :n_sel[b, 1, h]].tolist() if x < n_pages)
+                assert got == want
+    # summaries + attention on sampled heads, against the keys read back from the pool
+    out = eng.out.double().cpu().numpy()
+    q = eng.q.double().cpu().numpy()
+    summ = st.summaries.double().cpu().numpy()
+    for (b, l, h) in ((0, 0, 3), (1, 1, 6)):
+        n_tok = int(seq[b])
+        n_pages = -(-n_tok // PS)
+        k, v = st.gather(b, l, h, n_pages)
+        k = k[:n_tok].double().cpu().numpy()
+        v = v[:n_tok].double().cpu().numpy()
+        mins, maxs, _ = O.minmax_build(k, PS)
+        assert np.array_equal(summ[b, l, h, :n_pages, 0], mins)
+        assert np.array_equal(summ[b, l, h, :n_pages, 1], maxs)
+        pages = [p for p in sel[b, l, h, :n_sel[b, l, h]].tolist() if p < n_pages]
+        # the last step attended the tokens present before its own advance
+        k_prev, v_prev = k[:n_tok], v[:n_tok]
+        want = O.gqa_sparse_decode(q[l, b, h * G:(h + 1) * G], k_prev, v_prev, PS, pages)
+        got = out[l, b, h * G:(h + 1) * G]
+        assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 2e-2
+    table = st.table.cpu().numpy()
+    live = table[table != 0]
+    assert np.unique(live).size == live.size
+    assert st.free_count() + live.size + 1 == st.n_blocks
