@@ -35,6 +35,7 @@ cudaError_t launch_attn(const StoreView &, int, const AttnArgs &, int, cudaStrea
 size_t attn_workspace_bytes(const StoreView &, int, int);
 cudaError_t set_attn_trace(void *);
 cudaError_t set_score_trace(void *);
+void set_score_mode(int);
 int attn_split(const StoreView &, int, int, int, int);
 size_t rerank_workspace_bytes(const StoreView &);
 cudaError_t launch_rerank(const StoreView &, int, const int32_t *, const int32_t *, const uint8_t *, int,

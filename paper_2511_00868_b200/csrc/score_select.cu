@@ -528,6 +528,157 @@ score_select_kernel(StoreView s, int layer, const T *__restrict__ q,
     if (trace && tid == 0) trace[blockIdx.x * 4 + 3] = gtimer_s();
 }
 
+// ---------------------------------------------------------------------------
+// Head-aligned scoring (batches with at least ~half as many heads as SMs):
+// one CTA of 16 warps per due head streams the head's summaries (one
+// contiguous [pages][min|max] run) through a ring of 64-page cp.async.bulk
+// chunks (~160 KiB in flight), writes the scores straight into shared-memory
+// keys and selects right away — no cross-CTA counter, no L2 round trip of the
+// scores, and each head's selection overlaps the other heads' streaming.
+
+#ifndef FC_HEAD_WARPS
+#define FC_HEAD_WARPS 16
+#endif
+#ifndef FC_HEAD_CHUNK_PAGES
+#define FC_HEAD_CHUNK_PAGES 64
+#endif
+#ifndef FC_HEAD_RING_KB
+#define FC_HEAD_RING_KB 160
+#endif
+constexpr int kHeadScoreWarps = FC_HEAD_WARPS;
+static int g_score_mode = -1;  // -1 auto, 0 balanced, 1 head-aligned (test hook)
+constexpr int kHeadChunkPages = FC_HEAD_CHUNK_PAGES;
+
+template <typename T, int D>
+struct HeadScoreGeom {
+    using Gm = ScoreGeom<T, D>;
+    static constexpr int kChunkBytes = kHeadChunkPages * Gm::kRecBytes;
+    static constexpr int kStages = (FC_HEAD_RING_KB * 1024) / kChunkBytes > 2 ? (FC_HEAD_RING_KB * 1024) / kChunkBytes : 2;
+    static constexpr int kRounds = kHeadChunkPages / (kHeadScoreWarps * Gm::kPagesPerSlot);  // per warp per chunk
+};
+
+template <typename T, int D>
+__global__ void __launch_bounds__(kHeadScoreWarps * 32, 1)
+score_head_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t *__restrict__ unstable,
+                  int period, int force_due, int topk, int extra_tokens, float *scores, int kv_prefetch) {
+    using Gm = ScoreGeom<T, D>;
+    using HG = HeadScoreGeom<T, D>;
+    constexpr int NW = kHeadScoreWarps, NS = HG::kStages, R = HG::kRounds;
+    constexpr int LPP = Gm::kLanesPerPage, CPL = Gm::kChunksPerLane, EPC = Gm::kElemsPerChunk;
+    static_assert(R >= 1 && R <= LPP, "chunk geometry");
+    extern __shared__ __align__(128) char dsm[];  // ring [NS][chunk] | keys [NCAP]
+    __shared__ __align__(8) uint64_t full[NS], empty[NS];
+    __shared__ float w[2 * D];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    griddep_launch_dependents();
+    if (!kv_prefetch) griddep_wait();
+    const int bh = blockIdx.x, b = bh / s.H, h = bh % s.H;
+    const bool due = force_due || unstable[layer * s.H + h] || (*s.step % period == 0);
+    const int n_tok = s.seq_len[b] + extra_tokens;
+    const int n_pages = n_tok > 0 ? (n_tok + s.PS - 1) / s.PS : 0;
+    const int hx = s.hix(b, layer, h);
+    if (!due || n_pages == 0) {
+        if (kv_prefetch) griddep_wait();
+        return;
+    }
+    int32_t *out = s.sel + (int64_t)hx * s.SELCAP;
+    if (n_pages <= topk) {  // budget covers every page
+        if (kv_prefetch) griddep_wait();
+        for (int i = tid; i < n_pages; i += blockDim.x) out[i] = i;
+        if (tid == 0) s.n_sel[hx] = n_pages;
+        return;
+    }
+    const int n_cand = n_pages - 1;  // the last page is pinned
+    const int n_chunks = (n_cand + kHeadChunkPages - 1) / kHeadChunkPages;
+    char *ring = dsm;
+    uint32_t *keys = reinterpret_cast<uint32_t *>(dsm + (size_t)NS * HG::kChunkBytes);
+    const char *base = reinterpret_cast<const char *>(s.summ) + (int64_t)hx * s.NCAP * Gm::kRecBytes;
+    if (tid == 0) {
+        for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], NW); }
+        fence_mbar_init();
+        for (int c = 0; c < min(NS, n_chunks); ++c) {
+            const uint32_t bytes = min(kHeadChunkPages, n_cand - c * kHeadChunkPages) * Gm::kRecBytes;
+            mbar_arrive_expect_tx(&full[c], bytes);
+            bulk_g2s(ring + (size_t)c * HG::kChunkBytes, base + (int64_t)c * HG::kChunkBytes, bytes, &full[c]);
+        }
+    }
+    if (kv_prefetch) griddep_wait();  // q comes from the previous launch
+    load_group_coeffs<T>(s, q, b, h, w);
+    __syncthreads();
+    const int sub = lane / LPP, cl = lane % LPP;
+    float coef[CPL][EPC];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) coef[c][e] = w[(cl + c * LPP) * EPC + e];
+    float *srow = scores + (int64_t)bh * s.NCAP;
+    for (int c = 0; c < n_chunks; ++c) {
+        const int stg = c % NS;
+        mbar_wait(&full[stg], (c / NS) & 1);
+        const char *chunk = ring + (size_t)stg * HG::kChunkBytes;
+        const int cp = min(kHeadChunkPages, n_cand - c * kHeadChunkPages);
+        float v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int p = (wid * R + r) * Gm::kPagesPerSlot + sub;  // page within the chunk
+            float acc = 0.f;
+            if (p < cp) {
+#pragma unroll
+                for (int cc = 0; cc < CPL; ++cc) {
+                    const uint4 raw = *reinterpret_cast<const uint4 *>(chunk + p * Gm::kRecBytes + (cl + cc * LPP) * 16);
+                    float f[EPC];
+                    chunk_to_f<T>(raw, f);
+#pragma unroll
+                    for (int e = 0; e < EPC; ++e) acc = fmaf(f[e], coef[cc][e], acc);
+                }
+            }
+            v[r] = acc;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stg]);  // this warp is done reading the stage
+        // transpose-reduce R values over LPP lanes
+        int ridx = 0;
+#pragma unroll
+        for (int dist = LPP / 2, cnt = R / 2; cnt >= 1; dist >>= 1, cnt >>= 1) {
+            const bool upper = (lane & dist) != 0;
+#pragma unroll
+            for (int i = 0; i < cnt; ++i) {
+                const float send = upper ? v[i] : v[i + cnt];
+                const float keep = upper ? v[i + cnt] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, dist);
+            }
+            if (upper) ridx += cnt;
+        }
+#pragma unroll
+        for (int dist = LPP / R / 2; dist > 0; dist >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], dist);
+        if ((cl & (LPP / R - 1)) == 0) {
+            const int p = (wid * R + ridx) * Gm::kPagesPerSlot + sub;
+            if (p < cp) {
+                const int gp = c * kHeadChunkPages + p;
+                keys[gp] = score_key(v[0]);
+                srow[gp] = v[0];
+            }
+        }
+        // refill this stage once every warp has released it
+        if (tid == 0 && c + NS < n_chunks) {
+            mbar_wait(&empty[stg], (c / NS) & 1);
+            fence_proxy_async_smem();
+            const int cn = c + NS;
+            const uint32_t bytes = min(kHeadChunkPages, n_cand - cn * kHeadChunkPages) * Gm::kRecBytes;
+            mbar_arrive_expect_tx(&full[stg], bytes);
+            bulk_g2s(ring + (size_t)stg * HG::kChunkBytes, base + (int64_t)cn * HG::kChunkBytes, bytes, &full[stg]);
+        }
+    }
+    if (tid == 0) srow[n_pages - 1] = -INFINITY;  // pinned page: not scored
+    __syncthreads();
+    const int kprime = topk - 1;  // n_pages > topk, so kprime < n_cand
+    if (kprime > 0) block_select<NW * 32>(keys, n_cand, kprime, out);
+    if (tid == 0) {
+        out[kprime] = n_pages - 1;
+        s.n_sel[hx] = topk;
+    }
+}
+
 // standalone select over caller scores: grid n_heads, block kScoreThreads
 __global__ void __launch_bounds__(kScoreThreads)
 select_topk_kernel(const float *scores, int stride, const int32_t *n_valid, int topk,
@@ -567,6 +718,32 @@ static cudaError_t launch_score_t(const StoreView &s, int layer, const void *q,
                                   int extra, float *scores, int32_t *counters, int do_select,
                                   int batch, int kv_prefetch, cudaStream_t st) {
     const int n_heads = batch * s.H;
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const bool head_mode = g_score_mode < 0 ? 2 * n_heads >= sms : g_score_mode == 1;
+    using HG = HeadScoreGeom<T, D>;
+    const size_t hsmem = (size_t)HG::kStages * HG::kChunkBytes + (size_t)s.NCAP * sizeof(uint32_t);
+    auto hk = score_head_kernel<T, D>;
+    static size_t hstatic = SIZE_MAX;
+    if (hstatic == SIZE_MAX) {
+        cudaFuncAttributes fa{};
+        if (cudaFuncGetAttributes(&fa, hk) != cudaSuccess) return cudaGetLastError();
+        hstatic = fa.sharedSizeBytes;
+    }
+    if (do_select && head_mode && hsmem + hstatic <= 227 * 1024) {  // head-aligned: one CTA per head
+        static size_t hcached = 0;
+        if (hcached != hsmem) {
+            if (cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem) != cudaSuccess)
+                return cudaGetLastError();
+            hcached = hsmem;
+        }
+        return launch_pdl(hk, dim3(n_heads), dim3(kHeadScoreWarps * 32), hsmem, st, s, layer, (const T *)q,
+                          unstable, period, force_due, topk, extra, scores, kv_prefetch);
+    }
     const size_t smem = (do_select ? (size_t)s.NCAP * sizeof(uint32_t) : 0) + (size_t)(n_heads + 1) * sizeof(int);
     auto kern = score_select_kernel<T, D>;
     static size_t cached_smem = (size_t)-1;
@@ -597,6 +774,8 @@ cudaError_t launch_score(const StoreView &s, int dtype, int layer, const void *q
         return launch_score_t<float, 128>(s, layer, q, unstable, period, force_due, topk, extra, scores, counters, do_select, batch, kv_prefetch, st);
     return launch_score_t<float, 64>(s, layer, q, unstable, period, force_due, topk, extra, scores, counters, do_select, batch, kv_prefetch, st);
 }
+
+void set_score_mode(int m) { g_score_mode = m; }
 
 cudaError_t set_score_trace(void *p) {
     return cudaMemcpyToSymbol(g_score_trace, &p, sizeof(p));

@@ -44,10 +44,30 @@ def timed(fn, reps=3):
 
 att_bytes = sum(eng.attention_bytes(l) for l in range(L)) / L
 sc_bytes = eng.scoring_bytes(0, 1)
+import ctypes  # noqa: E402
+from paper_2511_00868_b200 import _lib  # noqa: E402
+lib = _lib.load()
+lib.fc_debug_score_mode.argtypes = [ctypes.c_int]
+
+
+def moded(mode, fn):
+    def run(layer):
+        fn(layer)
+    lib.fc_debug_score_mode(mode)
+    try:
+        return timed(run)
+    finally:
+        lib.fc_debug_score_mode(-1)
+
+
 res = {
     "attn_us": timed(lambda l: st.sparse_decode(l, eng.q[l], eng.out[l], B, max_pages=eng.att_bound,
                                                  attend_appended=False)),
     "score_select_us": timed(lambda l: st.score_select(l, eng.q[l], eng.unstable, R, K, B, force_due=True)),
+    "score_select_bal_us": moded(0, lambda l: st.score_select(l, eng.q[l], eng.unstable, R, K, B, force_due=True)),
+    "score_select_head_us": moded(1, lambda l: st.score_select(l, eng.q[l], eng.unstable, R, K, B, force_due=True)),
+    "unstable_bal_us": moded(0, lambda l: st.score_select(l, eng.q[l], eng.unstable, R, K, B)),
+    "unstable_head_us": moded(1, lambda l: st.score_select(l, eng.q[l], eng.unstable, R, K, B)),
     "score_only_us": timed(lambda l: st.score_pages(l, eng.q[l], B, extra_tokens=1)),
 }
 res["attn_GBs"] = att_bytes / (res["attn_us"] * 1e-6) / 1e9

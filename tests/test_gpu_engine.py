@@ -154,3 +154,31 @@ def test_engine_tiered_rerank_fetch_matches_oracle():
                                             use_graph=True, tiering=True)
     assert int(eng.fetched_pages.item()) > 0
     eng.store.check_errors()
+
+
+@pytest.fixture
+def head_aligned_scoring():
+    """Force the head-aligned scoring kernel (one CTA per head) that the
+    launcher otherwise picks only when the batch has >= SMs/2 heads."""
+    import ctypes
+    from paper_2511_00868_b200 import _lib
+    lib = _lib.load()
+    lib.fc_debug_score_mode.argtypes = [ctypes.c_int]
+    lib.fc_debug_score_mode(1)
+    yield
+    lib.fc_debug_score_mode(-1)
+
+
+@pytest.mark.parametrize("dtype,D,G", [(torch.bfloat16, 128, 4), (torch.float32, 128, 4),
+                                       (torch.bfloat16, 64, 2), (torch.float32, 64, 7)])
+def test_engine_head_aligned_scoring_matches_oracle(head_aligned_scoring, dtype, D, G):
+    # T0 = 1500 tokens -> ~94 candidate pages: two 64-page chunks, the last partial
+    worst, ties, eng = run_engine_vs_oracle(B=2, L=2, H=2, G=G, D=D, T0=1500, steps=10, K=8,
+                                            R=4, frac=0.5, dtype=dtype, seed=11, use_graph=True,
+                                            ragged=True)
+    assert ties <= 2
+
+
+def test_engine_head_aligned_tiered(head_aligned_scoring):
+    run_engine_vs_oracle(B=2, L=2, H=4, G=4, D=128, T0=400, steps=16, K=6, R=4, frac=0.5,
+                         dtype=torch.bfloat16, seed=12, use_graph=True, tiering=True)

@@ -29,7 +29,22 @@ def _cuda():
         pytest.skip("needs a CUDA device")
 
 
-def test_fullsize_32k_properties():
+@pytest.mark.parametrize("score_mode", [0, 1])
+def test_fullsize_32k_properties(score_mode):
+    """score_mode 0: balanced multi-CTA scoring; 1: head-aligned (one CTA per
+    head streaming 2048 summaries through the 32-chunk smem ring)."""
+    import ctypes
+    from paper_2511_00868_b200 import _lib
+    lib = _lib.load()
+    lib.fc_debug_score_mode.argtypes = [ctypes.c_int]
+    lib.fc_debug_score_mode(score_mode)
+    try:
+        _run_fullsize()
+    finally:
+        lib.fc_debug_score_mode(-1)
+
+
+def _run_fullsize():
     from paper_2511_00868_b200.engine import DecodeEngine
     from paper_2511_00868_b200.stability import HeadProfile
     from paper_2511_00868_b200.synthetic import device_normal
