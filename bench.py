@@ -374,7 +374,7 @@ def run_ours(args, cfg):
                      "peak_source": peak_src, "avg_launch_us": att_avg_s * 1e6,
                      "isolated_launch_us": att_iso_s * 1e6, "alg_bytes_per_launch": att_alg,
                      "method": "32 layer launches back to back, one CUDA event pair, best of 3"},
-        "scoring": {"kernel": "fc_score_select (score_select_kernel), all heads due, 32 launches back to back",
+        "scoring": {"kernel": "fc_score_select (score_head_kernel: one CTA per head, bulk-copy ring + in-CTA select), all heads due, 32 launches back to back",
                     "us": sc_ms * 1e3, "alg_bytes": sc_bytes,
                     "achieved_gbs": sc_bytes / (sc_ms / 1e3) / 1e9},
         "clocks": clk.summary(),

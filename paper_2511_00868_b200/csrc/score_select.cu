@@ -542,6 +542,9 @@ score_select_kernel(StoreView s, int layer, const T *__restrict__ q,
 #ifndef FC_HEAD_CHUNK_PAGES
 #define FC_HEAD_CHUNK_PAGES 64
 #endif
+#ifndef FC_HEAD_LAST_REFILL
+#define FC_HEAD_LAST_REFILL 0
+#endif
 #ifndef FC_HEAD_RING_KB
 #define FC_HEAD_RING_KB 160
 #endif
@@ -568,6 +571,7 @@ score_head_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t
     static_assert(R >= 1 && R <= LPP, "chunk geometry");
     extern __shared__ __align__(128) char dsm[];  // ring [NS][chunk] | keys [NCAP]
     __shared__ __align__(8) uint64_t full[NS], empty[NS];
+    __shared__ int s_rel[NS];
     __shared__ float w[2 * D];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     griddep_launch_dependents();
@@ -594,7 +598,7 @@ score_head_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t
     uint32_t *keys = reinterpret_cast<uint32_t *>(dsm + (size_t)NS * HG::kChunkBytes);
     const char *base = reinterpret_cast<const char *>(s.summ) + (int64_t)hx * s.NCAP * Gm::kRecBytes;
     if (tid == 0) {
-        for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], NW); }
+        for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], NW); s_rel[i] = 0; }
         fence_mbar_init();
         for (int c = 0; c < min(NS, n_chunks); ++c) {
             const uint32_t bytes = min(kHeadChunkPages, n_cand - c * kHeadChunkPages) * Gm::kRecBytes;
@@ -635,7 +639,23 @@ score_head_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t
             v[r] = acc;
         }
         __syncwarp();
+#if FC_HEAD_LAST_REFILL
+        // the last warp to release the stage refills it (nobody blocks on it)
+        if (lane == 0) {
+            __threadfence_block();
+            const bool last = atomicAdd(&s_rel[stg], 1) == NW - 1;
+            if (last && c + NS < n_chunks) {
+                s_rel[stg] = 0;
+                fence_proxy_async_smem();
+                const int cn = c + NS;
+                const uint32_t bytes = min(kHeadChunkPages, n_cand - cn * kHeadChunkPages) * Gm::kRecBytes;
+                mbar_arrive_expect_tx(&full[stg], bytes);
+                bulk_g2s(ring + (size_t)stg * HG::kChunkBytes, base + (int64_t)cn * HG::kChunkBytes, bytes, &full[stg]);
+            }
+        }
+#else
         if (lane == 0) mbar_arrive(&empty[stg]);  // this warp is done reading the stage
+#endif
         // transpose-reduce R values over LPP lanes
         int ridx = 0;
 #pragma unroll
@@ -660,7 +680,7 @@ score_head_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t
             }
         }
         // refill this stage once every warp has released it
-        if (tid == 0 && c + NS < n_chunks) {
+        if (!FC_HEAD_LAST_REFILL && tid == 0 && c + NS < n_chunks) {
             mbar_wait(&empty[stg], (c / NS) & 1);
             fence_proxy_async_smem();
             const int cn = c + NS;
