@@ -148,7 +148,7 @@ def cpu_baseline(cfg, target_s=15.0):
     from oracle import cpu_ref
     cores = cpu_ref.host_cores()
     due = cpu_ref.due_fraction(cfg["unstable_fraction"], cfg["period"])
-    n_units = max(cores * 8, 64)
+    n_units = max(cores * 64, 256)  # ~10-20 core-seconds of float64 oracle work
     spu, n = cpu_ref.time_units(ctx=cfg["ctx"], heads=cfg["kv_heads"], d=cfg["head_dim"],
                                 g=cfg["group"], k=cfg["topk"], due_frac=due, n_units=n_units,
                                 cores=cores, repeats=2)
@@ -181,7 +181,7 @@ def run_reference(args, cfg):
         dt = time.perf_counter() - t0
     spu = dt / (args.steps * units_per_sample)
     step_s = spu * cfg["batch"] * cfg["layers"] * cfg["kv_heads"]
-    tps = cfg["batch"] * world / step_s if False else cfg["batch"] / step_s
+    tps = cfg["batch"] / step_s
     line = {"metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",

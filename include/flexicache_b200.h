@@ -185,13 +185,21 @@ int fc_select_topk(const float *scores, int stride, const int32_t *n_valid,
  * the previous kernel on the stream completes (programmatic dependent
  * launch); only q and k_new/v_new are waited for.  Valid when no kernel
  * between this layer's last selection/table update and this call is still
- * writing them (e.g. layers without a scoring launch this step). */
+ * writing them (e.g. layers without a scoring launch this step).
+ * early_unstable (optional, [layers][H] u8) with early_period: heads that
+ * the preceding fc_score_select of this layer does not select this step
+ * (not unstable and step % early_period != 0 — the same rerank_due rule)
+ * start without waiting for it, overlapping the scoring of the due heads;
+ * due heads wait as usual.  Pass null when a kernel other than that
+ * fc_score_select (e.g. fc_rerank_recycle) precedes the call. */
 size_t fc_sparse_decode_workspace_size(const fc_store *s, int batch,
                                        int max_pages, int n_ctas);
 int fc_sparse_decode(const fc_store *s, int layer, const void *q,
                      const void *k_new, const void *v_new, void *out,
                      float *lse, float scale, int extra_tokens,
-                     int attend_appended, int kv_prefetch, int max_pages, int n_ctas,
+                     int attend_appended, int kv_prefetch,
+                     const uint8_t *early_unstable, int early_period,
+                     int max_pages, int n_ctas,
                      void *workspace, size_t ws_bytes, int batch,
                      void *stream);
 

@@ -62,7 +62,7 @@ _SIGNATURES = {
     "fc_score_pages": (_i, [_p, _i, _p, _i, _p, _i, _p]),
     "fc_select_topk": (_i, [_p, _i, _p, _i, _i, _i, _p, _p, _p]),
     "fc_sparse_decode_workspace_size": (_sz, [_p, _i, _i, _i]),
-    "fc_sparse_decode": (_i, [_p, _i, _p, _p, _p, _p, _p, _f, _i, _i, _i, _i, _i, _p, _sz, _i, _p]),
+    "fc_sparse_decode": (_i, [_p, _i, _p, _p, _p, _p, _p, _f, _i, _i, _i, _p, _i, _i, _i, _p, _sz, _i, _p]),
     "fc_rerank_workspace_size": (_sz, [_p]),
     "fc_rerank_recycle": (_i, [_p, _i, _p, _p, _p, _i, _i, _i, _i, _p, _p, _i, _p, _p, _i, _p]),
     "fc_fetch_pages": (_i, [_p, _i, _p, _p, _p, _i, _p]),

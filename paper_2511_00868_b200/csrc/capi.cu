@@ -169,7 +169,8 @@ size_t fc_sparse_decode_workspace_size(const fc_store *s, int batch, int max_pag
 
 int fc_sparse_decode(const fc_store *s, int layer, const void *q, const void *k_new, const void *v_new,
                      void *out, float *lse, float scale, int extra_tokens, int attend_appended,
-                     int kv_prefetch, int max_pages, int n_ctas, void *workspace, size_t ws_bytes,
+                     int kv_prefetch, const uint8_t *early_unstable, int early_period,
+                     int max_pages, int n_ctas, void *workspace, size_t ws_bytes,
                      int batch, void *stream) {
     FC_CHECK(check_store(s));
     if (layer < 0 || layer >= s->layers) return invalid("layer out of range");
@@ -181,6 +182,7 @@ int fc_sparse_decode(const fc_store *s, int layer, const void *q, const void *k_
     if (max_pages < 1) return invalid("max_pages must be >= 1");
     if (!(scale > 0.f) || !std::isfinite(scale)) return invalid("scale must be positive");
     if (extra_tokens < 0 || extra_tokens > 1) return invalid("extra_tokens must be 0 or 1");
+    if (early_unstable && early_period < 1) return invalid("early_period must be >= 1");
     const StoreView v = make_view(s);
     const int grid = attn_split(v, s->dtype, batch, max_pages, n_ctas);
     const size_t need = attn_workspace_bytes(v, batch, grid);
@@ -191,6 +193,10 @@ int fc_sparse_decode(const fc_store *s, int layer, const void *q, const void *k_
     a.scale_log2 = scale * 1.4426950408889634f;
     a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.max_splits = grid;
     a.kv_prefetch = kv_prefetch ? 1 : 0;
+    // the balanced (grid < 0) variant shares workspace partials across launches:
+    // it never overlaps its predecessor
+    a.early_unstable = grid > 0 ? early_unstable : nullptr;
+    a.early_period = early_period;
     char *w = (char *)workspace;
     const size_t n = grid < 0 ? (size_t)(-grid) : 0;
     a.counters = (int32_t *)w;

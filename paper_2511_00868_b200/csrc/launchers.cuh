@@ -14,6 +14,8 @@ struct AttnArgs {
     int extra_tokens;
     int attend_appended;
     int kv_prefetch;      // stage KV pages before the previous launch completes
+    const uint8_t *early_unstable;  // [L][H]: heads not due this step skip the wait
+    int early_period;
     int max_splits;       // CTAs per head (cluster size S)
     int32_t *counters;    // [B_cap*H] partials published per head (zeroed once, self-resetting)
     float *part_m;        // [parts][16]

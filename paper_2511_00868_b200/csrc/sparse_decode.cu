@@ -413,8 +413,12 @@ attn_kernel(StoreView s, AttnArgs a, int S) {
     // Without kv_prefetch the selection / table / seq_len may come from the
     // previous launch: wait for it.  With kv_prefetch the caller guarantees
     // they do not, so pages are resolved and their loads issued while the
-    // previous kernel drains; only q and the new token wait.
-    if (!a.kv_prefetch) griddep_wait();
+    // previous kernel drains; only q and the new token wait.  A head the
+    // preceding scoring launch does not select this step (early_unstable)
+    // reads nothing that launch writes: it runs without waiting at all.
+    const bool early = a.early_unstable != nullptr && !a.early_unstable[a.layer * s.H + (blockIdx.x / S) % s.H] &&
+                       (*s.step % a.early_period) != 0;
+    if (!a.kv_prefetch && !early) griddep_wait();
     char *ring = dsm;
     float *s_q = reinterpret_cast<float *>(dsm + (size_t)NW * NST * Gm::kPageBytes);
     float *cstate = s_q + (sizeof(T) == 4 ? G * D : 0);  // [G][D] acc, then m[16], l[16]
@@ -467,7 +471,7 @@ attn_kernel(StoreView s, AttnArgs a, int S) {
     }
     const unsigned long long t_issued = trace ? gtimer() : 0ull;
 
-    if (a.kv_prefetch) griddep_wait();  // q and the new token come from the previous launch
+    if (a.kv_prefetch && !early) griddep_wait();  // q and the new token come from the previous launch
     if constexpr (sizeof(T) == 4) {
         const float *qg = reinterpret_cast<const float *>(a.q) + qoff;
         for (int i = tid; i < G * D; i += blockDim.x) s_q[i] = qg[i];
@@ -579,6 +583,9 @@ attn_kernel(StoreView s, AttnArgs a, int S) {
         }
         cluster.sync();  // keep every rank's shared memory alive until rank 0 is done
     }
+    // an early head still waits before exiting, so this launch completing
+    // implies the scoring launch (and everything before it) completed
+    if (early) griddep_wait();
     if (trace && tid == 0) {
         unsigned smid;
         asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
@@ -945,6 +952,9 @@ static int num_sms() {
 
 // CTAs per head (cluster size): the largest power of two <= 16 that keeps
 // heads * S within one wave and gives every warp at least two pages.
+#ifndef FC_ATTN_NO_BAL
+#define FC_ATTN_NO_BAL 0
+#endif
 int attn_split(const StoreView &s, int dtype, int batch, int max_pages, int n_ctas) {
     if (n_ctas > 0) return n_ctas;  // explicit split (profiling)
     const int n_heads = batch * s.H;
@@ -952,7 +962,7 @@ int attn_split(const StoreView &s, int dtype, int batch, int max_pages, int n_ct
     const int occ = FC_ATTN_DISPATCH(dtype, s.D, FC_OCC);
 #undef FC_OCC
     const int64_t slots = (int64_t)occ * num_sms();
-    if ((int64_t)n_heads * 2 <= slots) {  // far fewer heads than CTA slots: balanced all-SM variant
+    if (!FC_ATTN_NO_BAL && (int64_t)n_heads * 2 <= slots) {  // far fewer heads than CTA slots: balanced all-SM variant
 #define FC_BOCC(T, DD, N, W) attn_bal_ctas_per_sm_t<T, DD, N, W>(s, n_heads)
         const int bocc = FC_ATTN_DISPATCH(dtype, s.D, FC_BOCC);
 #undef FC_BOCC
@@ -964,6 +974,9 @@ int attn_split(const StoreView &s, int dtype, int batch, int max_pages, int n_ct
     return S;
 }
 
+#ifndef FC_ATTN_CLUSTER1
+#define FC_ATTN_CLUSTER1 0
+#endif
 template <typename T, int D, int NST, int NW>
 static cudaError_t launch_attn_t(const StoreView &s, const AttnArgs &a, int batch, cudaStream_t st) {
     const int n_heads = batch * s.H;
@@ -986,7 +999,7 @@ static cudaError_t launch_attn_t(const StoreView &s, const AttnArgs &a, int batc
     attr[1].val.clusterDim.y = 1;
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = (S > 1 || FC_ATTN_CLUSTER1) ? 2 : 1;  // S = 1: a plain launch
     return cudaLaunchKernelEx(&cfg, attn_kernel<T, D, NST, NW>, s, a, S);
 }
 

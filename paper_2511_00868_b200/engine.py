@@ -66,6 +66,9 @@ class DecodeEngine:
         # per-layer hook after the attention launch (e.g. the head-sharded
         # all-gather of outputs, dist.HeadGroup); captured into the step graph
         self.after_layer = after_layer
+        # attention of heads a layer's scoring launch does not select starts
+        # without waiting for it (fc_sparse_decode early_unstable)
+        self.early_heads = True
         # two-tier mode (subsystem 4): stable heads keep only their selection in
         # HBM; every full page lives once in the pinned host tier
         self.tiering = tiering
@@ -138,7 +141,10 @@ class DecodeEngine:
             st.sparse_decode(layer, self.q[layer], self.out[layer], self.B,
                              max_pages=self.att_bound, extra_tokens=1, attend_appended=False,
                              k_new=self.k_new[layer], v_new=self.v_new[layer],
-                             kv_prefetch=not (scored or recycle) and self.after_layer is None)
+                             kv_prefetch=not (scored or recycle) and self.after_layer is None,
+                             # heads the scoring launch leaves alone overlap it
+                             early_unstable=self.unstable if scored and not recycle and not force_due
+                             and self.early_heads else None, early_period=self.R)
             if self.after_layer is not None:
                 self.after_layer(layer)
         st.step_advance(self.B)

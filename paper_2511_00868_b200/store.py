@@ -181,13 +181,18 @@ class KVStore:
                       max_pages: int, n_ctas: int = 0, lse: torch.Tensor | None = None,
                       scale: float | None = None, extra_tokens: int = 1,
                       attend_appended: bool = True, k_new: torch.Tensor | None = None,
-                      v_new: torch.Tensor | None = None, kv_prefetch: bool = False) -> None:
-        """Split-K paged attention; with k_new/v_new the decode append is fused."""
+                      v_new: torch.Tensor | None = None, kv_prefetch: bool = False,
+                      early_unstable: torch.Tensor | None = None, early_period: int = 1) -> None:
+        """Split-K paged attention; with k_new/v_new the decode append is fused.
+        ``early_unstable`` (the [L, H] flags the preceding score_select used,
+        with its period): heads it does not select this step start without
+        waiting for it."""
         ws = self.attn_workspace(batch, max_pages, n_ctas)
         scale = 1.0 / math.sqrt(self.D) if scale is None else scale
         _lib.check(self.lib.fc_sparse_decode(
             self.cptr, layer, q.data_ptr(), _ptr(k_new), _ptr(v_new), out.data_ptr(), _ptr(lse),
-            scale, extra_tokens, int(attend_appended), int(kv_prefetch), max_pages, n_ctas, ws.data_ptr(),
+            scale, extra_tokens, int(attend_appended), int(kv_prefetch), _ptr(early_unstable),
+            early_period, max_pages, n_ctas, ws.data_ptr(),
             ws.numel(), batch, self.stream()), "fc_sparse_decode")
 
     # -- (4) rerank / tiers ------------------------------------------------------------

@@ -182,3 +182,36 @@ def test_engine_head_aligned_scoring_matches_oracle(head_aligned_scoring, dtype,
 def test_engine_head_aligned_tiered(head_aligned_scoring):
     run_engine_vs_oracle(B=2, L=2, H=4, G=4, D=128, T0=400, steps=16, K=6, R=4, frac=0.5,
                          dtype=torch.bfloat16, seed=12, use_graph=True, tiering=True)
+
+
+def test_early_heads_bitwise_equal_to_serialized():
+    """Attention of heads the scoring launch does not select starts without
+    waiting for it (PDL); the outputs, selections and summaries must be
+    bit-identical to the fully serialized schedule."""
+    from paper_2511_00868_b200.engine import DecodeEngine
+    from paper_2511_00868_b200.stability import HeadProfile
+    from paper_2511_00868_b200.synthetic import device_normal
+    B, L, H, G, D, T, K, R = 4, 4, 4, 4, 128, 3000, 16, 4
+    outs = []
+    for early in (False, True):
+        eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=T + 64,
+                           topk_pages=K, rerank_period=R, profile=HeadProfile.first_n(L, H, 0.25))
+        eng.early_heads = early
+        for b in range(B):
+            for l in range(L):
+                eng.prefill_layer(b, l, device_normal((H, T + 7 * b, D), seed=4 * b + l),
+                                  device_normal((H, T + 7 * b, D), seed=100 + 4 * b + l), alloc=(l == 0))
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(21)
+        rec = []
+        for step in range(10):
+            eng.q.normal_(generator=gen)
+            eng.k_new.normal_(generator=gen)
+            eng.v_new.normal_(generator=gen)
+            eng.step()
+            rec.append(eng.out.clone())
+        torch.cuda.synchronize()
+        eng.store.check_errors()
+        outs.append((torch.stack(rec), eng.store.sel.clone(), eng.store.summaries.clone()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
