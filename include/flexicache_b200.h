@@ -48,6 +48,7 @@ extern "C" {
 #define FC_ERR_SEL_CAP         16u  /* selection longer than sel_cap                 */
 #define FC_ERR_DOUBLE_EVICT    32u  /* ConsistencyError   (blocktable.py:319-322)    */
 #define FC_ERR_WRITE_TWICE     64u  /* ConsistencyError   (tiering.py:105-110 ledger) */
+#define FC_ERR_TRACE_SHORT    128u  /* trace capture: a selection shorter than K      */
 
 #define FC_NULL_BLOCK 0             /* blocktable.py:25 */
 
@@ -268,6 +269,34 @@ int fc_evict_unselected(const fc_store *s, const uint8_t *unstable, int batch,
  * (blocktable.py:280-294). */
 int fc_evict_pages(const fc_store *s, const int32_t *pages, int n_pages,
                    void *stream);
+
+/* ---- (f2) selection traces and head stability --------- */
+
+/* Copy the current top-K selection of every (row < batch, layer, head) into
+ * trace slot (*step - step_base) of a device trace buffer, skipped when the
+ * slot is outside [0, n_slots):
+ *   trace_sel  [batch_cap][n_slots][L][H][topk] u32 — FXTK records, layer-
+ *              major, head-minor (trace.py:1-19);
+ *   trace_pool [batch_cap][n_slots] u32 — candidate pool size,
+ *              ceil((seq_len + extra_tokens) / ps).
+ * Run after the step's scoring with every head due (a profiling step); a
+ * selection shorter than topk (pool <= K) sets FC_ERR_TRACE_SHORT and writes
+ * 0xffffffff.  Graph-capturable (the slot comes from the device step). */
+int fc_trace_capture(const fc_store *s, uint32_t *trace_sel, uint32_t *trace_pool,
+                     int step_base, int n_slots, int topk, int extra_tokens,
+                     int batch, void *stream);
+
+/* Integer core of the random-corrected overlap (stability.py:24-62) over a
+ * device trace sel [n_steps][L][H][topk] u32, pool [n_steps] u32:
+ * inter[l][h][w][delta-1] = |sel[starts[w]] ∩ sel[starts[w]+delta]| for
+ * delta in 1..window-1, or -1 when pool[starts[w]+delta] <= topk
+ * (degenerate pair).  starts: device int32 [n_windows], each with
+ * starts[w] + window - 1 < n_steps (checked by the caller); max_pool bounds
+ * every page index + 1 (indices at or above it never match). */
+int fc_trace_overlap(const uint32_t *sel, const uint32_t *pool, int n_steps,
+                     int layers, int kv_heads, int topk, const int32_t *starts,
+                     int n_windows, int window, int max_pool, int32_t *inter,
+                     void *stream);
 
 #ifdef __cplusplus
 }

@@ -27,6 +27,7 @@ FC_ERR_PAGES_CAP = 8
 FC_ERR_SEL_CAP = 16
 FC_ERR_DOUBLE_EVICT = 32
 FC_ERR_WRITE_TWICE = 64
+FC_ERR_TRACE_SHORT = 128
 
 _p = ctypes.c_void_p
 _i = ctypes.c_int
@@ -70,6 +71,8 @@ _SIGNATURES = {
     "fc_evict_pages": (_i, [_p, _p, _i, _p]),
     "fc_offload_filled": (_i, [_p, _p, _p, _p, _i, _p]),
     "fc_evict_unselected": (_i, [_p, _p, _i, _p]),
+    "fc_trace_capture": (_i, [_p, _p, _p, _i, _i, _i, _i, _i, _p]),
+    "fc_trace_overlap": (_i, [_p, _p, _i, _i, _i, _i, _p, _i, _i, _i, _p, _p]),
 }
 
 _lib = None

@@ -27,6 +27,8 @@ class Config:
     topk_pages: int = 64            # config.py:31
     unstable_fraction: float = 0.25  # config.py:32
     rerank_period: int = 16         # config.py:33
+    stability_window: int = 32      # config.py:34 (head profiling window, decode steps)
+    window_stride: int = 0          # config.py:35 (0 = non-overlapping windows)
     num_layers: int = 4             # config.py:37
     kv_heads_per_layer: int = 8     # config.py:38
     head_dim: int = 64              # config.py:39
@@ -36,14 +38,24 @@ class Config:
 
     def __post_init__(self):
         for name in ("page_size_tokens", "topk_pages", "rerank_period", "num_layers",
-                     "kv_heads_per_layer", "head_dim", "bytes_per_kv_element", "group_size"):
+                     "kv_heads_per_layer", "head_dim", "bytes_per_kv_element", "group_size",
+                     "stability_window"):
             v = getattr(self, name)
             if not isinstance(v, int) or v < 1:
                 raise ConfigError(f"{name} must be a positive integer, got {v!r}")
         if not 0.0 < self.unstable_fraction < 1.0:
             raise ConfigError(f"unstable_fraction must lie in (0, 1), got {self.unstable_fraction!r}")
+        if self.stability_window < 2:
+            raise ConfigError(f"stability_window must be >= 2, got {self.stability_window!r}")
+        if not isinstance(self.window_stride, int) or self.window_stride < 0:
+            raise ConfigError(f"window_stride must be a non-negative integer, got {self.window_stride!r}")
         if self.bytes_per_kv_element not in (2, 4):
             raise ConfigError("bytes_per_kv_element must be 2 (bf16) or 4 (fp32)")
+
+    @property
+    def stride(self) -> int:
+        """Window stride; 0 means non-overlapping (config.py:92-93)."""
+        return self.window_stride if self.window_stride else self.stability_window
 
     @property
     def n_heads(self) -> int:

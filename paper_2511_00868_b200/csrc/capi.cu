@@ -274,4 +274,29 @@ int fc_evict_pages(const fc_store *s, const int32_t *pages, int n_pages, void *s
     return cuda_status(launch_evict_pages(make_view(s), pages, n_pages, (cudaStream_t)stream));
 }
 
+int fc_trace_capture(const fc_store *s, uint32_t *trace_sel, uint32_t *trace_pool, int step_base,
+                     int n_slots, int topk, int extra_tokens, int batch, void *stream) {
+    FC_CHECK(check_store(s));
+    if (!trace_sel || !trace_pool) return invalid("null buffer");
+    if (n_slots < 1) return invalid("n_slots must be >= 1");
+    if (topk < 1 || topk > s->sel_cap) return invalid("topk must be in 1..sel_cap");
+    if (extra_tokens < 0 || extra_tokens > 1) return invalid("extra_tokens must be 0 or 1");
+    if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
+    return cuda_status(launch_trace_capture(make_view(s), trace_sel, trace_pool, step_base, n_slots, topk,
+                                            extra_tokens, batch, (cudaStream_t)stream));
+}
+
+int fc_trace_overlap(const uint32_t *sel, const uint32_t *pool, int n_steps, int layers, int kv_heads,
+                     int topk, const int32_t *starts, int n_windows, int window, int max_pool,
+                     int32_t *inter, void *stream) {
+    if (!sel || !pool || !starts || !inter) return invalid("null buffer");
+    if (layers < 1 || kv_heads < 1 || topk < 1) return invalid("zero dimension");
+    if (window < 2) return invalid("window must be >= 2");
+    if (n_windows < 0 || window > n_steps) return invalid("window longer than the trace");
+    if (max_pool < 1 || max_pool > 8 * 200 * 1024) return invalid("max_pool out of range (1..1638400)");
+    if (n_windows == 0) return FC_OK;
+    return cuda_status(launch_trace_overlap(sel, pool, layers, kv_heads, topk, starts, n_windows, window,
+                                            max_pool, inter, (cudaStream_t)stream));
+}
+
 }  // extern "C"

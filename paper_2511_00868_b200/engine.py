@@ -62,13 +62,17 @@ class DecodeEngine:
         self.k_new = torch.zeros((layers, batch, kv_heads, head_dim), dtype=dtype, device=self.device)
         self.v_new = torch.zeros_like(self.k_new)
         self.out = torch.zeros_like(self.q)
-        self._graphs: dict[bool, torch.cuda.CUDAGraph] = {}
+        self._graphs: dict[tuple, torch.cuda.CUDAGraph] = {}  # (rerank, score_all_heads)
         # per-layer hook after the attention launch (e.g. the head-sharded
         # all-gather of outputs, dist.HeadGroup); captured into the step graph
         self.after_layer = after_layer
         # attention of heads a layer's scoring launch does not select starts
         # without waiting for it (fc_sparse_decode early_unstable)
         self.early_heads = True
+        # profiling: score every head every step and record
+        # the selections on the device (trace.TraceRecorder)
+        self.score_all_heads = False
+        self.recorder = None
         # two-tier mode (subsystem 4): stable heads keep only their selection in
         # HBM; every full page lives once in the pinned host tier
         self.tiering = tiering
@@ -148,6 +152,8 @@ class DecodeEngine:
             if self.after_layer is not None:
                 self.after_layer(layer)
         st.step_advance(self.B)
+        if self.recorder is not None:
+            self.recorder.capture()
         if self.tiering:  # write-once offload of the page that just filled
             st.offload_filled(self.tier.host, self.unstable, self.tier.slow_resident, self.B)
 
@@ -170,21 +176,28 @@ class DecodeEngine:
                 self.store.evict_unselected(self.unstable, self.B)
             self.selected = True
         elif use_graph:
-            g = self._graphs.get(rerank)
+            g = self._graphs.get((rerank, self.score_all_heads))
             if g is None:
                 g = self._capture(rerank)
             g.replay()
         else:
-            self._launch_step(rerank, force_due=False)
+            self._launch_step(rerank, force_due=self.score_all_heads)
         self.t += 1
         self.seq_host = [s + 1 for s in self.seq_host]
         return self.out
+
+    def attach_recorder(self, recorder) -> None:
+        """Record top-K traces from the next step on (every head scored every
+        step while attached); ``None`` detaches.  Step graphs are re-captured."""
+        self.recorder = recorder
+        self.score_all_heads = recorder is not None
+        self._graphs.clear()
 
     def capture_graphs(self) -> None:
         """Capture both step graphs now (rerank and plain), so no capture or
         instantiation happens inside a timed region."""
         for rerank in (False, True):
-            if rerank not in self._graphs:
+            if (rerank, self.score_all_heads) not in self._graphs:
                 self._capture(rerank)
 
     def _capture(self, rerank: bool) -> torch.cuda.CUDAGraph:
@@ -196,10 +209,10 @@ class DecodeEngine:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(s):
             with torch.cuda.graph(g, stream=s):
-                self._launch_step(rerank, force_due=False)
+                self._launch_step(rerank, force_due=self.score_all_heads)
         torch.cuda.current_stream(self.device).wait_stream(s)
         torch.cuda.synchronize(self.device)
-        self._graphs[rerank] = g
+        self._graphs[(rerank, self.score_all_heads)] = g
         return g
 
     def launches_per_step(self, t: int) -> int:

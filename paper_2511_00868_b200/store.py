@@ -110,6 +110,8 @@ class KVStore:
                 f"(device error bits {bits:#x})")
         if bits & _lib.FC_ERR_NULL_WRITE:
             raise ConsistencyError("append into a page with no physical block")
+        if bits & _lib.FC_ERR_TRACE_SHORT:
+            raise ValueError("trace capture: a selection shorter than K (candidate pool <= K)")
         raise ValueError(f"capacity exceeded (device error bits {bits:#x})")
 
     def free_count(self) -> int:
@@ -214,6 +216,14 @@ class KVStore:
             int(force_due), int(old_has_tail), extra_tokens, _ptr(slow_resident),
             copies.data_ptr(), copies.shape[0], n_copies.data_ptr(), ws.data_ptr(), batch,
             self.stream()), "fc_rerank_recycle")
+
+    def trace_capture(self, trace_sel: torch.Tensor, trace_pool: torch.Tensor, step_base: int,
+                      topk: int, batch: int, extra_tokens: int = 0) -> None:
+        """Record every head's top-K selection into trace slot
+        (device step - step_base) — fc_trace_capture."""
+        _lib.check(self.lib.fc_trace_capture(self.cptr, trace_sel.data_ptr(), trace_pool.data_ptr(),
+                                             step_base, trace_sel.shape[1], topk, extra_tokens, batch,
+                                             self.stream()), "fc_trace_capture")
 
     def fetch_pages(self, layer: int, host_pages: torch.Tensor, copies: torch.Tensor,
                     n_copies: torch.Tensor) -> None:

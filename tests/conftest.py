@@ -24,3 +24,16 @@ def golden_arrays():
 def golden_cases():
     with open(os.path.join(GOLDEN, "golden_cases.json")) as fh:
         return json.load(fh)
+
+
+@pytest.fixture(scope="session")
+def trace_golden():
+    """Reference stability reports / classifications / load errors on the
+    committed FXTK fixtures (tests/golden/make_golden_trace.py)."""
+    with open(os.path.join(GOLDEN, "trace_golden.json")) as fh:
+        return json.load(fh)
+
+
+def golden_blob(name):
+    with open(os.path.join(GOLDEN, name), "rb") as fh:
+        return fh.read()
