@@ -8,8 +8,8 @@ include/flexicache_b200.h; PyTorch provides device memory and streams.
 """
 
 from .config import Config, HeadId, all_heads, pages_for_tokens
-from .errors import (AdmissionError, ConfigError, ConsistencyError, PoolExhausted,
-                     TierKVError)
+from .errors import (AdmissionError, ConfigError, ConsistencyError, DegeneratePoolError,
+                     PoolExhausted, TierKVError, TraceFormatError)
 
 __version__ = "0.1.0"
 
@@ -23,6 +23,11 @@ _LAZY = {
     "sparsity_error": ".attention", "BlockTable": ".blocktable",
     "PhysicalPool": ".blocktable", "RecyclePlan": ".blocktable", "NULL_BLOCK": ".blocktable",
     "promoted_delta": ".tiering", "TierStore": ".tiering",
+    "TopKTrace": ".trace", "save_trace": ".trace", "load_trace": ".trace",
+    "TraceRecorder": ".trace", "rco": ".stability", "temporal_stability": ".stability",
+    "StabilityReport": ".stability", "compute_stability_report": ".stability",
+    "classify_heads": ".stability", "cross_task_overlap": ".stability",
+    "save_overlap_csv": ".stability",
 }
 
 
@@ -35,4 +40,5 @@ def __getattr__(name):
 
 
 __all__ = sorted(["Config", "HeadId", "all_heads", "pages_for_tokens", "AdmissionError",
-                  "ConfigError", "ConsistencyError", "PoolExhausted", "TierKVError", *_LAZY])
+                  "ConfigError", "ConsistencyError", "DegeneratePoolError", "PoolExhausted",
+                  "TierKVError", "TraceFormatError", *_LAZY])

@@ -66,6 +66,9 @@ int fc_debug_attn_trace(void *device_buf) { return cuda_status(set_attn_trace(de
 int fc_debug_score_trace(void *device_buf) { return cuda_status(set_score_trace(device_buf)); }
 /* test hook: scoring kernel choice, -1 auto, 0 balanced, 1 head-aligned */
 int fc_debug_score_mode(int mode) { set_score_mode(mode); return FC_OK; }
+/* test hook: attention variant, 0 cluster per head (default), 1 balanced
+ * all-SM variant for small head counts */
+int fc_debug_attn_mode(int mode) { set_attn_mode(mode); return FC_OK; }
 
 int fc_alloc_pages(const fc_store *s, int row, int first_page, int n_pages, void *stream) {
     FC_CHECK(check_store(s));

@@ -38,6 +38,7 @@ size_t attn_workspace_bytes(const StoreView &, int, int);
 cudaError_t set_attn_trace(void *);
 cudaError_t set_score_trace(void *);
 void set_score_mode(int);
+void set_attn_mode(int);
 cudaError_t launch_trace_capture(const StoreView &, uint32_t *, uint32_t *, int, int, int, int, int, cudaStream_t);
 cudaError_t launch_trace_overlap(const uint32_t *, const uint32_t *, int, int, int, const int32_t *, int, int,
                                  int, int32_t *, cudaStream_t);

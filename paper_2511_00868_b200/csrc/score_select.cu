@@ -549,7 +549,10 @@ score_select_kernel(StoreView s, int layer, const T *__restrict__ q,
 #define FC_HEAD_RING_KB 160
 #endif
 constexpr int kHeadScoreWarps = FC_HEAD_WARPS;
-static int g_score_mode = -1;  // -1 auto, 0 balanced, 1 head-aligned (test hook)
+#ifndef FC_SCORE_MODE_DEFAULT
+#define FC_SCORE_MODE_DEFAULT -1
+#endif
+static int g_score_mode = FC_SCORE_MODE_DEFAULT;  // -1 auto, 0 balanced, 1 head-aligned (test hook)
 constexpr int kHeadChunkPages = FC_HEAD_CHUNK_PAGES;
 
 template <typename T, int D>

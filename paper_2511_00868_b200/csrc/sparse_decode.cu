@@ -952,9 +952,16 @@ static int num_sms() {
 
 // CTAs per head (cluster size): the largest power of two <= 16 that keeps
 // heads * S within one wave and gives every warp at least two pages.
-#ifndef FC_ATTN_NO_BAL
-#define FC_ATTN_NO_BAL 0
+// Variant choice: 0 = cluster-per-head kernel always (default: measured faster
+// than the balanced variant at 32-128 heads and equal within noise at 8-16);
+// 1 = balanced all-SM variant whenever heads <= half the CTA slots; -1 = that
+// rule too (kept for the test hook).
+#ifndef FC_ATTN_MODE_DEFAULT
+#define FC_ATTN_MODE_DEFAULT 0
 #endif
+static int g_attn_mode = FC_ATTN_MODE_DEFAULT;
+void set_attn_mode(int m) { g_attn_mode = m; }
+
 int attn_split(const StoreView &s, int dtype, int batch, int max_pages, int n_ctas) {
     if (n_ctas > 0) return n_ctas;  // explicit split (profiling)
     const int n_heads = batch * s.H;
@@ -962,7 +969,7 @@ int attn_split(const StoreView &s, int dtype, int batch, int max_pages, int n_ct
     const int occ = FC_ATTN_DISPATCH(dtype, s.D, FC_OCC);
 #undef FC_OCC
     const int64_t slots = (int64_t)occ * num_sms();
-    if (!FC_ATTN_NO_BAL && (int64_t)n_heads * 2 <= slots) {  // far fewer heads than CTA slots: balanced all-SM variant
+    if (g_attn_mode != 0 && (int64_t)n_heads * 2 <= slots) {  // far fewer heads than CTA slots: balanced all-SM variant
 #define FC_BOCC(T, DD, N, W) attn_bal_ctas_per_sm_t<T, DD, N, W>(s, n_heads)
         const int bocc = FC_ATTN_DISPATCH(dtype, s.D, FC_BOCC);
 #undef FC_BOCC

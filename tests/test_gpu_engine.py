@@ -215,3 +215,29 @@ def test_early_heads_bitwise_equal_to_serialized():
         outs.append((torch.stack(rec), eng.store.sel.clone(), eng.store.summaries.clone()))
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.fixture
+def balanced_attention():
+    """Force the balanced all-SM attention variant (not auto-selected: the
+    cluster-per-head kernel measured faster) so it stays covered."""
+    import ctypes
+    from paper_2511_00868_b200 import _lib
+    lib = _lib.load()
+    lib.fc_debug_attn_mode.argtypes = [ctypes.c_int]
+    lib.fc_debug_attn_mode(1)
+    yield
+    lib.fc_debug_attn_mode(0)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_engine_balanced_attention_matches_oracle(balanced_attention, dtype):
+    worst, ties, eng = run_engine_vs_oracle(B=3, L=2, H=2, G=4, D=128, T0=700, steps=12, K=8,
+                                            R=4, frac=0.5, dtype=dtype, seed=13, use_graph=True,
+                                            ragged=True)
+    assert ties <= 2
+
+
+def test_engine_balanced_attention_tiered(balanced_attention):
+    run_engine_vs_oracle(B=2, L=2, H=4, G=7, D=128, T0=400, steps=16, K=6, R=4, frac=0.5,
+                         dtype=torch.bfloat16, seed=14, use_graph=True, tiering=True)
