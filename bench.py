@@ -292,8 +292,16 @@ def run_ours(args, cfg):
             best = min(best, a.elapsed_time(b_) / L)
         return best / 1e3
 
+    # as in the step graph: the fused append, and (a launch whose predecessor
+    # never writes its selection / table) KV staged while the previous layer
+    # drains (kv_prefetch, used for every unscored layer of a step)
     att_avg_s = time_launches(lambda l: eng.store.sparse_decode(
-        l, eng.q[l], eng.out[l], B, max_pages=eng.att_bound, extra_tokens=1, attend_appended=False))
+        l, eng.q[l], eng.out[l], B, max_pages=eng.att_bound, extra_tokens=1, attend_appended=False,
+        k_new=eng.k_new[l], v_new=eng.v_new[l], kv_prefetch=l > 0))
+    # the same launches without the early staging (as after a scoring launch)
+    att_serial_s = time_launches(lambda l: eng.store.sparse_decode(
+        l, eng.q[l], eng.out[l], B, max_pages=eng.att_bound, extra_tokens=1, attend_appended=False,
+        k_new=eng.k_new[l], v_new=eng.v_new[l]))
     iso = []
     torch.cuda._sleep(100_000_000)
     for l in range(L):
@@ -373,7 +381,10 @@ def run_ours(args, cfg):
                      "frac": achieved / peak, "traffic": _traffic(), "kernel": "fc_sparse_decode (attn_kernel)",
                      "peak_source": peak_src, "avg_launch_us": att_avg_s * 1e6,
                      "isolated_launch_us": att_iso_s * 1e6, "alg_bytes_per_launch": att_alg,
-                     "method": "32 layer launches back to back, one CUDA event pair, best of 3"},
+                     "serialized_launch_us": att_serial_s * 1e6,
+                     "method": "32 layer launches back to back as in the step graph (fused append, KV "
+                               "staged while the previous layer drains), one CUDA event pair, best of 3; "
+                               "serialized_launch_us: same without early staging (layers after a scoring launch)"},
         "scoring": {"kernel": "fc_score_select (score_head_kernel: one CTA per head, bulk-copy ring + in-CTA select), all heads due, 32 launches back to back",
                     "us": sc_ms * 1e3, "alg_bytes": sc_bytes,
                     "achieved_gbs": sc_bytes / (sc_ms / 1e3) / 1e9},

@@ -49,6 +49,7 @@ extern "C" {
 #define FC_ERR_DOUBLE_EVICT    32u  /* ConsistencyError   (blocktable.py:319-322)    */
 #define FC_ERR_WRITE_TWICE     64u  /* ConsistencyError   (tiering.py:105-110 ledger) */
 #define FC_ERR_TRACE_SHORT    128u  /* trace capture: a selection shorter than K      */
+#define FC_ERR_RUN_RANGE      256u  /* fc_sparse_decode_layers: warp range overflow (sizing bug) */
 
 #define FC_NULL_BLOCK 0             /* blocktable.py:25 */
 
@@ -203,6 +204,36 @@ int fc_sparse_decode(const fc_store *s, int layer, const void *q,
                      int max_pages, int n_ctas,
                      void *workspace, size_t ws_bytes, int batch,
                      void *stream);
+
+/* Persistent form of fc_sparse_decode for a run of consecutive layers
+ * [layer_begin, layer_begin + n_layers) in ONE launch (same semantics per
+ * (layer, head) as fc_sparse_decode: sparse_decode, attention.py:85-111, the
+ * attended set of simulator.py:416-420,512, fused update_minmax,
+ * scoring.py:59-69).  One CTA per SM; every layer's attended pages are cut
+ * into equal ranges over all warps of the grid; a grid barrier separates
+ * layers (layer i's q and new token are consumed only after every output of
+ * layer i-1 is written) while page copies run ahead across it.  Layer
+ * layer_begin + i reads q + i*q_layer_stride, k_new/v_new + i*kv_layer_stride
+ * and writes out + i*out_layer_stride (elements), lse + i*lse_layer_stride
+ * (optional).  No layer of the run may need a selection / table update
+ * between layers (scoring, recycle): the host splits runs there.
+ * first_dep = 1 when the previous launch on the stream writes layer
+ * layer_begin's selection or table (its pages are then resolved after it
+ * completes).  max_pages bounds the attended pages of any head.
+ * Returns FC_E_UNSUPPORTED when the geometry does not fit (more than 256
+ * heads per layer, or shared memory): callers use fc_sparse_decode.
+ * workspace: fc_sparse_decode_layers_workspace_size() bytes, zeroed once
+ * (its counters reset themselves). */
+int fc_sparse_decode_layers_supported(const fc_store *s, int batch, int max_pages);
+size_t fc_sparse_decode_layers_workspace_size(const fc_store *s, int batch, int max_pages);
+int fc_sparse_decode_layers(const fc_store *s, int layer_begin, int n_layers,
+                            const void *q, int64_t q_layer_stride,
+                            const void *k_new, const void *v_new, int64_t kv_layer_stride,
+                            void *out, int64_t out_layer_stride,
+                            float *lse, int64_t lse_layer_stride,
+                            float scale, int extra_tokens, int attend_appended,
+                            int first_dep, int max_pages,
+                            void *workspace, size_t ws_bytes, int batch, void *stream);
 
 /* ---- (4) stable-head rerank: recycle + tier copies ---------------------- */
 

@@ -32,6 +32,7 @@ FC_ERR_TRACE_SHORT = 128
 _p = ctypes.c_void_p
 _i = ctypes.c_int
 _f = ctypes.c_float
+_i64 = ctypes.c_int64
 _sz = ctypes.c_size_t
 
 
@@ -64,6 +65,10 @@ _SIGNATURES = {
     "fc_select_topk": (_i, [_p, _i, _p, _i, _i, _i, _p, _p, _p]),
     "fc_sparse_decode_workspace_size": (_sz, [_p, _i, _i, _i]),
     "fc_sparse_decode": (_i, [_p, _i, _p, _p, _p, _p, _p, _f, _i, _i, _i, _p, _i, _i, _i, _p, _sz, _i, _p]),
+    "fc_sparse_decode_layers_supported": (_i, [_p, _i, _i]),
+    "fc_sparse_decode_layers_workspace_size": (_sz, [_p, _i, _i]),
+    "fc_sparse_decode_layers": (_i, [_p, _i, _i, _p, _i64, _p, _p, _i64, _p, _i64, _p, _i64, _f, _i, _i, _i, _i,
+                                     _p, _sz, _i, _p]),
     "fc_rerank_workspace_size": (_sz, [_p]),
     "fc_rerank_recycle": (_i, [_p, _i, _p, _p, _p, _i, _i, _i, _i, _p, _p, _i, _p, _p, _i, _p]),
     "fc_fetch_pages": (_i, [_p, _i, _p, _p, _p, _i, _p]),

@@ -1,0 +1,400 @@
+// attn_warp.cuh — per-warp page attention state (bf16 tensor-core and fp32
+// CUDA-core paths), the fused append, and per-head attended-set arithmetic,
+// shared by the per-layer attention kernels (sparse_decode.cu) and the
+// persistent multi-layer kernel (attn_run.cu).
+//
+// Reference semantics: _attend / sparse_decode (attention.py:67-111),
+// update_minmax (scoring.py:59-69), the stable-head attended set
+// (simulator.py:416-420,512).
+#pragma once
+#include "launchers.cuh"
+#include <type_traits>
+
+namespace fc {
+
+template <typename T, int D>
+struct AttnGeom {
+    static constexpr int kPageBytes = 2 * kPageSize * D * (int)sizeof(T);
+    static constexpr int kHalfBytes = kPageSize * D * (int)sizeof(T);
+};
+
+// ---------------------------------------------------------------------------
+// per-warp page processing
+
+// bf16 tensor-core path.  Query rows: r0 = lane/4 and r1 = lane/4 + 8 (G<=16).
+template <int D>
+struct Bf16Warp {
+    uint32_t qa[D / 16][4];
+    float acc[D / 8][4];
+    float m[2], l[2];
+
+    FC_DEVINL void init(const __nv_bfloat16 *qrow0, int G, int lane) {
+        const int r0 = lane >> 2, r1 = r0 + 8, c = (lane & 3) * 2;
+        const uint32_t *q0 = reinterpret_cast<const uint32_t *>(qrow0 + (int64_t)r0 * D);
+        const uint32_t *q1 = reinterpret_cast<const uint32_t *>(qrow0 + (int64_t)r1 * D);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+            qa[kk][0] = r0 < G ? q0[(kk * 16 + c) / 2] : 0u;
+            qa[kk][1] = r1 < G ? q1[(kk * 16 + c) / 2] : 0u;
+            qa[kk][2] = r0 < G ? q0[(kk * 16 + 8 + c) / 2] : 0u;
+            qa[kk][3] = r1 < G ? q1[(kk * 16 + 8 + c) / 2] : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < D / 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+        m[0] = m[1] = -INFINITY;
+        l[0] = l[1] = 0.f;
+    }
+
+    FC_DEVINL void page(char *stage, int ntok, float scale_log2, int lane) {
+        constexpr int RB = D * 2;  // row bytes
+        const uint32_t kb = smem_u32(stage);
+        const uint32_t vb = kb + kPageSize * RB;
+        if (ntok < kPageSize) {  // zero V rows past the fill (P=0 there, garbage could be NaN)
+            uint4 *vz = reinterpret_cast<uint4 *>(stage + kPageSize * RB + ntok * RB);
+            const int n16 = (kPageSize - ntok) * RB / 16;
+            for (int i = lane; i < n16; i += 32) vz[i] = make_uint4(0, 0, 0, 0);
+            __syncwarp();
+        }
+        const int mi = lane >> 3, ri = lane & 7;
+        // S = Q Kᵀ over 16 tokens: two n-tiles of 8 tokens
+        float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        {
+            // two accumulator chains per n-tile (even / odd k-steps) halve the
+            // dependent-HMMA latency of the page
+            float s2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+            const int t = (mi >> 1) * 8 + ri;
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+                const int c = 2 * kk + (mi & 1);
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(kb + t * RB + ((c ^ (t & 7)) << 4), b0, b1, b2, b3);
+                if (kk & 1) {
+                    mma_bf16_16816(s2[0], qa[kk], b0, b1);
+                    mma_bf16_16816(s2[1], qa[kk], b2, b3);
+                } else {
+                    mma_bf16_16816(s[0], qa[kk], b0, b1);
+                    mma_bf16_16816(s[1], qa[kk], b2, b3);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) s[j][e] += s2[j][e];
+        }
+        // online softmax; C-frag: s[j][0..1] row r0, s[j][2..3] row r1,
+        // token j*8 + (lane&3)*2 + {0,1}
+        const int tc = (lane & 3) * 2;
+        float x[2][4];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int tok = j * 8 + tc + (e & 1);
+                x[j][e] = tok < ntok ? s[j][e] * scale_log2 : -INFINITY;
+            }
+        float alpha[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            float mx = fmaxf(fmaxf(x[0][2 * r], x[0][2 * r + 1]), fmaxf(x[1][2 * r], x[1][2 * r + 1]));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            const float mn = fmaxf(m[r], mx);
+            alpha[r] = exp2f(m[r] - mn);  // m = -inf on the first page -> 0
+            m[r] = mn;
+        }
+        float p[2][4];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) p[j][e] = exp2f(x[j][e] - m[e >> 1]);
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+            l[r] = l[r] * alpha[r] + (p[0][2 * r] + p[0][2 * r + 1] + p[1][2 * r] + p[1][2 * r + 1]);
+#pragma unroll
+        for (int i = 0; i < D / 8; ++i) {
+            acc[i][0] *= alpha[0]; acc[i][1] *= alpha[0];
+            acc[i][2] *= alpha[1]; acc[i][3] *= alpha[1];
+        }
+        uint32_t pa[4];
+        pa[0] = pack_bf16x2(p[0][0], p[0][1]);
+        pa[1] = pack_bf16x2(p[0][2], p[0][3]);
+        pa[2] = pack_bf16x2(p[1][0], p[1][1]);
+        pa[3] = pack_bf16x2(p[1][2], p[1][3]);
+        // O += P V: B = V (k = token, n = column), ldmatrix.trans
+        {
+            const int t = (mi & 1) * 8 + ri;
+#pragma unroll
+            for (int dc = 0; dc < D / 16; ++dc) {
+                const int c = 2 * dc + (mi >> 1);
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_t(vb + t * RB + ((c ^ (t & 7)) << 4), b0, b1, b2, b3);
+                mma_bf16_16816(acc[2 * dc], pa, b0, b1);
+                mma_bf16_16816(acc[2 * dc + 1], pa, b2, b3);
+            }
+        }
+    }
+
+    FC_DEVINL void finalize() {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            l[r] += __shfl_xor_sync(0xffffffffu, l[r], 1);
+            l[r] += __shfl_xor_sync(0xffffffffu, l[r], 2);
+        }
+    }
+
+    // partial (unnormalised acc, running max m, sum l) of rows < G
+    FC_DEVINL void store_partial(float *po, float *pm, float *pl, int G, int lane) {
+        const int r0 = lane >> 2, c = (lane & 3) * 2;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int g = r0 + 8 * r;
+            if (g < G) {
+                if ((lane & 3) == 0) { pm[g] = m[r]; pl[g] = l[r]; }
+#pragma unroll
+                for (int i = 0; i < D / 8; ++i)
+                    *reinterpret_cast<float2 *>(po + g * D + i * 8 + c) = make_float2(acc[i][2 * r], acc[i][2 * r + 1]);
+            }
+        }
+    }
+
+    template <typename T>
+    FC_DEVINL void store_final(T *out, float *lse, int G, int lane) {
+        const int r0 = lane >> 2, c = (lane & 3) * 2;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int g = r0 + 8 * r;
+            if (g < G) {
+                const float inv = 1.f / l[r];
+#pragma unroll
+                for (int i = 0; i < D / 8; ++i) {
+                    out[g * D + i * 8 + c] = T(acc[i][2 * r] * inv);
+                    out[g * D + i * 8 + c + 1] = T(acc[i][2 * r + 1] * inv);
+                }
+                if (lse && (lane & 3) == 0) lse[g] = (m[r] + log2f(l[r])) * 0.69314718055994531f;
+            }
+        }
+    }
+};
+
+// fp32 CUDA-core path (G <= 8).  QK: lane = (token t = lane&15, half hf = lane>>4)
+// with a staggered column order (conflict-free); PV: lane owns D/32 columns.
+template <int D>
+struct F32Warp {
+    static constexpr int kC = D / 32;
+    float acc[8][kC];
+    float m[8], l[8];
+    const float *qs;  // shared [G][D]
+    int G;
+
+    FC_DEVINL void init(const float *qsh, int g_, int) {
+        qs = qsh; G = g_;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            m[g] = -INFINITY; l[g] = 0.f;
+#pragma unroll
+            for (int c = 0; c < kC; ++c) acc[g][c] = 0.f;
+        }
+    }
+
+    FC_DEVINL void page(char *stage, int ntok, float scale_log2, int lane) {
+        const float *K = reinterpret_cast<const float *>(stage);
+        const float *V = K + kPageSize * D;
+        const int t = lane & 15, hf = lane >> 4;
+        constexpr int HALF = D / 2;
+        float dot[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) dot[g] = 0.f;
+        for (int j = 0; j < HALF; ++j) {
+            const int i = hf * HALF + ((j + t + 16 * hf) % HALF);
+            const float kv = K[t * D + i];
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+                if (g < G) dot[g] = fmaf(qs[g * D + i], kv, dot[g]);
+        }
+        float p[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            if (g >= G) continue;
+            float x = dot[g] + __shfl_xor_sync(0xffffffffu, dot[g], 16);
+            x = t < ntok ? x * scale_log2 : -INFINITY;
+            float mx = x;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            const float mn = fmaxf(m[g], mx);
+            const float alpha = exp2f(m[g] - mn);
+            m[g] = mn;
+            p[g] = exp2f(x - mn);
+            float ps = p[g];
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+            l[g] = l[g] * alpha + ps;
+#pragma unroll
+            for (int c = 0; c < kC; ++c) acc[g][c] *= alpha;
+        }
+        for (int tt = 0; tt < ntok; ++tt) {
+            float v[kC];
+#pragma unroll
+            for (int c = 0; c < kC; ++c) v[c] = V[tt * D + lane * kC + c];
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                if (g >= G) continue;
+                const float pt = __shfl_sync(0xffffffffu, p[g], tt);
+#pragma unroll
+                for (int c = 0; c < kC; ++c) acc[g][c] = fmaf(pt, v[c], acc[g][c]);
+            }
+        }
+    }
+
+    FC_DEVINL void finalize() {}
+
+    FC_DEVINL void store_partial(float *po, float *pm, float *pl, int G_, int lane) {
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            if (g >= G_) continue;
+            if (lane == 0) { pm[g] = m[g]; pl[g] = l[g]; }
+#pragma unroll
+            for (int c = 0; c < kC; ++c) po[g * D + lane * kC + c] = acc[g][c];
+        }
+    }
+
+    template <typename T>
+    FC_DEVINL void store_final(T *out, float *lse, int G_, int lane) {
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            if (g >= G_) continue;
+            const float inv = 1.f / l[g];
+#pragma unroll
+            for (int c = 0; c < kC; ++c) out[g * D + lane * kC + c] = T(acc[g][c] * inv);
+            if (lse && lane == 0) lse[g] = (m[g] + log2f(l[g])) * 0.69314718055994531f;
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------
+
+template <typename T>
+FC_DEVINL void store_out(T *p, float v);
+template <>
+FC_DEVINL void store_out<__nv_bfloat16>(__nv_bfloat16 *p, float v) { *p = __float2bfloat16_rn(v); }
+template <>
+FC_DEVINL void store_out<float>(float *p, float v) { *p = v; }
+
+// Fused append (update_minmax, scoring.py:59-69): the warp that consumes a
+// head's last page writes the new token into the staged page (after the bulk
+// copy landed), into the HBM block, and folds the key into the page summary.
+template <typename T, int D>
+FC_DEVINL void patch_token(const StoreView &s, char *stage, T *gblock, int slot, int hx, int page,
+                           const T *kn, const T *vn, int lane) {
+    constexpr int V = D / 32;  // elements per lane, inside one 16-byte chunk for bf16
+    const int i0 = lane * V;
+    T kv[V], vv[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) { kv[j] = kn[i0 + j]; vv[j] = vn[i0 + j]; }
+    T *sk = reinterpret_cast<T *>(stage) + page_elem_offset<T>(slot, i0, D);
+    T *sv = reinterpret_cast<T *>(stage) + kPageSize * D + page_elem_offset<T>(slot, i0, D);
+    T *gk = gblock + page_elem_offset<T>(slot, i0, D);
+    T *gv = gblock + kPageSize * D + page_elem_offset<T>(slot, i0, D);
+#pragma unroll
+    for (int j = 0; j < V; ++j) { sk[j] = kv[j]; sv[j] = vv[j]; gk[j] = kv[j]; gv[j] = vv[j]; }
+    T *smin = reinterpret_cast<T *>(s.summ) + s.summ_off(hx, page, 0) + i0;
+    T *smax = reinterpret_cast<T *>(s.summ) + s.summ_off(hx, page, 1) + i0;
+    if (slot == 0) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) { smin[j] = kv[j]; smax[j] = kv[j]; }
+    } else {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const float f = Elem<T>::to_f(kv[j]);
+            if (f < Elem<T>::to_f(smin[j])) smin[j] = kv[j];
+            if (f > Elem<T>::to_f(smax[j])) smax[j] = kv[j];
+        }
+    }
+    __syncwarp();
+}
+
+// The same append split in two so that its loads leave the critical path:
+// load() (the new token's k / v and the page's current min / max row) is
+// issued as soon as the token may be read, long before the last page is
+// consumed; apply() then only writes.  Result identical to patch_token.
+template <typename T, int D>
+struct TokenPatch {
+    static constexpr int V = D / 32;
+    T kv[V], vv[V], mn[V], mx[V];
+    FC_DEVINL void load(const StoreView &s, const T *kn, const T *vn, int hx, int page, int slot, int lane) {
+        const int i0 = lane * V;
+#pragma unroll
+        for (int j = 0; j < V; ++j) { kv[j] = kn[i0 + j]; vv[j] = vn[i0 + j]; }
+        if (slot != 0) {
+            const T *smin = reinterpret_cast<const T *>(s.summ) + s.summ_off(hx, page, 0) + i0;
+            const T *smax = reinterpret_cast<const T *>(s.summ) + s.summ_off(hx, page, 1) + i0;
+#pragma unroll
+            for (int j = 0; j < V; ++j) { mn[j] = smin[j]; mx[j] = smax[j]; }
+        }
+    }
+    FC_DEVINL void apply(const StoreView &s, char *stage, T *gblock, int slot, int hx, int page, int lane) {
+        const int i0 = lane * V;
+        T *sk = reinterpret_cast<T *>(stage) + page_elem_offset<T>(slot, i0, D);
+        T *sv = reinterpret_cast<T *>(stage) + kPageSize * D + page_elem_offset<T>(slot, i0, D);
+        T *gk = gblock + page_elem_offset<T>(slot, i0, D);
+        T *gv = gblock + kPageSize * D + page_elem_offset<T>(slot, i0, D);
+#pragma unroll
+        for (int j = 0; j < V; ++j) { sk[j] = kv[j]; sv[j] = vv[j]; gk[j] = kv[j]; gv[j] = vv[j]; }
+        T *smin = reinterpret_cast<T *>(s.summ) + s.summ_off(hx, page, 0) + i0;
+        T *smax = reinterpret_cast<T *>(s.summ) + s.summ_off(hx, page, 1) + i0;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            if (slot == 0) {
+                smin[j] = kv[j];
+                smax[j] = kv[j];
+            } else {
+                const float f = Elem<T>::to_f(kv[j]);
+                smin[j] = f < Elem<T>::to_f(mn[j]) ? kv[j] : mn[j];
+                smax[j] = f > Elem<T>::to_f(mx[j]) ? kv[j] : mx[j];
+            }
+        }
+        __syncwarp();
+    }
+};
+
+// Attended page count of head bh (flat row*H + head of this layer).
+struct HeadInfo {
+    int hx, n_tok, n_pages, nsel, hi, n_att;
+};
+
+FC_DEVINL HeadInfo head_info(const StoreView &s, int layer, int extra_tokens, int attend_appended, int bh) {
+    HeadInfo hi;
+    const int b = bh / s.H, h = bh % s.H;
+    hi.hx = s.hix(b, layer, h);
+    hi.n_tok = s.seq_len[b] + extra_tokens;
+    hi.n_pages = hi.n_tok > 0 ? (hi.n_tok + kPageSize - 1) / kPageSize : 0;
+    hi.nsel = s.n_sel[hi.hx];
+    hi.hi = hi.nsel > 0 ? s.sel[(int64_t)hi.hx * s.SELCAP + hi.nsel - 1] : -1;
+    int n_att = attend_appended ? hi.nsel + max(0, hi.n_pages - 1 - hi.hi) : hi.nsel;
+    if (hi.n_tok <= 0) n_att = 0;
+    hi.n_att = n_att;
+    return hi;
+}
+
+FC_DEVINL HeadInfo head_info(const StoreView &s, const AttnArgs &a, int bh) {
+    return head_info(s, a.layer, a.extra_tokens, a.attend_appended, bh);
+}
+
+// page (logical) of attended entry j of a head: the selection, then the pages
+// appended since its last page (simulator.py:416-420)
+FC_DEVINL int entry_page(const StoreView &s, const HeadInfo &hd, int j) {
+    return j < hd.nsel ? s.sel[(int64_t)hd.hx * s.SELCAP + j] : hd.hi + 1 + (j - hd.nsel);
+}
+
+// physical block of a logical page; a null block is a residency violation
+// (attention.py:101-105, blocktable.py:192-198): error bit, -1
+FC_DEVINL int resolve_block(const StoreView &s, const HeadInfo &hd, int page) {
+    int blk = 0;
+    if (page >= 0 && page < hd.n_pages) blk = s.table[s.table_off(hd.hx, page)];
+    if (blk == FC_NULL_BLOCK) {
+        set_error(s.err, FC_ERR_NULL_READ);
+        blk = -1;
+    }
+    return blk;
+}
+
+}  // namespace fc

@@ -63,6 +63,7 @@ const char *fc_last_error(void) { return g_last_error; }
 /* profiling hook (not part of the ABI): per-CTA globaltimer trace of the
  * attention kernel into a device buffer [grid][4] u64, or null to disable */
 int fc_debug_attn_trace(void *device_buf) { return cuda_status(set_attn_trace(device_buf)); }
+int fc_debug_run_trace(void *device_buf) { return cuda_status(set_run_trace(device_buf)); }
 int fc_debug_score_trace(void *device_buf) { return cuda_status(set_score_trace(device_buf)); }
 /* test hook: scoring kernel choice, -1 auto, 0 balanced, 1 head-aligned */
 int fc_debug_score_mode(int mode) { set_score_mode(mode); return FC_OK; }
@@ -207,6 +208,54 @@ int fc_sparse_decode(const fc_store *s, int layer, const void *q, const void *k_
     a.part_l = a.part_m + n * 16;
     a.part_o = a.part_l + n * 16;
     return cuda_status(launch_attn(v, s->dtype, a, batch, (cudaStream_t)stream));
+}
+
+int fc_sparse_decode_layers_supported(const fc_store *s, int batch, int max_pages) {
+    if (check_store(s) != FC_OK || batch < 1 || batch > s->batch_cap || max_pages < 1) return 0;
+    return attn_run_supported(make_view(s), s->dtype, batch, max_pages);
+}
+
+size_t fc_sparse_decode_layers_workspace_size(const fc_store *s, int batch, int max_pages) {
+    if (check_store(s) != FC_OK || max_pages < 1) return 0;
+    return attn_run_workspace_bytes(make_view(s), s->dtype, batch, max_pages);
+}
+
+int fc_sparse_decode_layers(const fc_store *s, int layer_begin, int n_layers, const void *q,
+                            int64_t q_layer_stride, const void *k_new, const void *v_new,
+                            int64_t kv_layer_stride, void *out, int64_t out_layer_stride, float *lse,
+                            int64_t lse_layer_stride, float scale, int extra_tokens, int attend_appended,
+                            int first_dep, int max_pages, void *workspace, size_t ws_bytes, int batch,
+                            void *stream) {
+    FC_CHECK(check_store(s));
+    if (n_layers < 1 || layer_begin < 0 || layer_begin + n_layers > s->layers) return invalid("layer run out of range");
+    if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
+    if (!q || !out || !workspace) return invalid("null buffer");
+    if ((k_new == nullptr) != (v_new == nullptr)) return invalid("k_new and v_new go together");
+    if (k_new && extra_tokens != 1) return invalid("fused append needs extra_tokens = 1");
+    if (max_pages < 1) return invalid("max_pages must be >= 1");
+    if (!(scale > 0.f) || !std::isfinite(scale)) return invalid("scale must be positive");
+    if (extra_tokens < 0 || extra_tokens > 1) return invalid("extra_tokens must be 0 or 1");
+    if (n_layers > 1 && (q_layer_stride <= 0 || out_layer_stride <= 0 || (k_new && kv_layer_stride <= 0) ||
+                         (lse && lse_layer_stride <= 0)))
+        return invalid("layer strides must be positive for a run of several layers");
+    if (batch == 0) return FC_OK;
+    const StoreView v = make_view(s);
+    if (!attn_run_supported(v, s->dtype, batch, max_pages)) {
+        std::snprintf(g_last_error, sizeof(g_last_error), "run kernel does not fit this geometry");
+        return FC_E_UNSUPPORTED;
+    }
+    if (ws_bytes < attn_run_workspace_bytes(v, s->dtype, batch, max_pages)) return FC_E_CAPACITY;
+    RunArgs a = {};
+    a.l0 = layer_begin; a.nl = n_layers;
+    a.q = q; a.q_ls = q_layer_stride;
+    a.k_new = k_new; a.v_new = v_new; a.kv_ls = kv_layer_stride;
+    a.out = out; a.o_ls = out_layer_stride;
+    a.lse = lse; a.lse_ls = lse_layer_stride;
+    a.scale_log2 = scale * 1.4426950408889634f;
+    a.extra_tokens = extra_tokens; a.attend_appended = attend_appended;
+    a.first_dep = first_dep ? 1 : 0;
+    a.batch = batch;
+    return cuda_status(launch_attn_run(v, s->dtype, a, max_pages, workspace, (cudaStream_t)stream));
 }
 
 size_t fc_rerank_workspace_size(const fc_store *s) {

@@ -23,6 +23,31 @@ struct AttnArgs {
     float *part_o;
 };
 
+// persistent multi-layer attention (attn_run.cu)
+struct RunArgs {
+    int l0, nl;            // layers [l0, l0 + nl)
+    const void *q;         // layer l0 + i at q + i * q_ls elements: [batch][H*G][D]
+    int64_t q_ls;
+    const void *k_new;     // [batch][H][D] per layer (kv_ls apart) or null
+    const void *v_new;
+    int64_t kv_ls;
+    void *out;
+    int64_t o_ls;
+    float *lse;            // [batch*H*G] per layer (lse_ls apart) or null
+    int64_t lse_ls;
+    float scale_log2;
+    int extra_tokens, attend_appended;
+    int first_dep;         // the previous launch writes layer l0's selection / table
+    int batch;
+    int min_pages, maxr;   // set by the launcher
+    uint32_t *bar;         // workspace: [L][2] barrier / exit counters (self-resetting)
+    int32_t *head_cnt;     // workspace: per-head part counters (self-resetting)
+    float *part;           // workspace: [warps][2][G*D + 32]
+};
+int attn_run_supported(const StoreView &, int, int, int);
+size_t attn_run_workspace_bytes(const StoreView &, int, int, int);
+cudaError_t launch_attn_run(const StoreView &, int, const RunArgs &, int, void *, cudaStream_t);
+
 cudaError_t launch_alloc_pages(const StoreView &, int, int, int, cudaStream_t);
 cudaError_t launch_step_advance(const StoreView &, int, cudaStream_t);
 cudaError_t launch_evict_pages(const StoreView &, const int32_t *, int, cudaStream_t);
@@ -36,6 +61,7 @@ cudaError_t launch_select(const float *, int, const int32_t *, int, int, int, in
 cudaError_t launch_attn(const StoreView &, int, const AttnArgs &, int, cudaStream_t);
 size_t attn_workspace_bytes(const StoreView &, int, int);
 cudaError_t set_attn_trace(void *);
+cudaError_t set_run_trace(void *);
 cudaError_t set_score_trace(void *);
 void set_score_mode(int);
 void set_attn_mode(int);

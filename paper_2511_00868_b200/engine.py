@@ -69,6 +69,11 @@ class DecodeEngine:
         # attention of heads a layer's scoring launch does not select starts
         # without waiting for it (fc_sparse_decode early_unstable)
         self.early_heads = True
+        # True: attention as persistent launches over runs of layers with no
+        # scoring / recycle between them (fc_sparse_decode_layers).  Default
+        # False: one fc_sparse_decode launch per layer, measured faster at
+        # config 2 (24.9 vs 37.6 us per layer)
+        self.run_kernel = False
         # profiling: score every head every step and record
         # the selections on the device (trace.TraceRecorder)
         self.score_all_heads = False
@@ -121,13 +126,22 @@ class DecodeEngine:
     def _launch_step(self, rerank: bool, force_due: bool) -> None:
         st = self.store
         tiered_rerank = self.tiering and rerank and not force_due
-        for layer in range(self.L):
-            recycle = tiered_rerank and layer in self._stable_layers
+        use_run = self.run_kernel and st.run_supported(self.B, self.att_bound)
+
+        def recycles(l):
+            return tiered_rerank and l in self._stable_layers
+
+        def scores(l):
+            return force_due or not self._layer_skippable(l, rerank)
+
+        layer = 0
+        while layer < self.L:
+            recycle = recycles(layer)
             if recycle:  # resident set of stable heads = their current selection
                 self.old_sel.copy_(st.sel[:, layer])
                 self.n_old.copy_(st.n_sel[:, layer])
                 self.n_copies.zero_()
-            scored = force_due or not self._layer_skippable(layer, rerank)
+            scored = scores(layer)
             if scored:
                 # the previous kernel (the last layer's attention) never writes this
                 # layer's summaries / selection: plan and warm L2 while it drains
@@ -139,18 +153,34 @@ class DecodeEngine:
                                   slow_resident=self.tier.slow_resident)
                 self.tier.reload(layer, self.copies, self.n_copies)
                 self.fetched_pages.add_(self.n_copies)
+            if use_run:
+                # persistent attention over the run of layers up to the next one
+                # that needs a selection / table update (or a per-layer hook)
+                end = layer + 1
+                if self.after_layer is None:
+                    while end < self.L and not (scores(end) or recycles(end)):
+                        end += 1
+                st.sparse_decode_layers(layer, end - layer, self.q[layer:end], self.out[layer:end], self.B,
+                                        max_pages=self.att_bound, extra_tokens=1, attend_appended=False,
+                                        k_new=self.k_new[layer:end], v_new=self.v_new[layer:end],
+                                        first_dep=scored or recycle or layer == 0)
+                if self.after_layer is not None:
+                    self.after_layer(layer)
+                layer = end
+                continue
             # with no scoring / recycle launch in this layer, the previous kernel
             # (the last layer's attention, or the step advance) does not touch
             # this layer's selection, table or pages: stage KV while it drains
             st.sparse_decode(layer, self.q[layer], self.out[layer], self.B,
                              max_pages=self.att_bound, extra_tokens=1, attend_appended=False,
                              k_new=self.k_new[layer], v_new=self.v_new[layer],
-                             kv_prefetch=not (scored or recycle) and self.after_layer is None,
+                             kv_prefetch=not (scored or recycle) and self.after_layer is None and layer > 0,
                              # heads the scoring launch leaves alone overlap it
                              early_unstable=self.unstable if scored and not recycle and not force_due
                              and self.early_heads else None, early_period=self.R)
             if self.after_layer is not None:
                 self.after_layer(layer)
+            layer += 1
         st.step_advance(self.B)
         if self.recorder is not None:
             self.recorder.capture()
@@ -220,8 +250,13 @@ class DecodeEngine:
         attention launch (append fused), a scoring launch for every layer with
         a due head, and the step advance."""
         rerank = self.is_rerank_step(t)
-        scored = sum(not self._layer_skippable(l, rerank) for l in range(self.L))
-        n = self.L + scored + 1
+        flags = [not self._layer_skippable(l, rerank) for l in range(self.L)]
+        scored = sum(flags)
+        n_attn = self.L
+        if self.run_kernel and self.store.run_supported(self.B, self.att_bound) and self.after_layer is None:
+            breaks = [f or (self.tiering and rerank and l in self._stable_layers) for l, f in enumerate(flags)]
+            n_attn = 1 + sum(breaks[1:])  # one launch per run of layers
+        n = n_attn + scored + 1
         if self.tiering:
             n += 1 + (2 * len(self._stable_layers) if rerank else 0)
         return n

@@ -83,6 +83,7 @@ class KVStore:
         self.score_counters = torch.zeros(batch_cap * kv_heads, dtype=torch.int32, device=dev)
         self._attn_ws = torch.zeros(0, dtype=torch.uint8, device=dev)
         self._rerank_ws = None
+        self._run_ws = torch.zeros(0, dtype=torch.uint8, device=dev)
 
     # -- misc ------------------------------------------------------------------
 
@@ -196,6 +197,30 @@ class KVStore:
             scale, extra_tokens, int(attend_appended), int(kv_prefetch), _ptr(early_unstable),
             early_period, max_pages, n_ctas, ws.data_ptr(),
             ws.numel(), batch, self.stream()), "fc_sparse_decode")
+
+    def run_supported(self, batch: int, max_pages: int) -> bool:
+        """Whether the persistent multi-layer kernel fits this geometry."""
+        return bool(self.lib.fc_sparse_decode_layers_supported(self.cptr, batch, max_pages))
+
+    def sparse_decode_layers(self, layer: int, n_layers: int, q: torch.Tensor, out: torch.Tensor,
+                             batch: int, *, max_pages: int, lse: torch.Tensor | None = None,
+                             scale: float | None = None, extra_tokens: int = 1,
+                             attend_appended: bool = True, k_new: torch.Tensor | None = None,
+                             v_new: torch.Tensor | None = None, first_dep: bool = True) -> None:
+        """fc_sparse_decode_layers: the layers [layer, layer + n_layers) in one
+        persistent launch.  q/out (and k_new/v_new, lse) are per-layer stacks
+        ([n_layers, ...], dim 0 = layer); same per-(layer, head) semantics as
+        sparse_decode."""
+        need = self.lib.fc_sparse_decode_layers_workspace_size(self.cptr, batch, max_pages)
+        if self._run_ws.numel() < need:
+            self._run_ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
+        scale = 1.0 / math.sqrt(self.D) if scale is None else scale
+        st = (lambda t: t.stride(0) if (t is not None and t.dim() > 0 and n_layers > 1) else 0)
+        _lib.check(self.lib.fc_sparse_decode_layers(
+            self.cptr, layer, n_layers, q.data_ptr(), st(q), _ptr(k_new), _ptr(v_new), st(k_new),
+            out.data_ptr(), st(out), _ptr(lse), st(lse), scale, extra_tokens, int(attend_appended),
+            int(first_dep), max_pages, self._run_ws.data_ptr(), self._run_ws.numel(), batch,
+            self.stream()), "fc_sparse_decode_layers")
 
     # -- (4) rerank / tiers ------------------------------------------------------------
 

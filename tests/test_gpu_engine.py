@@ -25,7 +25,7 @@ def _round(x, dtype):
 
 
 def run_engine_vs_oracle(*, B, L, H, G, D, T0, steps, K, R, frac, dtype, seed, use_graph,
-                         ragged=False, tiering=False):
+                         ragged=False, tiering=False, run_kernel=False):
     from paper_2511_00868_b200.engine import DecodeEngine
     from paper_2511_00868_b200.stability import HeadProfile
     rng = np.random.default_rng(seed)
@@ -34,6 +34,7 @@ def run_engine_vs_oracle(*, B, L, H, G, D, T0, steps, K, R, frac, dtype, seed, u
     eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D,
                        ctx_cap_tokens=T0 + steps + 64, topk_pages=K, rerank_period=R,
                        profile=prof, dtype=dtype, tiering=tiering)
+    eng.run_kernel = run_kernel
     dev = eng.device
     lens = [T0 + (17 * b if ragged else 0) for b in range(B)]
     keys = {}
@@ -197,6 +198,7 @@ def test_early_heads_bitwise_equal_to_serialized():
         eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=T + 64,
                            topk_pages=K, rerank_period=R, profile=HeadProfile.first_n(L, H, 0.25))
         eng.early_heads = early
+        eng.run_kernel = False  # early heads belong to the per-layer kernel
         for b in range(B):
             for l in range(L):
                 eng.prefill_layer(b, l, device_normal((H, T + 7 * b, D), seed=4 * b + l),
@@ -234,10 +236,37 @@ def balanced_attention():
 def test_engine_balanced_attention_matches_oracle(balanced_attention, dtype):
     worst, ties, eng = run_engine_vs_oracle(B=3, L=2, H=2, G=4, D=128, T0=700, steps=12, K=8,
                                             R=4, frac=0.5, dtype=dtype, seed=13, use_graph=True,
-                                            ragged=True)
+                                            ragged=True, run_kernel=False)
     assert ties <= 2
 
 
 def test_engine_balanced_attention_tiered(balanced_attention):
     run_engine_vs_oracle(B=2, L=2, H=4, G=7, D=128, T0=400, steps=16, K=6, R=4, frac=0.5,
                          dtype=torch.bfloat16, seed=14, use_graph=True, tiering=True)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_engine_per_layer_attention_matches_oracle(dtype):
+    """The per-layer cluster kernel (fc_sparse_decode, the default) over
+    several unscored layers in a row (KV staged while the previous layer
+    drains)."""
+    run_engine_vs_oracle(B=2, L=4, H=2, G=4, D=128, T0=500, steps=10, K=8, R=4, frac=0.25,
+                         dtype=dtype, seed=15, use_graph=True, ragged=True)
+
+
+@pytest.mark.parametrize("dtype,D,G", [(torch.bfloat16, 128, 4), (torch.float32, 128, 4),
+                                       (torch.bfloat16, 64, 7), (torch.float32, 64, 2)])
+def test_engine_layer_runs_match_oracle(dtype, D, G):
+    """fc_sparse_decode_layers over runs of several layers (1/8 of the heads
+    unstable: layer 0 scored every step, layers 1-5 one persistent launch
+    between reranks); ragged rows, graph replay, rerank steps."""
+    worst, ties, eng = run_engine_vs_oracle(B=3, L=6, H=2, G=G, D=D, T0=600, steps=12, K=8, R=4,
+                                            frac=0.125, dtype=dtype, seed=16, use_graph=True,
+                                            ragged=True, run_kernel=True)
+    assert eng.launches_per_step(1) == 3  # score(0), run [0, 6), advance
+    assert ties <= 2
+
+
+def test_engine_layer_runs_tiered():
+    run_engine_vs_oracle(B=2, L=4, H=4, G=4, D=128, T0=400, steps=16, K=6, R=4, frac=0.25,
+                         dtype=torch.bfloat16, seed=17, use_graph=True, tiering=True, run_kernel=True)
