@@ -205,6 +205,23 @@ int fc_sparse_decode(const fc_store *s, int layer, const void *q,
                      void *workspace, size_t ws_bytes, int batch,
                      void *stream);
 
+/* fc_score_select followed by fc_sparse_decode of the same layer, fused:
+ * one CTA per (row, head) scores and selects (as fc_score_select:
+ * score_pages / select_topk / rerank_due, scoring.py:93-202) and then, in
+ * the same CTA, attends over the selection it just wrote (as
+ * fc_sparse_decode: sparse_decode, attention.py:85-111, fused update_minmax,
+ * scoring.py:59-69).  Identical results to the two calls; no grid-wide wait
+ * between them.  Supported when the batch has at least ~half as many heads
+ * as SMs (fc_score_attend_supported); otherwise FC_E_UNSUPPORTED and the
+ * caller issues the two calls. */
+int fc_score_attend_supported(const fc_store *s, int batch);
+int fc_score_attend(const fc_store *s, int layer, const void *q,
+                    const uint8_t *unstable, int period, int force_due,
+                    int topk, int extra_tokens, int kv_prefetch,
+                    float *scores_out, const void *k_new, const void *v_new,
+                    void *out, float *lse, float scale, int attend_appended,
+                    int batch, void *stream);
+
 /* Persistent form of fc_sparse_decode for a run of consecutive layers
  * [layer_begin, layer_begin + n_layers) in ONE launch (same semantics per
  * (layer, head) as fc_sparse_decode: sparse_decode, attention.py:85-111, the

@@ -397,4 +397,136 @@ FC_DEVINL int resolve_block(const StoreView &s, const HeadInfo &hd, int page) {
     return blk;
 }
 
+
+// Named barrier over the first n threads of the CTA (id 1..15).
+FC_DEVINL void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// Attention of ONE head by the first NW warps of a CTA (S = 1 form of
+// attn_kernel's body, used by the fused score+attend kernel): each warp
+// streams an equal contiguous range of the head's attended pages through its
+// own NST-stage cp.async.bulk ring, warps merge through shared memory, the
+// append is fused (TokenPatch).  Threads >= NW*32 must not call it.  ring:
+// NW*NST pages of shared memory (also the merge scratch, NW*G*D floats);
+// s_q: fp32 q [G][D] (fp32 only).  Every read this needs must already be
+// visible (the caller waited for the previous launch / wrote sel itself).
+template <typename T, int D, int NST, int NW>
+FC_DEVINL void attend_head_cta(const StoreView &s, const AttnArgs &a, int bh, char *ring, uint64_t *bars,
+                               float (*s_wm)[16], float (*s_wl)[16], float *s_q, int bar_id) {
+    using Gm = AttnGeom<T, D>;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    constexpr int NT = NW * 32;
+    const int G = s.G;
+    const HeadInfo hd = head_info(s, a, bh);
+    const int n_att = hd.n_att;
+    const int j0 = (int)((int64_t)n_att * w / NW);
+    const int n_e = (int)((int64_t)n_att * (w + 1) / NW) - j0;
+    const int b = bh / s.H, h = bh % s.H;
+    const int64_t qoff = ((int64_t)b * s.H * G + (int64_t)h * G) * D;
+    const int last_fill = hd.n_tok - (hd.n_pages - 1) * kPageSize;
+    if (tid < NW * NST) mbar_init(&bars[tid], 1);
+    fence_mbar_init();
+    fence_proxy_async_smem();  // the ring held generic-proxy data before
+    named_bar_sync(bar_id, NT);
+    int cur_blk = 0, nxt_blk = 0;
+    {
+        const int j = j0 + lane;
+        if (lane < n_e) cur_blk = resolve_block(s, hd, entry_page(s, hd, j));
+        if (lane + 32 < n_e) nxt_blk = resolve_block(s, hd, entry_page(s, hd, j + 32));
+    }
+    const char *pool = reinterpret_cast<const char *>(s.pool);
+    char *myring = ring + (size_t)w * NST * Gm::kPageBytes;
+    uint64_t *mybars = bars + w * NST;
+    int chunk = 0;
+#pragma unroll
+    for (int i = 0; i < NST; ++i) {
+        const int blk = __shfl_sync(0xffffffffu, cur_blk, i);
+        if (lane == 0 && i < n_e) {
+            if (blk > 0) {
+                mbar_arrive_expect_tx(&mybars[i], Gm::kPageBytes);
+                bulk_g2s(myring + (size_t)i * Gm::kPageBytes, pool + (int64_t)blk * Gm::kPageBytes, Gm::kPageBytes,
+                         &mybars[i]);
+            } else {
+                mbar_arrive_expect_tx(&mybars[i], 0);
+            }
+        }
+    }
+    if constexpr (sizeof(T) == 4) {
+        const float *qg = reinterpret_cast<const float *>(a.q) + qoff;
+        for (int i = tid; i < G * D; i += NT) s_q[i] = qg[i];
+        named_bar_sync(bar_id, NT);
+    }
+    typename std::conditional<sizeof(T) == 2, Bf16Warp<D>, F32Warp<D>>::type st;
+    if constexpr (sizeof(T) == 4) st.init(s_q, G, lane);
+    else st.init(reinterpret_cast<const T *>(a.q) + qoff, G, lane);
+    TokenPatch<T, D> tp;
+    const int tok_slot = (hd.n_tok - 1) % kPageSize;
+    const bool last_is_last_page =
+        n_e > 0 && j0 + n_e == n_att && entry_page(s, hd, n_att - 1) == hd.n_pages - 1;
+    if (a.k_new != nullptr && n_e > 0 && j0 + n_e == n_att) {
+        const int64_t nk = ((int64_t)b * s.H + h) * D;
+        tp.load(s, reinterpret_cast<const T *>(a.k_new) + nk, reinterpret_cast<const T *>(a.v_new) + nk, hd.hx,
+                hd.n_pages - 1, tok_slot, lane);
+    }
+    for (int i = 0; i < n_e; ++i) {
+        if (i > 0 && (i & 31) == 0) {
+            cur_blk = nxt_blk;
+            ++chunk;
+            const int j = j0 + (chunk + 1) * 32 + lane;
+            nxt_blk = (j < j0 + n_e) ? resolve_block(s, hd, entry_page(s, hd, j)) : 0;
+        }
+        const int blk = __shfl_sync(0xffffffffu, cur_blk, i & 31);
+        const int ni = i + NST;
+        const int nb_cur = __shfl_sync(0xffffffffu, cur_blk, ni & 31);
+        const int nb_nxt = __shfl_sync(0xffffffffu, nxt_blk, ni & 31);
+        const int nblk = (ni >> 5) == chunk ? nb_cur : nb_nxt;
+        const int stg = i % NST;
+        mbar_wait(&mybars[stg], (i / NST) & 1);
+        if (blk > 0) {
+            char *stage = myring + (size_t)stg * Gm::kPageBytes;
+            const bool last = (j0 + i == n_att - 1);
+            if (last && a.k_new != nullptr)
+                tp.apply(s, stage, reinterpret_cast<T *>(s.pool) + s.block_off(blk), tok_slot, hd.hx,
+                         hd.n_pages - 1, lane);
+            st.page(stage, last && last_is_last_page ? last_fill : kPageSize, a.scale_log2, lane);
+        }
+        __syncwarp();
+        if (lane == 0 && ni < n_e) {
+            fence_proxy_async_smem();
+            if (nblk > 0) {
+                mbar_arrive_expect_tx(&mybars[stg], Gm::kPageBytes);
+                bulk_g2s(myring + (size_t)stg * Gm::kPageBytes, pool + (int64_t)nblk * Gm::kPageBytes,
+                         Gm::kPageBytes, &mybars[stg]);
+            } else {
+                mbar_arrive_expect_tx(&mybars[stg], 0);
+            }
+        }
+    }
+    st.finalize();
+    named_bar_sync(bar_id, NT);  // every warp done with its ring: merge scratch
+    float *scratch = reinterpret_cast<float *>(ring);  // [NW][G][D]
+    for (int g = lane; g < 16; g += 32) { s_wm[w][g] = -INFINITY; s_wl[w][g] = 0.f; }
+    __syncwarp();
+    st.store_partial(scratch + (size_t)w * G * D, s_wm[w], s_wl[w], G, lane);
+    named_bar_sync(bar_id, NT);
+    T *out = reinterpret_cast<T *>(a.out) + qoff;
+    float *lse = a.lse ? a.lse + (int64_t)bh * G : nullptr;
+    if (n_att > 0) {
+        for (int e = tid; e < G * D; e += NT) {
+            const int g = e / D;
+            float M = -INFINITY;
+#pragma unroll
+            for (int ww = 0; ww < NW; ++ww) M = fmaxf(M, s_wm[ww][g]);
+            float L = 0.f, O = 0.f;
+#pragma unroll
+            for (int ww = 0; ww < NW; ++ww) {
+                const float f = exp2f(s_wm[ww][g] - M);
+                L += s_wl[ww][g] * f;
+                O += scratch[(size_t)ww * G * D + e] * f;
+            }
+            out[e] = T(O / L);
+            if (lse && e % D == 0) lse[g] = (M + log2f(L)) * 0.69314718055994531f;
+        }
+    }
+}
+
 }  // namespace fc

@@ -56,6 +56,9 @@ cudaError_t launch_append(const StoreView &, int, int, const void *, const void 
 cudaError_t launch_gather(const StoreView &, int, int, int, int, int, void *, void *, cudaStream_t);
 cudaError_t launch_score(const StoreView &, int, int, const void *, const uint8_t *, int, int, int, int,
                          float *, int32_t *, int, int, int, cudaStream_t);
+int score_attend_supported(const StoreView &, int, int);
+cudaError_t launch_score_attend(const StoreView &, int, int, const void *, const uint8_t *, int, int, int, int,
+                                float *, int, int, const AttnArgs &, cudaStream_t);
 cudaError_t launch_select(const float *, int, const int32_t *, int, int, int, int32_t *, int32_t *,
                           cudaStream_t);
 cudaError_t launch_attn(const StoreView &, int, const AttnArgs &, int, cudaStream_t);

@@ -17,7 +17,7 @@
 // an orderable 32-bit key of the fp32 score (-0.0 == +0.0), ties resolved by
 // lowest page index, fused into the last CTA to finish scoring a head
 // (threadfence reduction).
-#include "store.cuh"
+#include "attn_warp.cuh"
 #include <cub/block/block_scan.cuh>
 
 namespace fc {
@@ -555,29 +555,40 @@ constexpr int kHeadScoreWarps = FC_HEAD_WARPS;
 static int g_score_mode = FC_SCORE_MODE_DEFAULT;  // -1 auto, 0 balanced, 1 head-aligned (test hook)
 constexpr int kHeadChunkPages = FC_HEAD_CHUNK_PAGES;
 
-template <typename T, int D>
+template <typename T, int D, int NWS = kHeadScoreWarps>
 struct HeadScoreGeom {
     using Gm = ScoreGeom<T, D>;
     static constexpr int kChunkBytes = kHeadChunkPages * Gm::kRecBytes;
     static constexpr int kStages = (FC_HEAD_RING_KB * 1024) / kChunkBytes > 2 ? (FC_HEAD_RING_KB * 1024) / kChunkBytes : 2;
-    static constexpr int kRounds = kHeadChunkPages / (kHeadScoreWarps * Gm::kPagesPerSlot);  // per warp per chunk
+    static constexpr int kRounds = kHeadChunkPages / (NWS * Gm::kPagesPerSlot);  // per warp per chunk
 };
 
-template <typename T, int D>
-__global__ void __launch_bounds__(kHeadScoreWarps * 32, 1)
-score_head_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t *__restrict__ unstable,
-                  int period, int force_due, int topk, int extra_tokens, float *scores, int kv_prefetch) {
+// shared bytes before the fp32 q of the fused kernel: max(scoring ring + keys,
+// attention ring / merge scratch)
+template <typename T, int D, int NST, int NWA>
+__host__ __device__ constexpr size_t score_attend_ring_bytes(int ncap) {
+    return (size_t)HeadScoreGeom<T, D>::kStages * HeadScoreGeom<T, D>::kChunkBytes + (size_t)ncap * 4 >
+                   (size_t)NWA * NST * AttnGeom<T, D>::kPageBytes
+               ? (((size_t)HeadScoreGeom<T, D>::kStages * HeadScoreGeom<T, D>::kChunkBytes + (size_t)ncap * 4 + 127) &
+                  ~(size_t)127)
+               : (size_t)NWA * NST * AttnGeom<T, D>::kPageBytes;
+}
+
+// Body of the head-aligned scoring for head blockIdx.x: every thread of the
+// CTA (kHeadScoreWarps warps) calls it; returns after the selection is in
+// s.sel / s.n_sel (or at once for a head that is not due).  Waits for the
+// previous launch (PDL) on every path.  dsm: ring [NS][chunk] | keys [NCAP].
+template <typename T, int D, int NWS = kHeadScoreWarps>
+__device__ void score_head_body(const StoreView &s, int layer, const T *__restrict__ q,
+                                const uint8_t *__restrict__ unstable, int period, int force_due, int topk,
+                                int extra_tokens, float *scores, int kv_prefetch, char *dsm, uint64_t *full,
+                                uint64_t *empty, int *s_rel, float *w) {
     using Gm = ScoreGeom<T, D>;
-    using HG = HeadScoreGeom<T, D>;
-    constexpr int NW = kHeadScoreWarps, NS = HG::kStages, R = HG::kRounds;
+    using HG = HeadScoreGeom<T, D, NWS>;
+    constexpr int NW = NWS, NS = HG::kStages, R = HG::kRounds;
     constexpr int LPP = Gm::kLanesPerPage, CPL = Gm::kChunksPerLane, EPC = Gm::kElemsPerChunk;
     static_assert(R >= 1 && R <= LPP, "chunk geometry");
-    extern __shared__ __align__(128) char dsm[];  // ring [NS][chunk] | keys [NCAP]
-    __shared__ __align__(8) uint64_t full[NS], empty[NS];
-    __shared__ int s_rel[NS];
-    __shared__ float w[2 * D];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    griddep_launch_dependents();
     if (!kv_prefetch) griddep_wait();
     const int bh = blockIdx.x, b = bh / s.H, h = bh % s.H;
     const bool due = force_due || unstable[layer * s.H + h] || (*s.step % period == 0);
@@ -702,6 +713,47 @@ score_head_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t
     }
 }
 
+template <typename T, int D>
+__global__ void __launch_bounds__(kHeadScoreWarps * 32, 1)
+score_head_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t *__restrict__ unstable,
+                  int period, int force_due, int topk, int extra_tokens, float *scores, int kv_prefetch) {
+    extern __shared__ __align__(128) char dsm[];  // ring [NS][chunk] | keys [NCAP]
+    __shared__ __align__(8) uint64_t full[HeadScoreGeom<T, D>::kStages], empty[HeadScoreGeom<T, D>::kStages];
+    __shared__ int s_rel[HeadScoreGeom<T, D>::kStages];
+    __shared__ float w[2 * D];
+    griddep_launch_dependents();
+    score_head_body<T, D>(s, layer, q, unstable, period, force_due, topk, extra_tokens, scores, kv_prefetch,
+                          dsm, full, empty, s_rel, w);
+}
+
+// Fused scoring + attention of one head per CTA (layers whose heads are
+// scored this step): the selection never leaves the CTA's view before its
+// pages stream — no grid-wide wait between scoring and attention, no second
+// launch, no selection -> table round trip through another kernel.  Warps
+// 0..NWA-1 then attend exactly as attn_kernel (attend_head_cta); the ring
+// reuses the scoring ring / keys.  Same results as fc_score_select followed
+// by fc_sparse_decode (the attention reads the selection just written).
+template <typename T, int D, int NST, int NWA>
+__global__ void __launch_bounds__(NWA * 32, 1)
+score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t *__restrict__ unstable,
+                    int period, int force_due, int topk, int extra_tokens, float *scores, int kv_prefetch,
+                    AttnArgs a) {
+    extern __shared__ __align__(128) char dsm[];
+    __shared__ __align__(8) uint64_t full[HeadScoreGeom<T, D>::kStages], empty[HeadScoreGeom<T, D>::kStages];
+    __shared__ int s_rel[HeadScoreGeom<T, D>::kStages];
+    __shared__ float w[2 * D];
+    __shared__ __align__(8) uint64_t abars[NWA * NST];
+    __shared__ float s_wm[NWA][16], s_wl[NWA][16];
+    griddep_launch_dependents();
+    // the same warps score (NWA warps: the attention phase needs > 128
+    // registers per thread, so the CTA is not the 16-warp scoring CTA)
+    score_head_body<T, D, NWA>(s, layer, q, unstable, period, force_due, topk, extra_tokens, scores, kv_prefetch,
+                               dsm, full, empty, s_rel, w);
+    __syncthreads();  // selection written by this CTA; scoring smem free
+    float *s_q = reinterpret_cast<float *>(dsm + score_attend_ring_bytes<T, D, NST, NWA>(s.NCAP));
+    attend_head_cta<T, D, NST, NWA>(s, a, blockIdx.x, dsm, abars, s_wm, s_wl, s_q, 1);
+}
+
 // standalone select over caller scores: grid n_heads, block kScoreThreads
 __global__ void __launch_bounds__(kScoreThreads)
 select_topk_kernel(const float *scores, int stride, const int32_t *n_valid, int topk,
@@ -796,6 +848,66 @@ cudaError_t launch_score(const StoreView &s, int dtype, int layer, const void *q
     if (s.D == 128)
         return launch_score_t<float, 128>(s, layer, q, unstable, period, force_due, topk, extra, scores, counters, do_select, batch, kv_prefetch, st);
     return launch_score_t<float, 64>(s, layer, q, unstable, period, force_due, topk, extra, scores, counters, do_select, batch, kv_prefetch, st);
+}
+
+// fused score + attend: head-aligned only (one CTA per head)
+template <typename T, int D, int NST, int NWA>
+static size_t score_attend_smem(const StoreView &s) {
+    return score_attend_ring_bytes<T, D, NST, NWA>(s.NCAP) + (sizeof(T) == 4 ? (size_t)s.G * D * sizeof(float) : 0);
+}
+
+template <typename T, int D, int NST, int NWA>
+static int score_attend_fits_t(const StoreView &s) {
+    auto k = score_attend_kernel<T, D, NST, NWA>;
+    const size_t smem = score_attend_smem<T, D, NST, NWA>(s);
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NWA * 32, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return occ >= 1;
+}
+
+template <typename T, int D, int NST, int NWA>
+static cudaError_t launch_score_attend_t(const StoreView &s, int layer, const void *q, const uint8_t *unstable,
+                                         int period, int force_due, int topk, int extra, float *scores,
+                                         int batch, int kv_prefetch, const AttnArgs &a, cudaStream_t st) {
+    if (!score_attend_fits_t<T, D, NST, NWA>(s)) return cudaErrorInvalidConfiguration;
+    return launch_pdl(score_attend_kernel<T, D, NST, NWA>, dim3(batch * s.H), dim3(NWA * 32),
+                      score_attend_smem<T, D, NST, NWA>(s), st, s, layer, (const T *)q, unstable, period, force_due,
+                      topk, extra, scores, kv_prefetch, a);
+}
+
+#define FC_SA_DISPATCH(dtype, D, CALL)                                                  \
+    ((dtype) == FC_BF16 ? ((D) == 128 ? CALL(__nv_bfloat16, 128, 3, 8) : CALL(__nv_bfloat16, 64, 6, 8)) \
+                        : ((D) == 128 ? CALL(float, 128, 3, 4) : CALL(float, 64, 6, 4)))
+
+// used when the batch fills the GPU with heads (the head-aligned scoring rule)
+int score_attend_supported(const StoreView &s, int dtype, int batch) {
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const bool head_mode = g_score_mode < 0 ? 2 * batch * s.H >= sms : g_score_mode == 1;
+    if (!head_mode || batch < 1) return 0;
+#define FC_SAF(T, DD, N, W) score_attend_fits_t<T, DD, N, W>(s)
+    return FC_SA_DISPATCH(dtype, s.D, FC_SAF);
+#undef FC_SAF
+}
+
+cudaError_t launch_score_attend(const StoreView &s, int dtype, int layer, const void *q, const uint8_t *unstable,
+                                int period, int force_due, int topk, int extra, float *scores, int batch,
+                                int kv_prefetch, const AttnArgs &a, cudaStream_t st) {
+#define FC_SAL(T, DD, N, W) \
+    launch_score_attend_t<T, DD, N, W>(s, layer, q, unstable, period, force_due, topk, extra, scores, batch, kv_prefetch, a, st)
+    return FC_SA_DISPATCH(dtype, s.D, FC_SAL);
+#undef FC_SAL
 }
 
 void set_score_mode(int m) { g_score_mode = m; }

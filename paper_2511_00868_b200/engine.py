@@ -74,6 +74,11 @@ class DecodeEngine:
         # False: one fc_sparse_decode launch per layer, measured faster at
         # config 2 (24.9 vs 37.6 us per layer)
         self.run_kernel = False
+        # True: scored layers run scoring, selection and attention in one
+        # launch (one CTA per head, fc_score_attend) when the batch fills the
+        # GPU with heads.  Default False: measured slower at config 2 (57.9 vs
+        # 55.9 us per scored layer)
+        self.fused_score_attend = False
         # profiling: score every head every step and record
         # the selections on the device (trace.TraceRecorder)
         self.score_all_heads = False
@@ -127,6 +132,7 @@ class DecodeEngine:
         st = self.store
         tiered_rerank = self.tiering and rerank and not force_due
         use_run = self.run_kernel and st.run_supported(self.B, self.att_bound)
+        use_fused = self.fused_score_attend and st.score_attend_supported(self.B)
 
         def recycles(l):
             return tiered_rerank and l in self._stable_layers
@@ -142,6 +148,15 @@ class DecodeEngine:
                 self.n_old.copy_(st.n_sel[:, layer])
                 self.n_copies.zero_()
             scored = scores(layer)
+            if scored and not recycle and use_fused:
+                # one launch: every head's CTA scores, selects and attends
+                st.score_attend(layer, self.q[layer], self.unstable, self.R, self.K, self.out[layer], self.B,
+                                force_due=force_due, extra_tokens=1, kv_prefetch=layer > 0,
+                                k_new=self.k_new[layer], v_new=self.v_new[layer], attend_appended=False)
+                if self.after_layer is not None:
+                    self.after_layer(layer)
+                layer += 1
+                continue
             if scored:
                 # the previous kernel (the last layer's attention) never writes this
                 # layer's summaries / selection: plan and warm L2 while it drains
@@ -246,19 +261,39 @@ class DecodeEngine:
         return g
 
     def launches_per_step(self, t: int) -> int:
-        """Library kernel launches in the step graph for step t: per layer an
-        attention launch (append fused), a scoring launch for every layer with
-        a due head, and the step advance."""
+        """Library kernel launches in the step graph for step t (mirrors
+        _launch_step): per layer a scoring launch when a head is due and an
+        attention launch (append fused) — one fused launch for both, or one
+        persistent launch per run of layers, when those are enabled — plus
+        the step advance (and the tier copies in two-tier mode)."""
         rerank = self.is_rerank_step(t)
-        flags = [not self._layer_skippable(l, rerank) for l in range(self.L)]
-        scored = sum(flags)
-        n_attn = self.L
-        if self.run_kernel and self.store.run_supported(self.B, self.att_bound) and self.after_layer is None:
-            breaks = [f or (self.tiering and rerank and l in self._stable_layers) for l, f in enumerate(flags)]
-            n_attn = 1 + sum(breaks[1:])  # one launch per run of layers
-        n = n_attn + scored + 1
+        st = self.store
+        use_run = self.run_kernel and st.run_supported(self.B, self.att_bound)
+        use_fused = self.fused_score_attend and st.score_attend_supported(self.B)
+
+        def recycles(l):
+            return self.tiering and rerank and l in self._stable_layers
+
+        def scores(l):
+            return self.score_all_heads or not self._layer_skippable(l, rerank)
+
+        n, layer = 1, 0  # the step advance
+        while layer < self.L:
+            if recycles(layer):
+                n += 2  # recycle + fetch
+            if scores(layer) and not recycles(layer) and use_fused:
+                n += 1
+                layer += 1
+                continue
+            n += 1 if scores(layer) else 0
+            end = layer + 1
+            if use_run and self.after_layer is None:
+                while end < self.L and not (scores(end) or recycles(end)):
+                    end += 1
+            n += 1
+            layer = end
         if self.tiering:
-            n += 1 + (2 * len(self._stable_layers) if rerank else 0)
+            n += 1  # offload of the page that just filled
         return n
 
     # -- host-buffer API (end-to-end path) -------------------------------------------

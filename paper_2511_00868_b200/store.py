@@ -167,6 +167,22 @@ class KVStore:
             extra_tokens, int(kv_prefetch), self.scores.data_ptr(), self.score_counters.data_ptr(),
             batch, self.stream()), "fc_score_select")
 
+    def score_attend_supported(self, batch: int) -> bool:
+        return bool(self.lib.fc_score_attend_supported(self.cptr, batch))
+
+    def score_attend(self, layer: int, q: torch.Tensor, unstable: torch.Tensor, period: int, topk: int,
+                     out: torch.Tensor, batch: int, *, force_due: bool = False, extra_tokens: int = 1,
+                     kv_prefetch: bool = False, k_new: torch.Tensor | None = None,
+                     v_new: torch.Tensor | None = None, lse: torch.Tensor | None = None,
+                     scale: float | None = None, attend_appended: bool = False) -> None:
+        """fc_score_attend: score_select then sparse_decode of one layer, one
+        CTA per head (same results as the two calls)."""
+        scale = 1.0 / math.sqrt(self.D) if scale is None else scale
+        _lib.check(self.lib.fc_score_attend(
+            self.cptr, layer, q.data_ptr(), unstable.data_ptr(), period, int(force_due), topk, extra_tokens,
+            int(kv_prefetch), self.scores.data_ptr(), _ptr(k_new), _ptr(v_new), out.data_ptr(), _ptr(lse),
+            scale, int(attend_appended), batch, self.stream()), "fc_score_attend")
+
     def score_pages(self, layer: int, q: torch.Tensor, batch: int, *, extra_tokens: int = 0) -> None:
         _lib.check(self.lib.fc_score_pages(self.cptr, layer, q.data_ptr(), extra_tokens,
                                            self.scores.data_ptr(), batch, self.stream()),

@@ -25,7 +25,7 @@ def _round(x, dtype):
 
 
 def run_engine_vs_oracle(*, B, L, H, G, D, T0, steps, K, R, frac, dtype, seed, use_graph,
-                         ragged=False, tiering=False, run_kernel=False):
+                         ragged=False, tiering=False, run_kernel=False, fused=False):
     from paper_2511_00868_b200.engine import DecodeEngine
     from paper_2511_00868_b200.stability import HeadProfile
     rng = np.random.default_rng(seed)
@@ -35,6 +35,7 @@ def run_engine_vs_oracle(*, B, L, H, G, D, T0, steps, K, R, frac, dtype, seed, u
                        ctx_cap_tokens=T0 + steps + 64, topk_pages=K, rerank_period=R,
                        profile=prof, dtype=dtype, tiering=tiering)
     eng.run_kernel = run_kernel
+    eng.fused_score_attend = fused
     dev = eng.device
     lens = [T0 + (17 * b if ragged else 0) for b in range(B)]
     keys = {}
@@ -178,6 +179,22 @@ def test_engine_head_aligned_scoring_matches_oracle(head_aligned_scoring, dtype,
                                             R=4, frac=0.5, dtype=dtype, seed=11, use_graph=True,
                                             ragged=True)
     assert ties <= 2
+
+
+@pytest.mark.parametrize("dtype,D,G", [(torch.bfloat16, 128, 4), (torch.float32, 128, 4),
+                                       (torch.bfloat16, 64, 7), (torch.float32, 64, 2)])
+def test_engine_fused_score_attend_matches_oracle(head_aligned_scoring, dtype, D, G):
+    """fc_score_attend: each head's CTA scores, selects and attends."""
+    worst, ties, eng = run_engine_vs_oracle(B=2, L=2, H=2, G=G, D=D, T0=1500, steps=10, K=8,
+                                            R=4, frac=0.5, dtype=dtype, seed=18, use_graph=True,
+                                            ragged=True, fused=True)
+    assert eng.launches_per_step(1) == 3  # fused layer 0, attention layer 1, advance
+    assert ties <= 2
+
+
+def test_engine_fused_tiered(head_aligned_scoring):
+    run_engine_vs_oracle(B=2, L=2, H=4, G=4, D=128, T0=400, steps=16, K=6, R=4, frac=0.5,
+                         dtype=torch.bfloat16, seed=19, use_graph=True, tiering=True, fused=True)
 
 
 def test_engine_head_aligned_tiered(head_aligned_scoring):

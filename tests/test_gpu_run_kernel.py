@@ -29,13 +29,15 @@ def _cuda():
         pytest.skip("needs a CUDA device")
 
 
-def _engine(run_kernel, B=16, L=4, H=8, G=4, D=128, T=2000, K=24, R=4, frac=0.25, steps=6, seed=3):
+def _engine(run_kernel, B=16, L=4, H=8, G=4, D=128, T=2000, K=24, R=4, frac=0.25, steps=6, seed=3,
+            fused=False):
     from paper_2511_00868_b200.engine import DecodeEngine
     from paper_2511_00868_b200.stability import HeadProfile
     from paper_2511_00868_b200.synthetic import device_normal
     eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=T + 64 + 16 * B,
                        topk_pages=K, rerank_period=R, profile=HeadProfile.first_n(L, H, frac))
     eng.run_kernel = run_kernel
+    eng.fused_score_attend = fused
     for b in range(B):
         for l in range(L):
             n = T + 13 * b  # ragged rows
@@ -121,3 +123,42 @@ def test_layers_call_lse_matches_per_layer(dtype):
     tol = 1e-2 if dtype == torch.bfloat16 else 1e-5
     assert ((o_run.float() - o_ref.float()).norm() / o_ref.float().norm()).item() < tol
     assert torch.allclose(lse_run, lse_ref, rtol=1e-5, atol=1e-5)
+
+
+def test_fused_score_attend_config2_heads_vs_oracle():
+    """fc_score_attend (one CTA per head scores, selects and attends) as the
+    engine's path for scored layers at 128 heads: selection == select_topk
+    over the GPU's own scores (exact), attention == float64 oracle on that
+    selection, summaries bit-identical to the unfused engine's."""
+    eng_f, out_f = _engine(False, L=2, frac=0.5, steps=5, seed=21, fused=True)
+    assert eng_f.fused_score_attend and eng_f.store.score_attend_supported(eng_f.B)
+    assert eng_f.launches_per_step(1) == 1 + 1 + 1  # fused layer 0, attention layer 1, advance
+    st = eng_f.store
+    B, L, H, G = eng_f.B, eng_f.L, eng_f.H, eng_f.G
+    seq = st.seq_len.cpu().numpy()
+    sel, n_sel = st.sel.cpu().numpy(), st.n_sel.cpu().numpy()
+    scores = st.scores.cpu().numpy()
+    out = eng_f.out.double().cpu().numpy()
+    q = eng_f.q.double().cpu().numpy()
+    K = eng_f.K
+    for bh in (0, 37, 90, 127):  # layer 0 (unstable, scored every step, scored last)
+        b, h = divmod(bh, H)
+        n_tok = int(seq[b])
+        n_pages = -(-n_tok // PS)
+        row = scores[bh, :n_pages - 1].astype(np.float64)
+        want_sel = O.select_topk_fast(np.append(row, 0.0), K, (n_pages - 1,))
+        got_sel = tuple(x for x in sel[b, 0, h, :n_sel[b, 0, h]].tolist() if x < n_pages)
+        assert got_sel == want_sel
+        k, v = st.gather(b, 0, h, n_pages)
+        k = k[:n_tok].double().cpu().numpy()
+        v = v[:n_tok].double().cpu().numpy()
+        want = O.gqa_sparse_decode(q[0, b, h * G:(h + 1) * G], k, v, PS, list(got_sel))
+        got = out[0, b, h * G:(h + 1) * G]
+        assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 2e-2, bh
+
+
+def test_fused_and_unfused_summaries_identical():
+    eng_f, _ = _engine(False, B=16, L=2, frac=0.5, steps=4, seed=22, fused=True)
+    eng_u, _ = _engine(False, B=16, L=2, frac=0.5, steps=4, seed=22, fused=False)
+    assert torch.equal(eng_f.store.summaries, eng_u.store.summaries)
+    assert torch.equal(eng_f.store.table, eng_u.store.table)
