@@ -426,6 +426,8 @@ def run_config3(args):
         eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D,
                            ctx_cap_tokens=T + steps_total + 16, topk_pages=K, rerank_period=R,
                            profile=prof, dtype=torch.bfloat16, device=dev, tiering=tiering)
+        if tiering and eng.stager is not None and os.environ.get("FC_STAGE_LEAD"):
+            eng.stager.lead = int(os.environ["FC_STAGE_LEAD"])  # profiling knob
         for l in range(L):
             k = device_normal((H, T, D), seed=12345 + 2 * l, device=dev)
             v = device_normal((H, T, D), seed=12346 + 2 * l, device=dev)
@@ -459,30 +461,46 @@ def run_config3(args):
         reranks = sum(1 for i in range(args.steps) if eng.is_rerank_step(eng.t + i))
         stream = torch.cuda.current_stream(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        kinds = []
+        hits0 = int(eng.stager.hits.item()) if tiering and eng.stager is not None else 0
         torch.cuda.synchronize(dev)
         e0.record(stream)
-        for _ in range(args.steps):
+        step_ev[0].record(stream)
+        for i in range(args.steps):
+            t = eng.t
+            lead = eng.stager.lead if tiering and eng.stager is not None else 0
+            kinds.append("rerank" if eng.is_rerank_step(t) else
+                         ("predict" if lead and (t + lead) % R == 0 else
+                          ("after_predict" if lead and (t + lead - 1) % R == 0 else "plain")))
             feed()
             eng.step()
+            step_ev[i + 1].record(stream)
         e1.record(stream)
         torch.cuda.synchronize(dev)
         eng.store.check_errors()
         ms = e0.elapsed_time(e1)
         out = {"ms_per_step": ms / args.steps, "tokens_s": B * args.steps / (ms / 1e3)}
+        by_kind = {}
+        for i, k in enumerate(kinds):
+            by_kind.setdefault(k, []).append(step_ev[i].elapsed_time(step_ev[i + 1]))
+        out["step_ms_by_kind"] = {k: sum(v) / len(v) for k, v in by_kind.items()}
+        if tiering and eng.stager is not None:
+            out["staged_hits"] = int(eng.stager.hits.item()) - hits0
         if tiering:
             fetched = int(eng.fetched_pages.item()) - fetched0
             pb = eng.store.page_bytes
             out.update(fetched_pages=fetched, fetched_mb_per_rerank=fetched * pb / max(reranks, 1) / 1e6,
                        promoted_fraction=fetched / max(reranks, 1) / (len(prof.stable) * B * (K - 1)))
             # host-link bandwidth of the fetch kernel alone, on the last copy list
-            n = int(eng.n_copies.item())
+            n = int(eng.n_copies[L - 1].item())
             if n > 0:
                 a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 ts = []
                 for _ in range(5):
                     torch.cuda._sleep(5_000_000)
                     a.record(stream)
-                    eng.tier.reload(L - 1, eng.copies, eng.n_copies)
+                    eng.tier.reload(L - 1, eng.copies[L - 1], eng.n_copies[L - 1:L])
                     b_.record(stream)
                     torch.cuda.synchronize(dev)
                     ts.append(a.elapsed_time(b_))

@@ -290,6 +290,47 @@ int fc_fetch_pages(const fc_store *s, int layer, const void *host_pages,
                    const int32_t *copies, const int32_t *n_copies,
                    int max_copies, void *stream);
 
+/* Reload staging — the paper's transfer/compute overlap:
+ * fc_stage_promoted diffs a PREDICTED selection (pred_sel / pred_n, same
+ * layout as the store's sel / n_sel, e.g. fc_score_select into a second
+ * fc_store view some steps before a rerank) of every stable (row, layer,
+ * head) against its resident set (its current selection) and fetches the
+ * pages it would promote that have a slow-tier copy (slow_resident) from
+ * host_pages into `staging` ([capacity] pages of device memory), recording
+ * staged_map[row][layer][head][page] = slot (-1 elsewhere) and stage_list
+ * [capacity][2] = (flat head, page); *stage_count counts them (pages past
+ * capacity are simply not staged).  Run it on a side stream while decode
+ * continues.  fc_fetch_pages_staged is fc_fetch_pages taking staged pages
+ * from `staging` (HBM) instead of the host link (+1 on *n_staged_hits per
+ * page, optional).  fc_stage_clear resets the map and the count after the
+ * rerank.  The rerank (selection, BlockTable.recycle, copy list) is
+ * unchanged: results are identical with or without staging. */
+int fc_fetch_pages_staged(const fc_store *s, int layer, const void *host_pages,
+                          const int32_t *copies, const int32_t *n_copies,
+                          int max_copies, const int32_t *staged_map,
+                          const void *staging, int32_t *n_staged_hits,
+                          void *stream);
+int fc_stage_promoted(const fc_store *s, const int32_t *pred_sel,
+                      const int32_t *pred_n, const uint8_t *unstable,
+                      const uint8_t *slow_resident, const void *host_pages,
+                      int32_t *staged_map, int32_t *stage_list,
+                      int32_t *stage_count, int capacity, void *staging,
+                      int batch, void *stream);
+/* The two halves of fc_stage_promoted: the diff / slot assignment (a few
+ * microseconds) and the host -> staging copies (on a few SMs, for a side
+ * stream beside decode). */
+int fc_stage_plan(const fc_store *s, const int32_t *pred_sel,
+                  const int32_t *pred_n, const uint8_t *unstable,
+                  const uint8_t *slow_resident, int32_t *staged_map,
+                  int32_t *stage_list, int32_t *stage_count, int capacity,
+                  int batch, void *stream);
+int fc_stage_fetch(const fc_store *s, const void *host_pages,
+                   const int32_t *stage_list, const int32_t *stage_count,
+                   int capacity, void *staging, void *stream);
+int fc_stage_clear(const fc_store *s, int32_t *staged_map,
+                   const int32_t *stage_list, int32_t *stage_count,
+                   int capacity, void *stream);
+
 /* Offload full pages of stable heads to the pinned host slow tier:
  * pages [n][4] = (row, layer, head, logical page), one write per page
  * (TierStore._record write-once ledger, tiering.py:99-157). */

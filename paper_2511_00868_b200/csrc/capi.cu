@@ -322,8 +322,68 @@ int fc_fetch_pages(const fc_store *s, int layer, const void *host_pages, const i
     if (!host_pages || !copies || !n_copies) return invalid("null buffer");
     if (max_copies <= 0) return FC_OK;
     const int pb = 2 * s->page_size * s->head_dim * (s->dtype == FC_BF16 ? 2 : 4);
-    return cuda_status(launch_fetch(make_view(s), layer, host_pages, copies, n_copies, max_copies, pb,
-                                    (cudaStream_t)stream));
+    return cuda_status(launch_fetch(make_view(s), layer, host_pages, copies, n_copies, max_copies, pb, nullptr,
+                                    nullptr, nullptr, (cudaStream_t)stream));
+}
+
+int fc_fetch_pages_staged(const fc_store *s, int layer, const void *host_pages, const int32_t *copies,
+                          const int32_t *n_copies, int max_copies, const int32_t *staged_map,
+                          const void *staging, int32_t *n_staged_hits, void *stream) {
+    FC_CHECK(check_store(s));
+    if (layer < 0 || layer >= s->layers) return invalid("layer out of range");
+    if (!host_pages || !copies || !n_copies || !staged_map || !staging) return invalid("null buffer");
+    if (max_copies <= 0) return FC_OK;
+    const int pb = 2 * s->page_size * s->head_dim * (s->dtype == FC_BF16 ? 2 : 4);
+    return cuda_status(launch_fetch(make_view(s), layer, host_pages, copies, n_copies, max_copies, pb, staged_map,
+                                    staging, n_staged_hits, (cudaStream_t)stream));
+}
+
+int fc_stage_promoted(const fc_store *s, const int32_t *pred_sel, const int32_t *pred_n, const uint8_t *unstable,
+                      const uint8_t *slow_resident, const void *host_pages, int32_t *staged_map,
+                      int32_t *stage_list, int32_t *stage_count, int capacity, void *staging, int batch,
+                      void *stream) {
+    FC_CHECK(check_store(s));
+    if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
+    if (!pred_sel || !pred_n || !unstable || !slow_resident || !host_pages || !staged_map || !stage_list ||
+        !stage_count || !staging)
+        return invalid("null buffer");
+    if (capacity < 1) return invalid("capacity must be >= 1");
+    if (batch == 0) return FC_OK;
+    const int pb = 2 * s->page_size * s->head_dim * (s->dtype == FC_BF16 ? 2 : 4);
+    return cuda_status(launch_stage(make_view(s), pred_sel, pred_n, unstable, slow_resident, staged_map, stage_list,
+                                    stage_count, capacity, host_pages, staging, pb, batch, (cudaStream_t)stream));
+}
+
+int fc_stage_plan(const fc_store *s, const int32_t *pred_sel, const int32_t *pred_n, const uint8_t *unstable,
+                  const uint8_t *slow_resident, int32_t *staged_map, int32_t *stage_list, int32_t *stage_count,
+                  int capacity, int batch, void *stream) {
+    FC_CHECK(check_store(s));
+    if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
+    if (!pred_sel || !pred_n || !unstable || !slow_resident || !staged_map || !stage_list || !stage_count)
+        return invalid("null buffer");
+    if (capacity < 1) return invalid("capacity must be >= 1");
+    if (batch == 0) return FC_OK;
+    return cuda_status(launch_stage_plan(make_view(s), pred_sel, pred_n, unstable, slow_resident, staged_map,
+                                         stage_list, stage_count, capacity, batch, (cudaStream_t)stream));
+}
+
+int fc_stage_fetch(const fc_store *s, const void *host_pages, const int32_t *stage_list, const int32_t *stage_count,
+                   int capacity, void *staging, void *stream) {
+    FC_CHECK(check_store(s));
+    if (!host_pages || !stage_list || !stage_count || !staging) return invalid("null buffer");
+    if (capacity < 1) return invalid("capacity must be >= 1");
+    const int pb = 2 * s->page_size * s->head_dim * (s->dtype == FC_BF16 ? 2 : 4);
+    return cuda_status(launch_stage_fetch(make_view(s), host_pages, stage_list, stage_count, capacity, staging, pb,
+                                          (cudaStream_t)stream));
+}
+
+int fc_stage_clear(const fc_store *s, int32_t *staged_map, const int32_t *stage_list, int32_t *stage_count,
+                   int capacity, void *stream) {
+    FC_CHECK(check_store(s));
+    if (!staged_map || !stage_list || !stage_count) return invalid("null buffer");
+    if (capacity < 1) return invalid("capacity must be >= 1");
+    return cuda_status(launch_stage_clear(make_view(s), staged_map, stage_list, stage_count, capacity,
+                                          (cudaStream_t)stream));
 }
 
 int fc_offload_pages(const fc_store *s, void *host_pages, const int32_t *pages, int n_pages, void *stream) {

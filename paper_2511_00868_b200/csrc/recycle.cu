@@ -222,16 +222,86 @@ FC_DEVINL void copy_page(uint4 *dst, const uint4 *src, int n16) {
     }
 }
 
+// staged_map (optional, [B][L][H][NCAP] int32, -1 = not staged): a promoted
+// page staged ahead of the rerank (stage_fetch_kernel) is copied from the
+// staging area in HBM instead of over the host link.
 __global__ void __launch_bounds__(kCopyThreads)
 fetch_kernel(StoreView s, int layer, const char *host_pages, const int32_t *copies,
-             const int32_t *n_copies, int max_copies, int page_bytes) {
+             const int32_t *n_copies, int max_copies, int page_bytes, const int32_t *staged_map,
+             const char *staging, int32_t *n_staged_hits) {
     const int n = min(*n_copies, max_copies);
     for (int c = blockIdx.x; c < n; c += gridDim.x) {
         const int b = copies[4 * c], h = copies[4 * c + 1], p = copies[4 * c + 2], blk = copies[4 * c + 3];
-        const int64_t src = (s.table_off(s.hix(b, layer, h), p)) * (int64_t)page_bytes;
+        const int64_t off = s.table_off(s.hix(b, layer, h), p);
+        const int slot = staged_map ? staged_map[off] : -1;
+        const char *src = slot >= 0 ? staging + (int64_t)slot * page_bytes : host_pages + off * (int64_t)page_bytes;
+        if (slot >= 0 && threadIdx.x == 0 && n_staged_hits) atomicAdd(n_staged_hits, 1);
         copy_page(reinterpret_cast<uint4 *>(reinterpret_cast<char *>(s.pool) + (int64_t)blk * page_bytes),
-                  reinterpret_cast<const uint4 *>(host_pages + src), page_bytes / 16);
+                  reinterpret_cast<const uint4 *>(src), page_bytes / 16);
     }
+}
+
+// ---------------------------------------------------------------------------
+// Reload staging (the paper's transfer/compute overlap, PAPER.md:221-224,
+// realised for the request itself): a selection predicted some steps before
+// a rerank (scored into a separate selection buffer) is diffed against the
+// resident set (= the current selection of a stable head); pages it would
+// promote that have a slow-tier copy are fetched host -> staging area on a
+// side stream while decode continues.  At the rerank, fetch_kernel takes
+// staged pages from HBM.  The rerank itself (selection, recycle, copy list)
+// is unchanged, so results are identical with or without staging.
+
+// one warp per (row, layer, head) of the stable heads
+__global__ void __launch_bounds__(256)
+stage_plan_kernel(StoreView s, const int32_t *pred_sel, const int32_t *pred_n, const uint8_t *unstable,
+                  const uint8_t *slow_resident, int32_t *staged_map, int32_t *stage_list, int32_t *stage_count,
+                  int cap, int batch) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int LH = s.L * s.H;
+    if (warp >= batch * LH) return;
+    const int b = warp / LH, lh = warp % LH, l = lh / s.H, h = lh % s.H;
+    if (unstable[lh]) return;
+    const int hx = s.hix(b, l, h);
+    const int32_t *cur = s.sel + (int64_t)hx * s.SELCAP;
+    const int ncur = s.n_sel[hx];
+    const int32_t *pred = pred_sel + (int64_t)hx * s.SELCAP;
+    const int npred = pred_n[hx];
+    for (int i = lane; i < npred; i += 32) {
+        const int p = pred[i];
+        int lo = 0, hi = ncur;  // resident set = the current (ascending) selection
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (cur[mid] < p) lo = mid + 1; else hi = mid;
+        }
+        if (lo < ncur && cur[lo] == p) continue;
+        const int64_t off = s.table_off(hx, p);
+        if (!slow_resident[off] || staged_map[off] >= 0) continue;
+        const int slot = atomicAdd(stage_count, 1);
+        if (slot >= cap) continue;  // staging area full: fetched from the host at the rerank
+        staged_map[off] = slot;
+        stage_list[2 * slot] = hx;
+        stage_list[2 * slot + 1] = p;
+    }
+}
+
+__global__ void __launch_bounds__(kCopyThreads)
+stage_fetch_kernel(StoreView s, const char *host_pages, const int32_t *stage_list, const int32_t *stage_count,
+                   int cap, char *staging, int page_bytes) {
+    const int n = min(*stage_count, cap);
+    for (int c = blockIdx.x; c < n; c += gridDim.x) {
+        const int64_t off = s.table_off(stage_list[2 * c], stage_list[2 * c + 1]);
+        copy_page(reinterpret_cast<uint4 *>(staging + (int64_t)c * page_bytes),
+                  reinterpret_cast<const uint4 *>(host_pages + off * (int64_t)page_bytes), page_bytes / 16);
+    }
+}
+
+__global__ void stage_clear_kernel(StoreView s, int32_t *staged_map, const int32_t *stage_list, int32_t *stage_count,
+                                   int cap) {
+    const int n = min(*stage_count, cap);
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
+        staged_map[s.table_off(stage_list[2 * c], stage_list[2 * c + 1])] = -1;
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0 && gridDim.x == 1) *stage_count = 0;
 }
 
 __global__ void __launch_bounds__(kCopyThreads)
@@ -331,10 +401,51 @@ cudaError_t launch_rerank(const StoreView &s, int layer, const int32_t *old_sel,
 }
 
 cudaError_t launch_fetch(const StoreView &s, int layer, const void *host_pages, const int32_t *copies,
-                         const int32_t *n_copies, int max_copies, int page_bytes, cudaStream_t st) {
+                         const int32_t *n_copies, int max_copies, int page_bytes, const int32_t *staged_map,
+                         const void *staging, int32_t *n_staged_hits, cudaStream_t st) {
     const int grid = max(1, min(max_copies, 148 * 8));
     fetch_kernel<<<grid, kCopyThreads, 0, st>>>(s, layer, (const char *)host_pages, copies, n_copies,
-                                                max_copies, page_bytes);
+                                                max_copies, page_bytes, staged_map, (const char *)staging,
+                                                n_staged_hits);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stage_plan(const StoreView &s, const int32_t *pred_sel, const int32_t *pred_n,
+                              const uint8_t *unstable, const uint8_t *slow_resident, int32_t *staged_map,
+                              int32_t *stage_list, int32_t *stage_count, int cap, int batch, cudaStream_t st) {
+    const int warps = batch * s.L * s.H;
+    if (warps == 0) return cudaSuccess;
+    stage_plan_kernel<<<(warps + 7) / 8, 256, 0, st>>>(s, pred_sel, pred_n, unstable, slow_resident, staged_map,
+                                                      stage_list, stage_count, cap, batch);
+    return cudaGetLastError();
+}
+
+// a few CTAs only: the copies run beside decode and must not take its SMs
+// (each CTA keeps 8 KiB of host reads in flight; 24 CTAs saturate the link)
+#ifndef FC_STAGE_CTAS
+#define FC_STAGE_CTAS 24
+#endif
+cudaError_t launch_stage_fetch(const StoreView &s, const void *host_pages, const int32_t *stage_list,
+                               const int32_t *stage_count, int cap, void *staging, int page_bytes, cudaStream_t st) {
+    stage_fetch_kernel<<<max(1, min(cap, FC_STAGE_CTAS)), kCopyThreads, 0, st>>>(
+        s, (const char *)host_pages, stage_list, stage_count, cap, (char *)staging, page_bytes);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stage(const StoreView &s, const int32_t *pred_sel, const int32_t *pred_n,
+                         const uint8_t *unstable, const uint8_t *slow_resident, int32_t *staged_map,
+                         int32_t *stage_list, int32_t *stage_count, int cap, const void *host_pages, void *staging,
+                         int page_bytes, int batch, cudaStream_t st) {
+    const int warps = batch * s.L * s.H;
+    if (warps == 0) return cudaSuccess;
+    stage_plan_kernel<<<(warps + 7) / 8, 256, 0, st>>>(s, pred_sel, pred_n, unstable, slow_resident, staged_map,
+                                                      stage_list, stage_count, cap, batch);
+    return launch_stage_fetch(s, host_pages, stage_list, stage_count, cap, staging, page_bytes, st);
+}
+
+cudaError_t launch_stage_clear(const StoreView &s, int32_t *staged_map, const int32_t *stage_list,
+                               int32_t *stage_count, int cap, cudaStream_t st) {
+    stage_clear_kernel<<<1, 1024, 0, st>>>(s, staged_map, stage_list, stage_count, cap);
     return cudaGetLastError();
 }
 

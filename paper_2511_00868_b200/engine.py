@@ -87,17 +87,28 @@ class DecodeEngine:
         # HBM; every full page lives once in the pinned host tier
         self.tiering = tiering
         self.tier = None
+        self.stager = None
         if tiering:
             from .tiering import TierStore
             self.tier = TierStore(self.store, profile)
             st = self.store
-            self.old_sel = torch.zeros((batch, kv_heads, st.SELCAP), dtype=torch.int32, device=self.device)
-            self.n_old = torch.zeros((batch, kv_heads), dtype=torch.int32, device=self.device)
-            self.copies = torch.zeros((batch * kv_heads * st.SELCAP, 4), dtype=torch.int32, device=self.device)
-            self.n_copies = torch.zeros(1, dtype=torch.int32, device=self.device)
+            # per layer (layer-major so each layer's slice is contiguous): the
+            # resident set before the rerank, the copy list and its length
+            self.old_sel = torch.zeros((layers, batch, kv_heads, st.SELCAP), dtype=torch.int32,
+                                       device=self.device)
+            self.n_old = torch.zeros((layers, batch, kv_heads), dtype=torch.int32, device=self.device)
+            self.copies = torch.zeros((layers, batch * kv_heads * st.SELCAP, 4), dtype=torch.int32,
+                                      device=self.device)
+            self.n_copies = torch.zeros(layers, dtype=torch.int32, device=self.device)
             self.fetched_pages = torch.zeros(1, dtype=torch.int64, device=self.device)
             self._stable_layers = [l for l in range(layers)
                                    if any(not profile.is_unstable(HeadId(l, h)) for h in range(kv_heads))]
+            # promoted pages staged on a side stream `lead` steps before each
+            # rerank (tiering.ReloadStager); None: every promotion crosses the
+            # host link inside the rerank step
+            from .tiering import ReloadStager
+            self.stager = ReloadStager(self.store, self.tier, self.unstable, topk_pages,
+                                       lead=min(2, max(1, rerank_period - 1)))
 
     # -- prefill ----------------------------------------------------------------
 
@@ -140,13 +151,13 @@ class DecodeEngine:
         def scores(l):
             return force_due or not self._layer_skippable(l, rerank)
 
+        if tiered_rerank:  # resident set of stable heads = their current selection
+            self.old_sel.copy_(st.sel.transpose(0, 1))
+            self.n_old.copy_(st.n_sel.transpose(0, 1))
+            self.n_copies.zero_()
         layer = 0
         while layer < self.L:
             recycle = recycles(layer)
-            if recycle:  # resident set of stable heads = their current selection
-                self.old_sel.copy_(st.sel[:, layer])
-                self.n_old.copy_(st.n_sel[:, layer])
-                self.n_copies.zero_()
             scored = scores(layer)
             if scored and not recycle and use_fused:
                 # one launch: every head's CTA scores, selects and attends
@@ -163,11 +174,14 @@ class DecodeEngine:
                 st.score_select(layer, self.q[layer], self.unstable, self.R, self.K, self.B,
                                 force_due=force_due, extra_tokens=1, kv_prefetch=layer > 0)
             if recycle:  # fused diff/recycle, then fetch the promoted pages over PCIe
-                st.rerank_recycle(layer, self.old_sel, self.n_old, self.unstable, self.R, self.copies,
-                                  self.n_copies, self.B, old_has_tail=False, extra_tokens=1,
+                nc = self.n_copies[layer:layer + 1]
+                st.rerank_recycle(layer, self.old_sel[layer], self.n_old[layer], self.unstable, self.R,
+                                  self.copies[layer], nc, self.B, old_has_tail=False, extra_tokens=1,
                                   slow_resident=self.tier.slow_resident)
-                self.tier.reload(layer, self.copies, self.n_copies)
-                self.fetched_pages.add_(self.n_copies)
+                if self.stager is not None:
+                    self.stager.fetch(layer, self.copies[layer], nc)
+                else:
+                    self.tier.reload(layer, self.copies[layer], nc)
             if use_run:
                 # persistent attention over the run of layers up to the next one
                 # that needs a selection / table update (or a per-layer hook)
@@ -196,6 +210,10 @@ class DecodeEngine:
             if self.after_layer is not None:
                 self.after_layer(layer)
             layer += 1
+        if tiered_rerank:
+            self.fetched_pages.add_(self.n_copies.sum())
+            if self.stager is not None:
+                self.stager.finish_rerank()
         st.step_advance(self.B)
         if self.recorder is not None:
             self.recorder.capture()
@@ -220,13 +238,19 @@ class DecodeEngine:
             if self.tiering:  # keep only the selection of stable heads in HBM
                 self.store.evict_unselected(self.unstable, self.B)
             self.selected = True
-        elif use_graph:
-            g = self._graphs.get((rerank, self.score_all_heads))
-            if g is None:
-                g = self._capture(rerank)
-            g.replay()
         else:
-            self._launch_step(rerank, force_due=self.score_all_heads)
+            if rerank and self.tiering and self.stager is not None:
+                self.stager.wait()  # staged promotions have landed
+            if use_graph:
+                g = self._graphs.get((rerank, self.score_all_heads))
+                if g is None:
+                    g = self._capture(rerank)
+                g.replay()
+            else:
+                self._launch_step(rerank, force_due=self.score_all_heads)
+            if (self.tiering and self.stager is not None and not self.score_all_heads
+                    and (self.t + self.stager.lead) % self.R == 0):
+                self.stager.predict(self.q, self.B, self._stable_layers)
         self.t += 1
         self.seq_host = [s + 1 for s in self.seq_host]
         return self.out
@@ -294,6 +318,8 @@ class DecodeEngine:
             layer = end
         if self.tiering:
             n += 1  # offload of the page that just filled
+            if rerank and self.stager is not None:
+                n += 1  # staging map clear
         return n
 
     # -- host-buffer API (end-to-end path) -------------------------------------------

@@ -266,6 +266,67 @@ class KVStore:
                                              step_base, trace_sel.shape[1], topk, extra_tokens, batch,
                                              self.stream()), "fc_trace_capture")
 
+    def _view_with_sel(self, sel: torch.Tensor, n_sel: torch.Tensor) -> int:
+        """An fc_store struct identical to this store's but whose selection
+        buffers are ``sel`` / ``n_sel`` (same shapes): scoring through it
+        writes a separate (e.g. predicted) selection."""
+        key = (sel.data_ptr(), n_sel.data_ptr())
+        views = self.__dict__.setdefault("_sel_views", {})
+        if key not in views:
+            if sel.shape != self.sel.shape or n_sel.shape != self.n_sel.shape:
+                raise ValueError("selection buffers must match the store's sel / n_sel shapes")
+            c = _lib.FcStore.from_buffer_copy(self._c)
+            c.sel, c.n_sel = sel.data_ptr(), n_sel.data_ptr()
+            views[key] = (c, (sel, n_sel))
+        return ctypes.addressof(views[key][0])
+
+    def score_select_into(self, layer: int, q: torch.Tensor, due_mask: torch.Tensor, topk: int, batch: int,
+                          sel_out: torch.Tensor, n_sel_out: torch.Tensor, scores_out: torch.Tensor,
+                          counters: torch.Tensor, *, extra_tokens: int = 1) -> None:
+        """fc_score_select of the heads flagged in ``due_mask`` ([L, H] uint8)
+        into the selection buffers ``sel_out`` / ``n_sel_out`` instead of the
+        store's own (reload prediction); own scores / counters workspaces."""
+        _lib.check(self.lib.fc_score_select(
+            self._view_with_sel(sel_out, n_sel_out), layer, q.data_ptr(), due_mask.data_ptr(), 1 << 30, 0,
+            topk, extra_tokens, 0, scores_out.data_ptr(), counters.data_ptr(), batch, self.stream()),
+            "fc_score_select")
+
+    def fetch_pages_staged(self, layer: int, host_pages: torch.Tensor, copies: torch.Tensor,
+                           n_copies: torch.Tensor, staged_map: torch.Tensor, staging: torch.Tensor,
+                           n_staged_hits: torch.Tensor | None = None) -> None:
+        _lib.check(self.lib.fc_fetch_pages_staged(
+            self.cptr, layer, host_pages.data_ptr(), copies.data_ptr(), n_copies.data_ptr(), copies.shape[0],
+            staged_map.data_ptr(), staging.data_ptr(), _ptr(n_staged_hits), self.stream()),
+            "fc_fetch_pages_staged")
+
+    def stage_promoted(self, pred_sel: torch.Tensor, pred_n: torch.Tensor, unstable: torch.Tensor,
+                       slow_resident: torch.Tensor, host_pages: torch.Tensor, staged_map: torch.Tensor,
+                       stage_list: torch.Tensor, stage_count: torch.Tensor, staging: torch.Tensor,
+                       batch: int) -> None:
+        _lib.check(self.lib.fc_stage_promoted(
+            self.cptr, pred_sel.data_ptr(), pred_n.data_ptr(), unstable.data_ptr(), slow_resident.data_ptr(),
+            host_pages.data_ptr(), staged_map.data_ptr(), stage_list.data_ptr(), stage_count.data_ptr(),
+            staging.shape[0], staging.data_ptr(), batch, self.stream()), "fc_stage_promoted")
+
+    def stage_plan(self, pred_sel: torch.Tensor, pred_n: torch.Tensor, unstable: torch.Tensor,
+                   slow_resident: torch.Tensor, staged_map: torch.Tensor, stage_list: torch.Tensor,
+                   stage_count: torch.Tensor, capacity: int, batch: int) -> None:
+        _lib.check(self.lib.fc_stage_plan(
+            self.cptr, pred_sel.data_ptr(), pred_n.data_ptr(), unstable.data_ptr(), slow_resident.data_ptr(),
+            staged_map.data_ptr(), stage_list.data_ptr(), stage_count.data_ptr(), capacity, batch,
+            self.stream()), "fc_stage_plan")
+
+    def stage_fetch(self, host_pages: torch.Tensor, stage_list: torch.Tensor, stage_count: torch.Tensor,
+                    staging: torch.Tensor) -> None:
+        _lib.check(self.lib.fc_stage_fetch(self.cptr, host_pages.data_ptr(), stage_list.data_ptr(),
+                                           stage_count.data_ptr(), staging.shape[0], staging.data_ptr(),
+                                           self.stream()), "fc_stage_fetch")
+
+    def stage_clear(self, staged_map: torch.Tensor, stage_list: torch.Tensor, stage_count: torch.Tensor,
+                    capacity: int) -> None:
+        _lib.check(self.lib.fc_stage_clear(self.cptr, staged_map.data_ptr(), stage_list.data_ptr(),
+                                           stage_count.data_ptr(), capacity, self.stream()), "fc_stage_clear")
+
     def fetch_pages(self, layer: int, host_pages: torch.Tensor, copies: torch.Tensor,
                     n_copies: torch.Tensor) -> None:
         _lib.check(self.lib.fc_fetch_pages(self.cptr, layer, host_pages.data_ptr(), copies.data_ptr(),

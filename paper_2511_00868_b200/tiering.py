@@ -107,3 +107,82 @@ class TierStore:
 
     def slow_pages(self, row: int, head: HeadId) -> set:
         return set(self._counts.get((row, HeadId(*head)), {}))
+
+
+class ReloadStager:
+    """Reload staging: the paper's transfer/compute overlap
+    for the request itself.  ``lead`` steps before a rerank, every stable head
+    is scored with that step's query into a separate PREDICTED selection
+    (fc_score_select through a second store view) on a side stream; the pages
+    it would promote that have a slow-tier copy are fetched host -> a staging
+    area in HBM there (fc_stage_promoted) while decode continues.  At the
+    rerank the real selection, recycle and copy list are computed as always;
+    fc_fetch_pages_staged takes every staged page from HBM and only the
+    mispredicted ones over the host link.  Results are identical with or
+    without staging."""
+
+    def __init__(self, store: KVStore, tier: TierStore, unstable: torch.Tensor, topk: int,
+                 lead: int = 2, capacity: int | None = None):
+        st = self.store = store
+        self.tier = tier
+        self.topk = topk
+        self.lead = lead
+        dev = st.device
+        n_stable = int((unstable == 0).sum().item())
+        if capacity is None:  # every stable head replacing its whole selection
+            capacity = max(1, min(st.B * n_stable * topk, 1 << 17))
+        self.capacity = capacity
+        self.unstable = unstable
+        self.stable_mask = (unstable == 0).to(torch.uint8).contiguous()
+        self.pred_sel = torch.zeros_like(st.sel)
+        self.pred_n = torch.zeros_like(st.n_sel)
+        self.pred_scores = torch.full_like(st.scores, float("-inf"))
+        self.pred_counters = torch.zeros_like(st.score_counters)
+        self.staged_map = torch.full(tuple(st.table.shape), -1, dtype=torch.int32, device=dev)
+        self.stage_list = torch.zeros((capacity, 2), dtype=torch.int32, device=dev)
+        self.stage_count = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.staging = torch.empty((capacity, 2, PAGE_SIZE, st.D), dtype=st.dtype, device=dev)
+        self.hits = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._hits32 = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.staged_pages = torch.zeros(1, dtype=torch.int64, device=dev)
+        # low priority: the host-link copies yield SMs to decode
+        self.stream = torch.cuda.Stream(dev, priority=0)
+        self.ev_input = torch.cuda.Event()
+        self.ev_staged = torch.cuda.Event()
+        self.pending = False
+
+    def predict(self, q: torch.Tensor, batch: int, layers) -> None:
+        """Predict and stage from the query ``q`` [L, B, Hq, d] of the step
+        that just ran (copied first: the caller may overwrite it)."""
+        # the prediction runs on the current stream (scoring kernels fill every
+        # SM: on a side stream they would stall the next step's launches); only
+        # the host-link copies go to the side stream, on a few SMs
+        main = torch.cuda.current_stream(self.store.device)
+        for layer in layers:
+            self.store.score_select_into(layer, q[layer], self.stable_mask, self.topk, batch,
+                                         self.pred_sel, self.pred_n, self.pred_scores, self.pred_counters)
+        self.store.stage_plan(self.pred_sel, self.pred_n, self.unstable, self.tier.slow_resident,
+                              self.staged_map, self.stage_list, self.stage_count, self.capacity, batch)
+        self.staged_pages.add_(self.stage_count.clamp(max=self.capacity).long())
+        self.ev_input.record(main)
+        with torch.cuda.stream(self.stream):
+            self.stream.wait_event(self.ev_input)
+            self.store.stage_fetch(self.tier.host, self.stage_list, self.stage_count, self.staging)
+            self.ev_staged.record(self.stream)
+        self.pending = True
+
+    def wait(self) -> None:
+        """Order the current stream after the staging copies (before a rerank)."""
+        if self.pending:
+            torch.cuda.current_stream(self.store.device).wait_event(self.ev_staged)
+            self.pending = False
+
+    def fetch(self, layer: int, copies: torch.Tensor, n_copies: torch.Tensor) -> None:
+        self.store.fetch_pages_staged(layer, self.tier.host, copies, n_copies, self.staged_map, self.staging,
+                                      self._hits32)
+
+    def finish_rerank(self) -> None:
+        """After the rerank's fetches (same stream): count hits, clear the map."""
+        self.hits.add_(self._hits32.long())
+        self._hits32.zero_()
+        self.store.stage_clear(self.staged_map, self.stage_list, self.stage_count, self.capacity)

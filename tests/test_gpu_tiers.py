@@ -220,3 +220,63 @@ def test_offload_evict_recycle_fetch_round_trip():
     got = out[0, G:2 * G].double().cpu().numpy()
     assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 2e-2
     del hk, pk
+
+
+def _tiered_run(staged, *, B=2, L=3, H=4, G=4, D=128, T=900, K=8, R=4, steps=12, drift=True):
+    """Tiered engine with AR(1)-drifting stable-head queries; returns outputs,
+    selections, tables and the engine."""
+    from paper_2511_00868_b200.engine import DecodeEngine
+    from paper_2511_00868_b200.stability import HeadProfile
+    from paper_2511_00868_b200.synthetic import device_normal
+    prof = HeadProfile.first_n(L, H, 0.25)
+    eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=T + steps + 64,
+                       topk_pages=K, rerank_period=R, profile=prof, tiering=True)
+    if not staged:
+        eng.stager = None
+    for b in range(B):
+        for l in range(L):
+            eng.prefill_layer(b, l, device_normal((H, T + 5 * b, D), seed=10 * b + l),
+                              device_normal((H, T + 5 * b, D), seed=500 + 10 * b + l), alloc=(l == 0))
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(4)
+    q = torch.randn(tuple(eng.q.shape), generator=gen, device="cuda")
+    outs = []
+    for _ in range(steps):
+        eps = torch.randn(tuple(q.shape), generator=gen, device="cuda")
+        q = 0.99 * q + (1 - 0.99 ** 2) ** 0.5 * eps if drift else eps
+        eng.q.copy_(q)
+        eng.k_new.normal_(generator=gen)
+        eng.v_new.normal_(generator=gen)
+        eng.step()
+        outs.append(eng.out.clone())
+    torch.cuda.synchronize()
+    eng.store.check_errors()
+    return torch.stack(outs), eng
+
+
+def test_reload_staging_identical_results_and_hits():
+    """Promotions staged two steps ahead on a side stream (ReloadStager):
+    outputs, selections, residency and fetched-page counts identical to the
+    unstaged engine; most promoted pages come from the staging area."""
+    out_s, eng_s = _tiered_run(True)
+    out_u, eng_u = _tiered_run(False)
+    assert torch.equal(out_s, out_u)
+    assert torch.equal(eng_s.store.sel, eng_u.store.sel)
+    # the same pages resident (block naming may differ: the post-prefill
+    # eviction frees blocks from parallel CTAs)
+    assert torch.equal(eng_s.store.table != 0, eng_u.store.table != 0)
+    fetched = int(eng_s.fetched_pages.item())
+    assert fetched == int(eng_u.fetched_pages.item()) and fetched > 0
+    hits = int(eng_s.stager.hits.item())
+    assert 0 < hits <= fetched
+    assert hits >= fetched // 4, (hits, fetched)   # drifting queries: the prediction mostly holds
+    # the run ends on a rerank step (t = 12): every staged page was consumed and cleared
+    assert int((eng_s.stager.staged_map >= 0).sum().item()) == 0
+    assert int(eng_s.stager.stage_count.item()) == 0
+
+
+def test_reload_staging_fresh_queries_still_exact():
+    """Unpredictable (fresh) queries: few hits, results still identical."""
+    out_s, eng_s = _tiered_run(True, drift=False, steps=10)
+    out_u, _ = _tiered_run(False, drift=False, steps=10)
+    assert torch.equal(out_s, out_u)
