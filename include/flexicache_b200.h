@@ -226,10 +226,13 @@ int fc_score_attend(const fc_store *s, int layer, const void *q,
  * [layer_begin, layer_begin + n_layers) in ONE launch (same semantics per
  * (layer, head) as fc_sparse_decode: sparse_decode, attention.py:85-111, the
  * attended set of simulator.py:416-420,512, fused update_minmax,
- * scoring.py:59-69).  One CTA per SM; every layer's attended pages are cut
- * into equal ranges over all warps of the grid; a grid barrier separates
- * layers (layer i's q and new token are consumed only after every output of
- * layer i-1 is written) while page copies run ahead across it.  Layer
+ * scoring.py:59-69).  Where every head's cluster of CTAs can be co-resident
+ * the kernel is the per-layer one's decomposition (one head per cluster,
+ * fc_sparse_decode_layers_split) looping over the layers; otherwise one CTA
+ * per SM with every layer's attended pages cut into equal ranges over all
+ * warps of the grid.  A grid barrier separates layers (layer i's q and new
+ * token are consumed only after every output of layer i-1 is written) while
+ * page copies run ahead across it.  Layer
  * layer_begin + i reads q + i*q_layer_stride, k_new/v_new + i*kv_layer_stride
  * and writes out + i*out_layer_stride (elements), lse + i*lse_layer_stride
  * (optional).  No layer of the run may need a selection / table update
@@ -242,6 +245,10 @@ int fc_score_attend(const fc_store *s, int layer, const void *q,
  * workspace: fc_sparse_decode_layers_workspace_size() bytes, zeroed once
  * (its counters reset themselves). */
 int fc_sparse_decode_layers_supported(const fc_store *s, int batch, int max_pages);
+/* CTAs per head (cluster size) of the per-head persistent kernel that
+ * fc_sparse_decode_layers uses for this batch, 0 when it falls back to the
+ * warp-balanced persistent kernel. */
+int fc_sparse_decode_layers_split(const fc_store *s, int batch, int max_pages);
 size_t fc_sparse_decode_layers_workspace_size(const fc_store *s, int batch, int max_pages);
 int fc_sparse_decode_layers(const fc_store *s, int layer_begin, int n_layers,
                             const void *q, int64_t q_layer_stride,

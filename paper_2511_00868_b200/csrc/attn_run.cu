@@ -569,7 +569,13 @@ static int run_plan_t(const StoreView &s, int batch, int max_pages, int *grid, i
     return 1;
 }
 
+// 0: per-head cluster persistent kernel when it fits (attn_persist.cu), else
+// the warp-balanced one; 1: warp-balanced always (test / profiling hook)
+static int g_run_mode = 0;
+void set_run_mode(int m) { g_run_mode = m; }
+
 int attn_run_supported(const StoreView &s, int dtype, int batch, int max_pages) {
+    if (g_run_mode == 0 && attn_persist_split(s, dtype, batch, max_pages) > 0) return 1;
     if (dtype == FC_BF16 && s.G > 16) return 0;
     if (dtype == FC_F32 && s.G > 8) return 0;
 #define FC_RP(T, DD, N, W_) run_plan_t<T, DD, N, W_>(s, batch, max_pages, nullptr, nullptr, nullptr)
@@ -604,6 +610,10 @@ cudaError_t launch_attn_run(const StoreView &s, int dtype, const RunArgs &a, int
     r.bar = (uint32_t *)w;
     r.head_cnt = (int32_t *)(w + (((size_t)s.L * 2 * sizeof(uint32_t) + 255) & ~(size_t)255));
     r.part = (float *)((char *)r.head_cnt + kRunMaxHeads * sizeof(int32_t));
+    if (g_run_mode == 0) {
+        const int S = attn_persist_split(s, dtype, a.batch, max_pages);
+        if (S > 0) return launch_attn_persist(s, dtype, r, S, st);
+    }
 #define FC_RL(T, DD, N, W_) launch_run_t<T, DD, N, W_>(s, r, max_pages, st)
     return FC_RUN_DISPATCH(dtype, s.D, FC_RL);
 #undef FC_RL

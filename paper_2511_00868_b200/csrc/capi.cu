@@ -70,6 +70,9 @@ int fc_debug_score_mode(int mode) { set_score_mode(mode); return FC_OK; }
 /* test hook: attention variant, 0 cluster per head (default), 1 balanced
  * all-SM variant for small head counts */
 int fc_debug_attn_mode(int mode) { set_attn_mode(mode); return FC_OK; }
+/* test hook: fc_sparse_decode_layers kernel, 0 per-head cluster persistent
+ * kernel when it fits (default), 1 warp-balanced persistent kernel */
+int fc_debug_run_mode(int mode) { set_run_mode(mode); return FC_OK; }
 
 int fc_alloc_pages(const fc_store *s, int row, int first_page, int n_pages, void *stream) {
     FC_CHECK(check_store(s));
@@ -248,6 +251,11 @@ int fc_sparse_decode(const fc_store *s, int layer, const void *q, const void *k_
 int fc_sparse_decode_layers_supported(const fc_store *s, int batch, int max_pages) {
     if (check_store(s) != FC_OK || batch < 1 || batch > s->batch_cap || max_pages < 1) return 0;
     return attn_run_supported(make_view(s), s->dtype, batch, max_pages);
+}
+
+int fc_sparse_decode_layers_split(const fc_store *s, int batch, int max_pages) {
+    if (check_store(s) != FC_OK || batch < 1 || batch > s->batch_cap || max_pages < 1) return 0;
+    return attn_persist_split(make_view(s), s->dtype, batch, max_pages);
 }
 
 size_t fc_sparse_decode_layers_workspace_size(const fc_store *s, int batch, int max_pages) {

@@ -47,6 +47,8 @@ struct RunArgs {
 int attn_run_supported(const StoreView &, int, int, int);
 size_t attn_run_workspace_bytes(const StoreView &, int, int, int);
 cudaError_t launch_attn_run(const StoreView &, int, const RunArgs &, int, void *, cudaStream_t);
+int attn_persist_split(const StoreView &, int, int, int);
+cudaError_t launch_attn_persist(const StoreView &, int, const RunArgs &, int, cudaStream_t);
 
 cudaError_t launch_alloc_pages(const StoreView &, int, int, int, cudaStream_t);
 cudaError_t launch_step_advance(const StoreView &, int, cudaStream_t);
@@ -68,6 +70,7 @@ cudaError_t set_run_trace(void *);
 cudaError_t set_score_trace(void *);
 void set_score_mode(int);
 void set_attn_mode(int);
+void set_run_mode(int);
 cudaError_t launch_trace_capture(const StoreView &, uint32_t *, uint32_t *, int, int, int, int, int, cudaStream_t);
 cudaError_t launch_trace_overlap(const uint32_t *, const uint32_t *, int, int, int, const int32_t *, int, int,
                                  int, int32_t *, cudaStream_t);

@@ -69,11 +69,13 @@ class DecodeEngine:
         # attention of heads a layer's scoring launch does not select starts
         # without waiting for it (fc_sparse_decode early_unstable)
         self.early_heads = True
-        # True: attention as persistent launches over runs of layers with no
-        # scoring / recycle between them (fc_sparse_decode_layers).  Default
-        # False: one fc_sparse_decode launch per layer, measured faster at
-        # config 2 (24.9 vs 37.6 us per layer)
-        self.run_kernel = False
+        # attention as persistent launches over runs of layers with no scoring /
+        # recycle between them (fc_sparse_decode_layers) — True / False, or
+        # None = auto: where the per-head persistent kernel splits heads over
+        # clusters (<= 74 heads per layer on 148 SMs; measured 1.6x faster
+        # steps at batch 1, 9 % at batch 4), per-layer launches above (equal
+        # or 2 % faster at config 2)
+        self.run_kernel = None
         # True: scored layers run scoring, selection and attention in one
         # launch (one CTA per head, fc_score_attend) when the batch fills the
         # GPU with heads.  Default False: measured slower at config 2 (57.9 vs
@@ -142,7 +144,7 @@ class DecodeEngine:
     def _launch_step(self, rerank: bool, force_due: bool) -> None:
         st = self.store
         tiered_rerank = self.tiering and rerank and not force_due
-        use_run = self.run_kernel and st.run_supported(self.B, self.att_bound)
+        use_run = self._use_run()
         use_fused = self.fused_score_attend and st.score_attend_supported(self.B)
 
         def recycles(l):
@@ -220,6 +222,11 @@ class DecodeEngine:
         if self.tiering:  # write-once offload of the page that just filled
             st.offload_filled(self.tier.host, self.unstable, self.tier.slow_resident, self.B)
 
+    def _use_run(self) -> bool:
+        if self.run_kernel is None:
+            return self.store.run_split(self.B, self.att_bound) >= 2
+        return bool(self.run_kernel) and self.store.run_supported(self.B, self.att_bound)
+
     def _layer_skippable(self, layer: int, rerank: bool) -> bool:
         # a representative step of the same kind: R (rerank) or 1 (plain, R > 1)
         t = self.R if rerank else (1 if self.R > 1 else self.R)
@@ -292,7 +299,7 @@ class DecodeEngine:
         the step advance (and the tier copies in two-tier mode)."""
         rerank = self.is_rerank_step(t)
         st = self.store
-        use_run = self.run_kernel and st.run_supported(self.B, self.att_bound)
+        use_run = self._use_run()
         use_fused = self.fused_score_attend and st.score_attend_supported(self.B)
 
         def recycles(l):

@@ -218,6 +218,10 @@ class KVStore:
         """Whether the persistent multi-layer kernel fits this geometry."""
         return bool(self.lib.fc_sparse_decode_layers_supported(self.cptr, batch, max_pages))
 
+    def run_split(self, batch: int, max_pages: int) -> int:
+        """CTAs per head of the per-head persistent kernel (0: warp-balanced)."""
+        return int(self.lib.fc_sparse_decode_layers_split(self.cptr, batch, max_pages))
+
     def sparse_decode_layers(self, layer: int, n_layers: int, q: torch.Tensor, out: torch.Tensor,
                              batch: int, *, max_pages: int, lse: torch.Tensor | None = None,
                              scale: float | None = None, extra_tokens: int = 1,

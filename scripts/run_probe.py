@@ -59,9 +59,24 @@ def runs(n):
 
 res = {}
 att_bytes = sum(eng.attention_bytes(l) for l in range(L))
+import ctypes  # noqa: E402
+st.lib.fc_debug_run_mode.argtypes = [ctypes.c_int]
+
+
+def moded(mode, fn):
+    def f():
+        st.lib.fc_debug_run_mode(mode)
+        try:
+            fn()
+        finally:
+            st.lib.fc_debug_run_mode(0)
+    return f
+
+
 cases = [("per_layer", per_layer)]
 if not os.environ.get("SKIP_RUN"):
-    cases += [("run1", runs(1)), ("run8", runs(8)), ("run32", runs(L))]
+    cases += [("persist1", runs(1)), ("persist8", runs(8)), ("persist32", runs(L)),
+              ("warpbal32", moded(1, runs(L)))]
 for name, fn in cases:
     us = timed(fn)
     st.check_errors()

@@ -25,7 +25,7 @@ def _round(x, dtype):
 
 
 def run_engine_vs_oracle(*, B, L, H, G, D, T0, steps, K, R, frac, dtype, seed, use_graph,
-                         ragged=False, tiering=False, run_kernel=False, fused=False):
+                         ragged=False, tiering=False, run_kernel=None, fused=False):
     from paper_2511_00868_b200.engine import DecodeEngine
     from paper_2511_00868_b200.stability import HeadProfile
     rng = np.random.default_rng(seed)

@@ -29,6 +29,19 @@ def _cuda():
         pytest.skip("needs a CUDA device")
 
 
+@pytest.fixture(params=[0, 1], ids=["per_head_clusters", "warp_balanced"])
+def run_mode(request):
+    """fc_sparse_decode_layers kernel: 0 the per-head cluster persistent
+    kernel (default where it fits), 1 the warp-balanced one."""
+    import ctypes
+    from paper_2511_00868_b200 import _lib
+    lib = _lib.load()
+    lib.fc_debug_run_mode.argtypes = [ctypes.c_int]
+    lib.fc_debug_run_mode(request.param)
+    yield request.param
+    lib.fc_debug_run_mode(0)
+
+
 def _engine(run_kernel, B=16, L=4, H=8, G=4, D=128, T=2000, K=24, R=4, frac=0.25, steps=6, seed=3,
             fused=False):
     from paper_2511_00868_b200.engine import DecodeEngine
@@ -57,7 +70,7 @@ def _engine(run_kernel, B=16, L=4, H=8, G=4, D=128, T=2000, K=24, R=4, frac=0.25
     return eng, torch.stack(outs)
 
 
-def test_run_kernel_config2_heads_vs_oracle_and_per_layer():
+def test_run_kernel_config2_heads_vs_oracle_and_per_layer(run_mode):
     eng_r, out_r = _engine(True)
     eng_p, out_p = _engine(False)
     st = eng_r.store
@@ -85,14 +98,14 @@ def test_run_kernel_config2_heads_vs_oracle_and_per_layer():
             assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 2e-2, (b, l, h)
 
 
-def test_run_kernel_deterministic():
+def test_run_kernel_deterministic(run_mode):
     _, a = _engine(True, B=8, L=3, steps=4, seed=9)
     _, b = _engine(True, B=8, L=3, steps=4, seed=9)
     assert torch.equal(a, b)
 
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
-def test_layers_call_lse_matches_per_layer(dtype):
+def test_layers_call_lse_matches_per_layer(dtype, run_mode):
     """Direct calls (no fused append, attend_appended): the run kernel over
     layers [0, L) vs fc_sparse_decode per layer, outputs and LSE."""
     from paper_2511_00868_b200.engine import DecodeEngine
@@ -162,3 +175,27 @@ def test_fused_and_unfused_summaries_identical():
     eng_u, _ = _engine(False, B=16, L=2, frac=0.5, steps=4, seed=22, fused=False)
     assert torch.equal(eng_f.store.summaries, eng_u.store.summaries)
     assert torch.equal(eng_f.store.table, eng_u.store.table)
+
+
+@pytest.mark.parametrize("B", [1, 4])
+def test_run_kernel_small_batch_clusters_vs_oracle(B, run_mode):
+    """Small batches: the per-head persistent kernel splits each head over a
+    cluster of up to 16 CTAs (DSMEM merge) for every layer of the run."""
+    eng, out = _engine(True, B=B, L=4, H=8, T=3000, K=32, frac=0.125, steps=5, seed=30 + B)
+    st = eng.store
+    L, H, G = eng.L, eng.H, eng.G
+    seq = st.seq_len.cpu().numpy()
+    sel, n_sel = st.sel.cpu().numpy(), st.n_sel.cpu().numpy()
+    o = eng.out.double().cpu().numpy()
+    q = eng.q.double().cpu().numpy()
+    for b in range(B):
+        for (l, h) in ((0, 0), (1, 3), (2, 5), (3, 7)):
+            n_tok = int(seq[b])
+            n_pages = -(-n_tok // PS)
+            k, v = st.gather(b, l, h, n_pages)
+            k = k[:n_tok].double().cpu().numpy()
+            v = v[:n_tok].double().cpu().numpy()
+            pages = [p for p in sel[b, l, h, :n_sel[b, l, h]].tolist() if p < n_pages]
+            want = O.gqa_sparse_decode(q[l, b, h * G:(h + 1) * G], k, v, PS, pages)
+            got = o[l, b, h * G:(h + 1) * G]
+            assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 2e-2, (b, l, h)
