@@ -427,7 +427,8 @@ def run_config3(args):
                            ctx_cap_tokens=T + steps_total + 16, topk_pages=K, rerank_period=R,
                            profile=prof, dtype=torch.bfloat16, device=dev, tiering=tiering)
         if tiering and eng.stager is not None and os.environ.get("FC_STAGE_LEAD"):
-            eng.stager.lead = int(os.environ["FC_STAGE_LEAD"])  # profiling knob
+            eng.stager.leads = tuple(int(x) for x in os.environ["FC_STAGE_LEAD"].split(","))  # profiling knob
+            eng.stager.lead = eng.stager.leads[0]
         for l in range(L):
             k = device_normal((H, T, D), seed=12345 + 2 * l, device=dev)
             v = device_normal((H, T, D), seed=12346 + 2 * l, device=dev)

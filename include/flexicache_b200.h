@@ -325,15 +325,18 @@ int fc_stage_promoted(const fc_store *s, const int32_t *pred_sel,
                       int batch, void *stream);
 /* The two halves of fc_stage_promoted: the diff / slot assignment (a few
  * microseconds) and the host -> staging copies (on a few SMs, for a side
- * stream beside decode). */
+ * stream beside decode).  Several predictions may stage before one rerank:
+ * pass k (0..3) records its slot range in stage_count[1 + 2k .. 2 + 2k]
+ * (stage_count has 9 ints; fc_stage_promoted is pass 0) and fc_stage_fetch
+ * of pass k copies exactly that range. */
 int fc_stage_plan(const fc_store *s, const int32_t *pred_sel,
                   const int32_t *pred_n, const uint8_t *unstable,
                   const uint8_t *slow_resident, int32_t *staged_map,
                   int32_t *stage_list, int32_t *stage_count, int capacity,
-                  int batch, void *stream);
+                  int batch, int pass, void *stream);
 int fc_stage_fetch(const fc_store *s, const void *host_pages,
                    const int32_t *stage_list, const int32_t *stage_count,
-                   int capacity, void *staging, void *stream);
+                   int capacity, void *staging, int pass, void *stream);
 int fc_stage_clear(const fc_store *s, int32_t *staged_map,
                    const int32_t *stage_list, int32_t *stage_count,
                    int capacity, void *stream);

@@ -79,8 +79,8 @@ _SIGNATURES = {
     "fc_fetch_pages_staged": (_i, [_p, _i, _p, _p, _p, _i, _p, _p, _p, _p]),
     "fc_stage_promoted": (_i, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _i, _p, _i, _p]),
     "fc_stage_clear": (_i, [_p, _p, _p, _p, _i, _p]),
-    "fc_stage_plan": (_i, [_p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _p]),
-    "fc_stage_fetch": (_i, [_p, _p, _p, _p, _i, _p, _p]),
+    "fc_stage_plan": (_i, [_p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _p]),
+    "fc_stage_fetch": (_i, [_p, _p, _p, _p, _i, _p, _i, _p]),
     "fc_evict_pages": (_i, [_p, _p, _i, _p]),
     "fc_offload_filled": (_i, [_p, _p, _p, _p, _i, _p]),
     "fc_evict_unselected": (_i, [_p, _p, _i, _p]),

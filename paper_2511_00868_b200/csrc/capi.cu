@@ -364,25 +364,26 @@ int fc_stage_promoted(const fc_store *s, const int32_t *pred_sel, const int32_t 
 
 int fc_stage_plan(const fc_store *s, const int32_t *pred_sel, const int32_t *pred_n, const uint8_t *unstable,
                   const uint8_t *slow_resident, int32_t *staged_map, int32_t *stage_list, int32_t *stage_count,
-                  int capacity, int batch, void *stream) {
+                  int capacity, int batch, int pass, void *stream) {
     FC_CHECK(check_store(s));
     if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
     if (!pred_sel || !pred_n || !unstable || !slow_resident || !staged_map || !stage_list || !stage_count)
         return invalid("null buffer");
     if (capacity < 1) return invalid("capacity must be >= 1");
-    if (batch == 0) return FC_OK;
+    if (pass < 0 || pass > 3) return invalid("pass must be in 0..3");
     return cuda_status(launch_stage_plan(make_view(s), pred_sel, pred_n, unstable, slow_resident, staged_map,
-                                         stage_list, stage_count, capacity, batch, (cudaStream_t)stream));
+                                         stage_list, stage_count, capacity, batch, pass, (cudaStream_t)stream));
 }
 
 int fc_stage_fetch(const fc_store *s, const void *host_pages, const int32_t *stage_list, const int32_t *stage_count,
-                   int capacity, void *staging, void *stream) {
+                   int capacity, void *staging, int pass, void *stream) {
     FC_CHECK(check_store(s));
     if (!host_pages || !stage_list || !stage_count || !staging) return invalid("null buffer");
     if (capacity < 1) return invalid("capacity must be >= 1");
+    if (pass < 0 || pass > 3) return invalid("pass must be in 0..3");
     const int pb = 2 * s->page_size * s->head_dim * (s->dtype == FC_BF16 ? 2 : 4);
     return cuda_status(launch_stage_fetch(make_view(s), host_pages, stage_list, stage_count, capacity, staging, pb,
-                                          (cudaStream_t)stream));
+                                          pass, (cudaStream_t)stream));
 }
 
 int fc_stage_clear(const fc_store *s, int32_t *staged_map, const int32_t *stage_list, int32_t *stage_count,

@@ -83,9 +83,9 @@ cudaError_t launch_fetch(const StoreView &, int, const void *, const int32_t *, 
 cudaError_t launch_stage(const StoreView &, const int32_t *, const int32_t *, const uint8_t *, const uint8_t *,
                          int32_t *, int32_t *, int32_t *, int, const void *, void *, int, int, cudaStream_t);
 cudaError_t launch_stage_plan(const StoreView &, const int32_t *, const int32_t *, const uint8_t *, const uint8_t *,
-                              int32_t *, int32_t *, int32_t *, int, int, cudaStream_t);
+                              int32_t *, int32_t *, int32_t *, int, int, int, cudaStream_t);
 cudaError_t launch_stage_fetch(const StoreView &, const void *, const int32_t *, const int32_t *, int, void *, int,
-                               cudaStream_t);
+                               int, cudaStream_t);
 cudaError_t launch_stage_clear(const StoreView &, int32_t *, const int32_t *, int32_t *, int, cudaStream_t);
 cudaError_t launch_offload(const StoreView &, void *, const int32_t *, int, int, cudaStream_t);
 cudaError_t launch_offload_filled(const StoreView &, void *, const uint8_t *, uint8_t *, int, int, cudaStream_t);

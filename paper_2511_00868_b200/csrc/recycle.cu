@@ -23,6 +23,7 @@ namespace fc {
 
 constexpr int kRecycleWarps = 4;
 constexpr int kListCap = 1024;  // max entries of an old/new selection list
+constexpr int kRecycleSlack = 64;  // pages appended since the old selection (old_has_tail)
 
 struct RerankWs {  // per head bh: [2 counts][kListCap free blocks][kListCap alloc pages]
     int32_t *base;
@@ -46,9 +47,22 @@ rerank_diff_kernel(StoreView s, int layer, const int32_t *__restrict__ old_sel,
                    int period, int force_due, int old_has_tail, int extra_tokens,
                    const uint8_t *__restrict__ slow_resident,
                    int32_t *copies, int max_copies, int32_t *n_copies, RerankWs ws, int batch) {
-    __shared__ int32_t s_ev[kRecycleWarps][kListCap];
-    __shared__ int32_t s_pr[kRecycleWarps][kListCap];
+    // per warp: old list | new list | old blocks | evicted | evicted blocks |
+    // promoted, sel_cap + slack entries each
+    // (both selections are staged in shared memory first: the membership
+    // tests are binary searches, which through global memory would chain
+    // ~8 dependent loads per entry)
+    extern __shared__ int32_t dsm_r[];
+    griddep_launch_dependents();
+    griddep_wait();  // the selection comes from the scoring launch before
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cap = s.SELCAP + kRecycleSlack;  // old list incl. pages appended since (old_has_tail)
+    int32_t *s_old = dsm_r + (int64_t)w * 6 * cap;
+    int32_t *s_new = s_old + cap;
+    int32_t *s_oblk = s_new + cap;   // block of old entry i
+    int32_t *s_evw = s_oblk + cap;   // evicted pages, ascending
+    int32_t *s_evblk = s_evw + cap;  // their blocks
+    int32_t *s_prw = s_evblk + cap;  // promoted pages, ascending
     const int bh = blockIdx.x * kRecycleWarps + w;
     if (bh >= batch * s.H) return;
     const int b = bh / s.H, h = bh % s.H;
@@ -70,48 +84,89 @@ rerank_diff_kernel(StoreView s, int layer, const int32_t *__restrict__ old_sel,
     const int n_new = s.n_sel[hx];
     int32_t *trow = s.table + s.table_off(hx, 0);
     const unsigned lt = (1u << lane) - 1u;
+    if (n_old_sel > s.SELCAP || n_new > s.SELCAP) {
+        if (lane == 0) { set_error(s.err, FC_ERR_SEL_CAP); cnt[0] = 0; cnt[1] = 0; }
+        return;
+    }
+    for (int i = lane; i < n_old_sel; i += 32) s_old[i] = olds[i];
+    for (int i = lane; i < n_new; i += 32) s_new[i] = news[i];
+    __syncwarp();
 
-    // evicted = old \ new (ascending), validating residency of old
+    // blocks of the old entries: every lane's loads issued before any use
+    // (this validation was a chain of dependent table reads per 32 entries)
+    if (n_old > cap) {
+        if (lane == 0) { set_error(s.err, FC_ERR_SEL_CAP); cnt[0] = 0; cnt[1] = 0; }
+        return;
+    }
+    for (int base = 0; base < n_old; base += 128) {
+        int xs[4], bl[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = base + u * 32 + lane;
+            xs[u] = i < n_old ? (i < n_old_sel ? s_old[i] : hi_old + 1 + (i - n_old_sel)) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) bl[u] = xs[u] >= 0 ? trow[xs[u]] : 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (xs[u] < 0) continue;
+            s_oblk[base + u * 32 + lane] = bl[u];
+            if (bl[u] == FC_NULL_BLOCK) set_error(s.err, FC_ERR_DOUBLE_EVICT);
+        }
+    }
+    __syncwarp();
+    // evicted = old \ new (ascending)
     int n_ev = 0;
     for (int base = 0; base < n_old; base += 32) {
         const int i = base + lane;
         bool ev = false;
         int x = 0;
         if (i < n_old) {
-            x = i < n_old_sel ? olds[i] : hi_old + 1 + (i - n_old_sel);
-            if (trow[x] == FC_NULL_BLOCK) set_error(s.err, FC_ERR_DOUBLE_EVICT);
-            ev = !sorted_contains(news, n_new, x);
+            x = i < n_old_sel ? s_old[i] : hi_old + 1 + (i - n_old_sel);
+            ev = !sorted_contains(s_new, n_new, x);
         }
         const unsigned mk = __ballot_sync(0xffffffffu, ev);
         if (ev) {
             const int r = n_ev + __popc(mk & lt);
-            if (r < kListCap) s_ev[w][r] = x;
+            if (r < cap) { s_evw[r] = x; s_evblk[r] = s_oblk[i]; }
         }
         n_ev += __popc(mk);
     }
-    // promoted = new \ old (ascending), validating non-residency and slow copy
+    // promoted = new \ old (ascending), then their validations (non-resident,
+    // slow copy present) with every lane's loads in flight together
     int n_pr = 0;
     for (int base = 0; base < n_new; base += 32) {
         const int i = base + lane;
         bool pr = false;
         int x = 0;
         if (i < n_new) {
-            x = news[i];
-            pr = (x > hi_res) || (x <= hi_old && !sorted_contains(olds, n_old_sel, x));
-            if (pr) {
-                if (trow[x] != FC_NULL_BLOCK) set_error(s.err, FC_ERR_DOUBLE_EVICT);
-                if (slow_resident && !slow_resident[s.table_off(hx, x)])
-                    set_error(s.err, FC_ERR_NULL_READ);
-            }
+            x = s_new[i];
+            pr = (x > hi_res) || (x <= hi_old && !sorted_contains(s_old, n_old_sel, x));
         }
         const unsigned mk = __ballot_sync(0xffffffffu, pr);
         if (pr) {
             const int r = n_pr + __popc(mk & lt);
-            if (r < kListCap) s_pr[w][r] = x;
+            if (r < cap) s_prw[r] = x;
         }
         n_pr += __popc(mk);
     }
-    if (n_ev > kListCap || n_pr > kListCap) {
+    __syncwarp();
+    for (int base = 0; base < min(n_pr, cap); base += 128) {
+        int bl[4], sr[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = base + u * 32 + lane;
+            const int x = i < min(n_pr, cap) ? s_prw[i] : -1;
+            bl[u] = x >= 0 ? trow[x] : FC_NULL_BLOCK;
+            sr[u] = (x >= 0 && slow_resident) ? slow_resident[s.table_off(hx, x)] : 1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (bl[u] != FC_NULL_BLOCK) set_error(s.err, FC_ERR_DOUBLE_EVICT);
+            if (!sr[u]) set_error(s.err, FC_ERR_NULL_READ);
+        }
+    }
+    if (n_ev > cap || n_pr > cap || n_ev > kListCap || n_pr > kListCap) {
         if (lane == 0) { set_error(s.err, FC_ERR_SEL_CAP); cnt[0] = 0; cnt[1] = 0; }
         return;
     }
@@ -121,8 +176,8 @@ rerank_diff_kernel(StoreView s, int layer, const int32_t *__restrict__ old_sel,
     if (lane == 0 && m > 0) cbase = atomicAdd(n_copies, m);
     cbase = __shfl_sync(0xffffffffu, cbase, 0);
     for (int i = lane; i < m; i += 32) {  // ascending pairs: evicted[i] hands its block to promoted[i]
-        const int e = s_ev[w][i], p = s_pr[w][i];
-        const int blk = trow[e];
+        const int e = s_evw[i], p = s_prw[i];
+        const int blk = s_evblk[i];
         trow[e] = FC_NULL_BLOCK;
         trow[p] = blk;
         if (cbase + i < max_copies) {
@@ -134,12 +189,12 @@ rerank_diff_kernel(StoreView s, int layer, const int32_t *__restrict__ old_sel,
     }
     int32_t *fr = ws.freed(bh);
     for (int i = m + lane; i < n_ev; i += 32) {  // surplus evictions
-        const int e = s_ev[w][i];
-        fr[i - m] = trow[e];
+        const int e = s_evw[i];
+        fr[i - m] = s_evblk[i];
         trow[e] = FC_NULL_BLOCK;
     }
     int32_t *al = ws.alloc(bh);
-    for (int i = m + lane; i < n_pr; i += 32) al[i - m] = s_pr[w][i];  // deficit pages
+    for (int i = m + lane; i < n_pr; i += 32) al[i - m] = s_prw[i];  // deficit pages
     if (lane == 0) { cnt[0] = n_ev - m; cnt[1] = n_pr - m; }
 }
 
@@ -150,6 +205,8 @@ rerank_commit_kernel(StoreView s, int layer, int32_t *copies, int max_copies, in
     using Scan = cub::BlockScan<int, 1024>;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ int s_fail;
+    griddep_launch_dependents();
+    griddep_wait();
     const int nh = batch * s.H;
     const int top0 = *s.free_top;
     // pass 1: pushes
@@ -229,6 +286,8 @@ __global__ void __launch_bounds__(kCopyThreads)
 fetch_kernel(StoreView s, int layer, const char *host_pages, const int32_t *copies,
              const int32_t *n_copies, int max_copies, int page_bytes, const int32_t *staged_map,
              const char *staging, int32_t *n_staged_hits) {
+    griddep_launch_dependents();
+    griddep_wait();  // the copy list comes from the recycle launch before
     const int n = min(*n_copies, max_copies);
     for (int c = blockIdx.x; c < n; c += gridDim.x) {
         const int b = copies[4 * c], h = copies[4 * c + 1], p = copies[4 * c + 2], blk = copies[4 * c + 3];
@@ -284,11 +343,17 @@ stage_plan_kernel(StoreView s, const int32_t *pred_sel, const int32_t *pred_n, c
     }
 }
 
+// stage_count layout: [0] slots taken; [1 + 2k], [2 + 2k] = first / end slot
+// of staging pass k (several predictions may stage before one rerank)
+constexpr int kStagePasses = 4;
+
+__global__ void stage_mark_kernel(int32_t *stage_count, int idx) { stage_count[idx] = stage_count[0]; }
+
 __global__ void __launch_bounds__(kCopyThreads)
 stage_fetch_kernel(StoreView s, const char *host_pages, const int32_t *stage_list, const int32_t *stage_count,
-                   int cap, char *staging, int page_bytes) {
-    const int n = min(*stage_count, cap);
-    for (int c = blockIdx.x; c < n; c += gridDim.x) {
+                   int cap, char *staging, int page_bytes, int pass) {
+    const int n = min(stage_count[2 + 2 * pass], cap);
+    for (int c = min(stage_count[1 + 2 * pass], cap) + blockIdx.x; c < n; c += gridDim.x) {
         const int64_t off = s.table_off(stage_list[2 * c], stage_list[2 * c + 1]);
         copy_page(reinterpret_cast<uint4 *>(staging + (int64_t)c * page_bytes),
                   reinterpret_cast<const uint4 *>(host_pages + off * (int64_t)page_bytes), page_bytes / 16);
@@ -301,7 +366,7 @@ __global__ void stage_clear_kernel(StoreView s, int32_t *staged_map, const int32
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
         staged_map[s.table_off(stage_list[2 * c], stage_list[2 * c + 1])] = -1;
     __syncthreads();
-    if (blockIdx.x == 0 && threadIdx.x == 0 && gridDim.x == 1) *stage_count = 0;
+    if (blockIdx.x == 0 && threadIdx.x < 1 + 2 * kStagePasses && gridDim.x == 1) stage_count[threadIdx.x] = 0;
 }
 
 __global__ void __launch_bounds__(kCopyThreads)
@@ -393,30 +458,40 @@ cudaError_t launch_rerank(const StoreView &s, int layer, const int32_t *old_sel,
                           int32_t *n_copies, void *workspace, int batch, cudaStream_t st) {
     RerankWs ws{reinterpret_cast<int32_t *>(workspace)};
     const int heads = batch * s.H;
-    rerank_diff_kernel<<<(heads + kRecycleWarps - 1) / kRecycleWarps, kRecycleWarps * 32, 0, st>>>(
-        s, layer, old_sel, n_old, unstable, period, force_due, old_has_tail, extra_tokens, slow_resident, copies, max_copies,
-        n_copies, ws, batch);
-    rerank_commit_kernel<<<1, 1024, 0, st>>>(s, layer, copies, max_copies, n_copies, ws, batch);
-    return cudaGetLastError();
+    const size_t smem = (size_t)kRecycleWarps * 6 * (s.SELCAP + kRecycleSlack) * sizeof(int32_t);
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && configured < smem) {
+        cudaFuncSetAttribute(rerank_diff_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = smem;
+    }
+    cudaError_t e = launch_pdl(rerank_diff_kernel, dim3((heads + kRecycleWarps - 1) / kRecycleWarps),
+                               dim3(kRecycleWarps * 32), smem, st, s, layer, old_sel, n_old, unstable, period,
+                               force_due, old_has_tail, extra_tokens, slow_resident, copies, max_copies, n_copies,
+                               ws, batch);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(rerank_commit_kernel, dim3(1), dim3(1024), 0, st, s, layer, copies, max_copies, n_copies, ws,
+                      batch);
 }
 
 cudaError_t launch_fetch(const StoreView &s, int layer, const void *host_pages, const int32_t *copies,
                          const int32_t *n_copies, int max_copies, int page_bytes, const int32_t *staged_map,
                          const void *staging, int32_t *n_staged_hits, cudaStream_t st) {
     const int grid = max(1, min(max_copies, 148 * 8));
-    fetch_kernel<<<grid, kCopyThreads, 0, st>>>(s, layer, (const char *)host_pages, copies, n_copies,
-                                                max_copies, page_bytes, staged_map, (const char *)staging,
-                                                n_staged_hits);
-    return cudaGetLastError();
+    return launch_pdl(fetch_kernel, dim3(grid), dim3(kCopyThreads), 0, st, s, layer, (const char *)host_pages,
+                      copies, n_copies, max_copies, page_bytes, staged_map, (const char *)staging, n_staged_hits);
 }
 
 cudaError_t launch_stage_plan(const StoreView &s, const int32_t *pred_sel, const int32_t *pred_n,
                               const uint8_t *unstable, const uint8_t *slow_resident, int32_t *staged_map,
-                              int32_t *stage_list, int32_t *stage_count, int cap, int batch, cudaStream_t st) {
+                              int32_t *stage_list, int32_t *stage_count, int cap, int batch, int pass,
+                              cudaStream_t st) {
+    if (pass < 0 || pass >= kStagePasses) return cudaErrorInvalidValue;
     const int warps = batch * s.L * s.H;
-    if (warps == 0) return cudaSuccess;
-    stage_plan_kernel<<<(warps + 7) / 8, 256, 0, st>>>(s, pred_sel, pred_n, unstable, slow_resident, staged_map,
-                                                      stage_list, stage_count, cap, batch);
+    stage_mark_kernel<<<1, 1, 0, st>>>(stage_count, 1 + 2 * pass);
+    if (warps > 0)
+        stage_plan_kernel<<<(warps + 7) / 8, 256, 0, st>>>(s, pred_sel, pred_n, unstable, slow_resident,
+                                                          staged_map, stage_list, stage_count, cap, batch);
+    stage_mark_kernel<<<1, 1, 0, st>>>(stage_count, 2 + 2 * pass);
     return cudaGetLastError();
 }
 
@@ -426,9 +501,11 @@ cudaError_t launch_stage_plan(const StoreView &s, const int32_t *pred_sel, const
 #define FC_STAGE_CTAS 24
 #endif
 cudaError_t launch_stage_fetch(const StoreView &s, const void *host_pages, const int32_t *stage_list,
-                               const int32_t *stage_count, int cap, void *staging, int page_bytes, cudaStream_t st) {
+                               const int32_t *stage_count, int cap, void *staging, int page_bytes, int pass,
+                               cudaStream_t st) {
+    if (pass < 0 || pass >= kStagePasses) return cudaErrorInvalidValue;
     stage_fetch_kernel<<<max(1, min(cap, FC_STAGE_CTAS)), kCopyThreads, 0, st>>>(
-        s, (const char *)host_pages, stage_list, stage_count, cap, (char *)staging, page_bytes);
+        s, (const char *)host_pages, stage_list, stage_count, cap, (char *)staging, page_bytes, pass);
     return cudaGetLastError();
 }
 
@@ -436,11 +513,10 @@ cudaError_t launch_stage(const StoreView &s, const int32_t *pred_sel, const int3
                          const uint8_t *unstable, const uint8_t *slow_resident, int32_t *staged_map,
                          int32_t *stage_list, int32_t *stage_count, int cap, const void *host_pages, void *staging,
                          int page_bytes, int batch, cudaStream_t st) {
-    const int warps = batch * s.L * s.H;
-    if (warps == 0) return cudaSuccess;
-    stage_plan_kernel<<<(warps + 7) / 8, 256, 0, st>>>(s, pred_sel, pred_n, unstable, slow_resident, staged_map,
-                                                      stage_list, stage_count, cap, batch);
-    return launch_stage_fetch(s, host_pages, stage_list, stage_count, cap, staging, page_bytes, st);
+    cudaError_t e = launch_stage_plan(s, pred_sel, pred_n, unstable, slow_resident, staged_map, stage_list,
+                                      stage_count, cap, batch, 0, st);
+    if (e != cudaSuccess) return e;
+    return launch_stage_fetch(s, host_pages, stage_list, stage_count, cap, staging, page_bytes, 0, st);
 }
 
 cudaError_t launch_stage_clear(const StoreView &s, int32_t *staged_map, const int32_t *stage_list,

@@ -110,7 +110,7 @@ class DecodeEngine:
             # host link inside the rerank step
             from .tiering import ReloadStager
             self.stager = ReloadStager(self.store, self.tier, self.unstable, topk_pages,
-                                       lead=min(2, max(1, rerank_period - 1)))
+                                       leads=(min(2, max(1, rerank_period - 1)),))
 
     # -- prefill ----------------------------------------------------------------
 
@@ -255,8 +255,10 @@ class DecodeEngine:
                 g.replay()
             else:
                 self._launch_step(rerank, force_due=self.score_all_heads)
+            if rerank and self.tiering and self.stager is not None:
+                self.stager.rerank_launched()
             if (self.tiering and self.stager is not None and not self.score_all_heads
-                    and (self.t + self.stager.lead) % self.R == 0):
+                    and any((self.t + ld) % self.R == 0 for ld in self.stager.leads)):
                 self.stager.predict(self.q, self.B, self._stable_layers)
         self.t += 1
         self.seq_host = [s + 1 for s in self.seq_host]

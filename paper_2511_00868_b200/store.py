@@ -284,6 +284,34 @@ class KVStore:
             views[key] = (c, (sel, n_sel))
         return ctypes.addressof(views[key][0])
 
+    def _all_layers_view(self, sel: torch.Tensor, n_sel: torch.Tensor) -> int:
+        """An fc_store view of every layer as ONE layer of L*H heads (flat
+        head index (b*L + l)*H + h is unchanged, so table, summaries and the
+        selection buffers are shared as they are) with the selection buffers
+        replaced: one scoring launch covers all layers."""
+        key = ("all", sel.data_ptr(), n_sel.data_ptr())
+        views = self.__dict__.setdefault("_sel_views", {})
+        if key not in views:
+            if sel.shape != self.sel.shape or n_sel.shape != self.n_sel.shape:
+                raise ValueError("selection buffers must match the store's sel / n_sel shapes")
+            c = _lib.FcStore.from_buffer_copy(self._c)
+            c.layers, c.kv_heads = 1, self.L * self.H
+            c.sel, c.n_sel = sel.data_ptr(), n_sel.data_ptr()
+            views[key] = (c, (sel, n_sel))
+        return ctypes.addressof(views[key][0])
+
+    def score_select_all_layers_into(self, q_bl: torch.Tensor, due_mask: torch.Tensor, topk: int, batch: int,
+                                     sel_out: torch.Tensor, n_sel_out: torch.Tensor, scores_out: torch.Tensor,
+                                     counters: torch.Tensor, *, extra_tokens: int = 1) -> None:
+        """fc_score_select of the heads flagged in ``due_mask`` ([L, H] uint8)
+        of EVERY layer in one launch, into ``sel_out`` / ``n_sel_out``.
+        q_bl: [B, L, Hq, d] (row-major over layers); scores_out:
+        [B*L*H, N_cap]; counters: [B*L*H]."""
+        _lib.check(self.lib.fc_score_select(
+            self._all_layers_view(sel_out, n_sel_out), 0, q_bl.data_ptr(), due_mask.data_ptr(), 1 << 30, 0,
+            topk, extra_tokens, 0, scores_out.data_ptr(), counters.data_ptr(), batch, self.stream()),
+            "fc_score_select")
+
     def score_select_into(self, layer: int, q: torch.Tensor, due_mask: torch.Tensor, topk: int, batch: int,
                           sel_out: torch.Tensor, n_sel_out: torch.Tensor, scores_out: torch.Tensor,
                           counters: torch.Tensor, *, extra_tokens: int = 1) -> None:
@@ -314,16 +342,16 @@ class KVStore:
 
     def stage_plan(self, pred_sel: torch.Tensor, pred_n: torch.Tensor, unstable: torch.Tensor,
                    slow_resident: torch.Tensor, staged_map: torch.Tensor, stage_list: torch.Tensor,
-                   stage_count: torch.Tensor, capacity: int, batch: int) -> None:
+                   stage_count: torch.Tensor, capacity: int, batch: int, pass_: int = 0) -> None:
         _lib.check(self.lib.fc_stage_plan(
             self.cptr, pred_sel.data_ptr(), pred_n.data_ptr(), unstable.data_ptr(), slow_resident.data_ptr(),
-            staged_map.data_ptr(), stage_list.data_ptr(), stage_count.data_ptr(), capacity, batch,
+            staged_map.data_ptr(), stage_list.data_ptr(), stage_count.data_ptr(), capacity, batch, pass_,
             self.stream()), "fc_stage_plan")
 
     def stage_fetch(self, host_pages: torch.Tensor, stage_list: torch.Tensor, stage_count: torch.Tensor,
-                    staging: torch.Tensor) -> None:
+                    staging: torch.Tensor, pass_: int = 0) -> None:
         _lib.check(self.lib.fc_stage_fetch(self.cptr, host_pages.data_ptr(), stage_list.data_ptr(),
-                                           stage_count.data_ptr(), staging.shape[0], staging.data_ptr(),
+                                           stage_count.data_ptr(), staging.shape[0], staging.data_ptr(), pass_,
                                            self.stream()), "fc_stage_fetch")
 
     def stage_clear(self, staged_map: torch.Tensor, stage_list: torch.Tensor, stage_count: torch.Tensor,

@@ -272,7 +272,7 @@ def test_reload_staging_identical_results_and_hits():
     assert hits >= fetched // 4, (hits, fetched)   # drifting queries: the prediction mostly holds
     # the run ends on a rerank step (t = 12): every staged page was consumed and cleared
     assert int((eng_s.stager.staged_map >= 0).sum().item()) == 0
-    assert int(eng_s.stager.stage_count.item()) == 0
+    assert int(eng_s.stager.stage_count[0].item()) == 0
 
 
 def test_reload_staging_fresh_queries_still_exact():
