@@ -11,6 +11,9 @@
 
 using namespace fc;
 
+// longest head the selection handles: 12288 pages (192k tokens at page 16)
+static constexpr int kMaxPagesCap = 12288;
+
 static thread_local char g_last_error[256] = "";
 
 static int cuda_status(cudaError_t e) {
@@ -137,7 +140,7 @@ int fc_score_select(const fc_store *s, int layer, const void *q, const uint8_t *
     if (topk > s->sel_cap) return FC_E_CAPACITY;
     if (extra_tokens < 0 || extra_tokens > 1) return invalid("extra_tokens must be 0 or 1");
     if (!q || !unstable || !scores_out || !counters) return invalid("null buffer");
-    if (s->pages_cap > 8192) return FC_E_CAPACITY;  /* 128k-token heads (block_select keys <= 32*256) */
+    if (s->pages_cap > kMaxPagesCap) return FC_E_CAPACITY;  /* block_select keys <= 48*256 */
     if (batch == 0) return FC_OK;
     return cuda_status(launch_score(make_view(s), s->dtype, layer, q, unstable, period, force_due, topk,
                                     extra_tokens, scores_out, counters, 1, batch, kv_prefetch ? 1 : 0,
@@ -145,7 +148,7 @@ int fc_score_select(const fc_store *s, int layer, const void *q, const uint8_t *
 }
 
 int fc_score_attend_supported(const fc_store *s, int batch) {
-    if (check_store(s) != FC_OK || batch < 1 || batch > s->batch_cap || s->pages_cap > 8192) return 0;
+    if (check_store(s) != FC_OK || batch < 1 || batch > s->batch_cap || s->pages_cap > kMaxPagesCap) return 0;
     return score_attend_supported(make_view(s), s->dtype, batch);
 }
 
@@ -164,7 +167,7 @@ int fc_score_attend(const fc_store *s, int layer, const void *q, const uint8_t *
     if ((k_new == nullptr) != (v_new == nullptr)) return invalid("k_new and v_new go together");
     if (k_new && extra_tokens != 1) return invalid("fused append needs extra_tokens = 1");
     if (!(scale > 0.f) || !std::isfinite(scale)) return invalid("scale must be positive");
-    if (s->pages_cap > 8192) return FC_E_CAPACITY;
+    if (s->pages_cap > kMaxPagesCap) return FC_E_CAPACITY;
     if (batch == 0) return FC_OK;
     const StoreView v = make_view(s);
     if (!score_attend_supported(v, s->dtype, batch)) {
@@ -196,7 +199,7 @@ int fc_select_topk(const float *scores, int stride, const int32_t *n_valid, int 
                    int32_t *sel_out, int32_t *n_out, void *stream) {
     if (topk < 1) return invalid("k must be >= 1");
     if (stride < 1 || n_heads < 0) return invalid("bad stride / n_heads");
-    if (stride > 8192) return FC_E_CAPACITY;
+    if (stride > kMaxPagesCap) return FC_E_CAPACITY;
     if (!scores || !n_valid || !sel_out || !n_out) return invalid("null buffer");
     if (n_heads == 0) return FC_OK;
     return cuda_status(launch_select(scores, stride, n_valid, n_heads, topk, pin_last, sel_out, n_out,

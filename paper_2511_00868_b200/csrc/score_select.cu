@@ -55,15 +55,31 @@ constexpr int kRoundsPerIter = FC_SCORE_ROUNDS;   // pages per lane-slot per ite
 // 0 < kprime < n <= 32*NT.
 constexpr int kSelBins = 2048;
 
+constexpr int kSelMaxKptAll = 48;  // = kSelMaxKpt below
+// shared scratch of one block_select, declared once for every keys-per-thread
+// variant (static shared arrays of separate instantiations would add up)
+template <int NT>
+struct SelScratch {
+    typename cub::BlockScan<int, NT>::TempStorage scan_tmp;
+    int hist[kSelBins];
+    uint32_t gt_bits[NT * kSelMaxKptAll / 32], eq_bits[NT * kSelMaxKptAll / 32];
+    int s_digit, s_above;
+    uint32_t s_kmin, s_kmax, s_T;
+    int s_rem, s_ncand, s_done;
+    uint32_t cand_key[32];
+    int cand_idx[32];
+};
+
 template <int NT, int KPT>
-__device__ void block_select_kpt(const uint32_t *keys, int n, int kprime, int32_t *out) {
+__device__ void block_select_kpt(const uint32_t *keys, int n, int kprime, int32_t *out, SelScratch<NT> &sc) {
     using Scan = cub::BlockScan<int, NT>;
     constexpr int BPT = kSelBins / NT;  // bins per thread
     constexpr int NWORDS = NT * KPT / 32;
-    __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ int hist[kSelBins];
-    __shared__ uint32_t gt_bits[NWORDS], eq_bits[NWORDS];
-    __shared__ int s_digit, s_above;
+    static_assert(KPT <= kSelMaxKptAll, "scratch sized for kSelMaxKptAll keys per thread");
+    auto &scan_tmp = sc.scan_tmp;
+    int *hist = sc.hist;
+    uint32_t *gt_bits = sc.gt_bits, *eq_bits = sc.eq_bits;
+    int &s_digit = sc.s_digit, &s_above = sc.s_above;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     uint32_t kv[KPT];
 #pragma unroll
@@ -77,10 +93,10 @@ __device__ void block_select_kpt(const uint32_t *keys, int n, int kprime, int32_
 #else
 #define FC_SEL_STAMP()
 #endif
-    __shared__ uint32_t s_kmin, s_kmax, s_T;
-    __shared__ int s_rem, s_ncand, s_done;
-    __shared__ uint32_t cand_key[32];
-    __shared__ int cand_idx[32];
+    uint32_t &s_kmin = sc.s_kmin, &s_kmax = sc.s_kmax, &s_T = sc.s_T;
+    int &s_rem = sc.s_rem, &s_ncand = sc.s_ncand, &s_done = sc.s_done;
+    uint32_t *cand_key = sc.cand_key;
+    int *cand_idx = sc.cand_idx;
     // ---- fast path: one pass of 2048 linear bins over [min key, max key]; the
     // crossing bin of a continuous score distribution holds a handful of keys,
     // ranked exactly by one warp.  Otherwise (ties / skew) the radix passes run.
@@ -227,28 +243,44 @@ __device__ void block_select_kpt(const uint32_t *keys, int n, int kprime, int32_
         }
     }
     __syncthreads();
-    // thread t < NWORDS owns bit-word t (indices 32t .. 32t+31, ascending)
-    static_assert(NWORDS <= NT, "one word per thread");
-    const uint32_t eqw = tid < NWORDS ? eq_bits[tid] : 0u;
-    const int eq_cnt = __popc(eqw);
+    // thread t owns bit-words [t*WPT, t*WPT + WPT) (indices ascending with t)
+    constexpr int WPT = (NWORDS + NT - 1) / NT;
+    uint32_t eqw[WPT], gtw[WPT];
+    int eq_cnt = 0;
+#pragma unroll
+    for (int u = 0; u < WPT; ++u) {
+        const int wd = tid * WPT + u;
+        eqw[u] = wd < NWORDS ? eq_bits[wd] : 0u;
+        gtw[u] = wd < NWORDS ? gt_bits[wd] : 0u;
+        eq_cnt += __popc(eqw[u]);
+    }
     int eq_before, dummy;
     Scan(scan_tmp).ExclusiveSum(eq_cnt, eq_before, dummy);
     __syncthreads();
     int take = max(0, min(eq_cnt, remaining - eq_before));  // lowest-index equal keys
-    uint32_t e = eqw, kept = 0;
-    while (take > 0 && e) {
-        const uint32_t low = e & (~e + 1u);
-        kept |= low;
-        e ^= low;
-        --take;
+    int sel_cnt = 0;
+#pragma unroll
+    for (int u = 0; u < WPT; ++u) {
+        uint32_t e = eqw[u], kept = 0;
+        while (take > 0 && e) {
+            const uint32_t low = e & (~e + 1u);
+            kept |= low;
+            e ^= low;
+            --take;
+        }
+        gtw[u] |= kept;
+        sel_cnt += __popc(gtw[u]);
     }
-    uint32_t selw = (tid < NWORDS ? gt_bits[tid] : 0u) | kept;
     int pos, total_sel;
-    Scan(scan_tmp).ExclusiveSum(__popc(selw), pos, total_sel);
-    while (selw) {
-        const int bit = __ffs(selw) - 1;
-        out[pos++] = tid * 32 + bit;
-        selw &= selw - 1;
+    Scan(scan_tmp).ExclusiveSum(sel_cnt, pos, total_sel);
+#pragma unroll
+    for (int u = 0; u < WPT; ++u) {
+        uint32_t selw = gtw[u];
+        while (selw) {
+            const int bit = __ffs(selw) - 1;
+            out[pos++] = (tid * WPT + u) * 32 + bit;
+            selw &= selw - 1;
+        }
     }
     __syncthreads();
     FC_SEL_STAMP();
@@ -257,10 +289,16 @@ __device__ void block_select_kpt(const uint32_t *keys, int n, int kprime, int32_
 #endif
 }
 
+// keys per thread by size: up to NT*48 keys (12288 pages at NT = 256, i.e.
+// 192k-token heads: config 4's 128k context plus generation)
+constexpr int kSelMaxKpt = 48;
 template <int NT>
 __device__ void block_select(const uint32_t *keys, int n, int kprime, int32_t *out) {
-    if (n <= NT * 8) block_select_kpt<NT, 8>(keys, n, kprime, out);
-    else block_select_kpt<NT, 32>(keys, n, kprime, out);
+    static_assert(kSelMaxKpt == kSelMaxKptAll, "one scratch size");
+    __shared__ SelScratch<NT> sc;
+    if (n <= NT * 8) block_select_kpt<NT, 8>(keys, n, kprime, out, sc);
+    else if (n <= NT * 32) block_select_kpt<NT, 32>(keys, n, kprime, out, sc);
+    else block_select_kpt<NT, kSelMaxKpt>(keys, n, kprime, out, sc);
 }
 
 // ---------------------------------------------------------------------------
@@ -921,8 +959,8 @@ cudaError_t launch_select(const float *scores, int stride, const int32_t *n_vali
                           cudaStream_t st) {
     const size_t smem = (size_t)stride * sizeof(uint32_t);
     static bool configured = false;
-    if (!configured) {  // keys up to 8192 (32 KiB) on top of ~12 KiB of static histogram
-        cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    if (!configured) {  // keys up to 12288 (48 KiB) on top of the static histogram / bit words
+        cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         configured = true;
     }
     select_topk_kernel<<<n_heads, kScoreThreads, smem, st>>>(scores, stride, n_valid, topk, pin_last,

@@ -33,22 +33,34 @@ def _cuda():
 def test_fullsize_32k_properties(score_mode):
     """score_mode 0: balanced multi-CTA scoring; 1: head-aligned (one CTA per
     head streaming 2048 summaries through the 32-chunk smem ring)."""
+    _with_score_mode(score_mode, lambda: _run_fullsize(B=2, T=32768))
+
+
+@pytest.mark.parametrize("score_mode", [0, 1])
+def test_fullsize_128k_properties(score_mode):
+    """Config 4's context: 128k tokens plus generation, so a head has more
+    than 8192 candidate pages (the selection's 48-keys-per-thread path on the
+    256-thread kernels)."""
+    _with_score_mode(score_mode, lambda: _run_fullsize(B=1, T=131072 + 40))
+
+
+def _with_score_mode(mode, fn):
     import ctypes
     from paper_2511_00868_b200 import _lib
     lib = _lib.load()
     lib.fc_debug_score_mode.argtypes = [ctypes.c_int]
-    lib.fc_debug_score_mode(score_mode)
+    lib.fc_debug_score_mode(mode)
     try:
-        _run_fullsize()
+        fn()
     finally:
         lib.fc_debug_score_mode(-1)
 
 
-def _run_fullsize():
+def _run_fullsize(B, T):
     from paper_2511_00868_b200.engine import DecodeEngine
     from paper_2511_00868_b200.stability import HeadProfile
     from paper_2511_00868_b200.synthetic import device_normal
-    B, L, H, G, D, T, K, R = 2, 2, 8, 4, 128, 32768, 128, 4
+    L, H, G, D, K, R = 2, 8, 4, 128, 128, 4
     prof = HeadProfile.first_n(L, H, 0.5)  # layer 0 unstable, layer 1 stable
     eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=T + 64,
                        topk_pages=K, rerank_period=R, profile=prof)
@@ -84,7 +96,7 @@ def _run_fullsize():
         # selection == select_topk over the GPU scores (layer 1 was scored last on rerank steps)
         if t % R == 0 or step == 0:
             scores = st.scores.cpu().numpy()
-            for bh in (0, 5, 9, 15):
+            for bh in [x for x in (0, 5, 9, 15) if x < B * H]:
                 b, h = divmod(bh, H)
                 n_pages = -(-int(seq[b]) // PS)
                 row = scores[bh, :n_pages - 1].astype(np.float64)
@@ -95,7 +107,7 @@ def _run_fullsize():
     out = eng.out.double().cpu().numpy()
     q = eng.q.double().cpu().numpy()
     summ = st.summaries.double().cpu().numpy()
-    for (b, l, h) in ((0, 0, 3), (1, 1, 6)):
+    for (b, l, h) in ((0, 0, 3), (B - 1, 1, 6)):
         n_tok = int(seq[b])
         n_pages = -(-n_tok // PS)
         k, v = st.gather(b, l, h, n_pages)
