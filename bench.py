@@ -37,6 +37,14 @@ CFG2 = dict(workload="config2: llama3.1-8b-shaped decode, 32 layers, 32q/8kv hea
             layers=32, kv_heads=8, group=4, head_dim=128, ctx=32768, batch=16, topk=128,
             period=16, unstable_fraction=0.25)
 METRIC = "decode-attn tokens/s/GPU at 32k ctx, % HBM roofline, vs CPU ref"
+# config 4: 128k context, 64 requests sharded over the GPUs request-parallel
+# (no collective).  A GPU holds at most 8 such requests fully resident (146 GB
+# of KV + summaries), so below 8 GPUs each rank runs the 8-GPU per-GPU share
+# (weak-scaling unit) and says so in the config.
+CFG4 = dict(workload="config4: llama3.1-8b-shaped decode, 32 layers, 32q/8kv heads, d=128, 128k ctx, "
+                     "64 requests request-parallel over the GPUs, page 16, top-K 128 pages, R=16, u=0.25",
+            layers=32, kv_heads=8, group=4, head_dim=128, ctx=131072, batch=8, topk=128,
+            period=16, unstable_fraction=0.25, total_requests=64)
 
 
 
@@ -61,8 +69,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=CFG2["batch"])
     ap.add_argument("--ctx", type=int, default=CFG2["ctx"])
     ap.add_argument("--layers", type=int, default=CFG2["layers"])
-    ap.add_argument("--config", type=int, choices=[2, 3, 5], default=2,
+    ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=2,
                     help="2: the metric's config (default); 3: long generation with host offload; "
+                         "4: 128k ctx, 64 requests request-parallel (per-GPU share); "
                          "5: Qwen2.5-7B-shaped, KV-head-sharded with an all-gather of outputs")
     return ap.parse_args()
 
@@ -374,7 +383,8 @@ def run_ours(args, cfg):
                    "kv_heads": H, "q_heads": H * G, "head_dim": D, "page": 16, "topk_pages": K,
                    "rerank_period": R, "unstable_fraction": cfg["unstable_fraction"],
                    "parallelism": f"request-parallel x{world}",
-                   "l2": "inputs larger than L2 (5+ GiB touched per step vs 126 MB L2)"},
+                   "l2": "inputs larger than L2 (5+ GiB touched per step vs 126 MB L2)",
+                   **({"share": cfg["share"]} if "share" in cfg else {})},
         "gpu_launches": launches,
         "step_ms": step_stats,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -635,6 +645,14 @@ def main():
         run_config3(args)
     elif args.config == 5:
         run_config5(args)
+    elif args.config == 4:
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        cfg = dict(CFG4)
+        per = CFG4["total_requests"] // max(world, 1)
+        cfg["batch"] = min(per, 8)
+        cfg["share"] = ("64 requests / %d GPUs" % world if per <= 8 else
+                        "per-GPU share of the 8-GPU run (8 of 64 requests; %d per GPU does not fit HBM)" % per)
+        run_ours(args, cfg)
     else:
         run_ours(args, cfg)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:

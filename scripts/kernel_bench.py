@@ -12,7 +12,8 @@ from paper_2511_00868_b200.engine import DecodeEngine  # noqa: E402
 from paper_2511_00868_b200.stability import HeadProfile  # noqa: E402
 from paper_2511_00868_b200.synthetic import device_normal  # noqa: E402
 
-B, L, H, G, D, T, K, R = int(os.environ.get("B", 16)), int(os.environ.get("L", 32)), 8, 4, 128, 32768, 128, 16
+B, L, H, G, D, T, K, R = (int(os.environ.get("B", 16)), int(os.environ.get("L", 32)), 8, 4, 128,
+                          int(os.environ.get("T", 32768)), 128, 16)
 dev = torch.device("cuda", 0)
 eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=T + 64,
                    topk_pages=K, rerank_period=R, profile=HeadProfile.first_n(L, H, 0.25), device=dev)
