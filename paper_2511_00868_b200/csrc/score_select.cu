@@ -551,7 +551,22 @@ score_select_kernel(StoreView s, int layer, const T *__restrict__ q,
         if (!s_last) continue;
         const int n_cand = h_end - h_beg;
         const int n_pages = n_cand + 1;
-        for (int i = tid; i < n_cand; i += blockDim.x) keys[i] = score_key(__ldcg(row + i));
+        // the head's scores (written by every CTA of the head) into keys: 8
+        // loads in flight per thread (a load-then-store loop would serialise
+        // ~n/256 L2 round trips: ~20 us for a 128k-token head)
+        for (int i0 = tid; i0 < n_cand; i0 += blockDim.x * 8) {
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * blockDim.x;
+                v[u] = i < n_cand ? __ldcg(row + i) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * blockDim.x;
+                if (i < n_cand) keys[i] = score_key(v[u]);
+            }
+        }
         if (tid == 0) row[n_pages - 1] = -INFINITY;  // pinned page: not scored
         __syncthreads();
         const int kprime = topk - 1;  // n_pages > topk, so kprime < n_cand
@@ -813,7 +828,19 @@ select_topk_kernel(const float *scores, int stride, const int32_t *n_valid, int 
         return;
     }
     const float *row = scores + (int64_t)hd * stride;
-    for (int i = threadIdx.x; i < n_cand; i += blockDim.x) dyn_keys[i] = score_key(row[i]);
+    for (int i0 = threadIdx.x; i0 < n_cand; i0 += blockDim.x * 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x;
+            v[u] = i < n_cand ? row[i] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x;
+            if (i < n_cand) dyn_keys[i] = score_key(v[u]);
+        }
+    }
     __syncthreads();
     if (kprime > 0) block_select<kScoreThreads>(dyn_keys, n_cand, kprime, out);
     if (threadIdx.x == 0) {
