@@ -63,13 +63,16 @@ FC_DEVINL uint32_t ld_acquire(const uint32_t *p) {
     return v;
 }
 
-FC_DEVINL int ld_acquire_cta(const int *p) {
-    int v;
-    asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+// CTA-scope flag in shared memory: atomic read / write with block fences
+// (acquire / release semantics; atomics also keep racecheck informed)
+FC_DEVINL int ld_acquire_cta(int *p) {
+    const int v = atomicAdd(p, 0);
+    __threadfence_block();
     return v;
 }
 FC_DEVINL void st_release_cta(int *p, int v) {
-    asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+    __threadfence_block();
+    atomicExch(p, v);
 }
 
 // per-warp plan of one layer: [prefix: nh+1 ints][blk: maxr][bh: maxr][pg: maxr]
