@@ -123,6 +123,21 @@ def test_select_topk_random_ties_large():
         assert got.pages == O.select_topk_fast(scores, k, (n - 1,))
 
 
+def test_select_topk_beyond_8192_candidates():
+    """The 48-keys-per-thread selection path (8192 < n <= 12288: config 4's
+    128k context plus generation): tie-heavy and continuous scores, small and
+    large k, exact against the oracle's select_topk."""
+    from paper_2511_00868_b200.scoring import select_topk
+    rng = np.random.default_rng(12)
+    for n in (8193, 9001, 10240, 12288):
+        for k in (1, 2, 128, 1000):
+            for ties in (True, False):
+                scores = (rng.integers(-3, 4, size=n).astype(float) if ties
+                          else rng.standard_normal(n).astype(np.float32).astype(float))
+                got = select_topk(scores, k, pinned=(n - 1,))
+                assert got.pages == O.select_topk_fast(scores, k, (n - 1,)), (n, k, ties)
+
+
 # ---------------------------------------------------------------------------
 # (3) attention
 
