@@ -642,6 +642,8 @@ __device__ void score_head_body(const StoreView &s, int layer, const T *__restri
     constexpr int LPP = Gm::kLanesPerPage, CPL = Gm::kChunksPerLane, EPC = Gm::kElemsPerChunk;
     static_assert(R >= 1 && R <= LPP, "chunk geometry");
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    unsigned long long *trace = g_score_trace;  // [grid][4]: entry, copies issued, streamed, selected
+    if (trace && tid == 0) trace[blockIdx.x * 4] = gtimer_s();
     if (!kv_prefetch) griddep_wait();
     const int bh = blockIdx.x, b = bh / s.H, h = bh % s.H;
     const bool due = force_due || unstable[layer * s.H + h] || (*s.step % period == 0);
@@ -673,6 +675,7 @@ __device__ void score_head_body(const StoreView &s, int layer, const T *__restri
             bulk_g2s(ring + (size_t)c * HG::kChunkBytes, base + (int64_t)c * HG::kChunkBytes, bytes, &full[c]);
         }
     }
+    if (trace && tid == 0) trace[blockIdx.x * 4 + 1] = gtimer_s();
     if (kv_prefetch) griddep_wait();  // q comes from the previous launch
     load_group_coeffs<T>(s, q, b, h, w);
     __syncthreads();
@@ -758,11 +761,13 @@ __device__ void score_head_body(const StoreView &s, int layer, const T *__restri
     }
     if (tid == 0) srow[n_pages - 1] = -INFINITY;  // pinned page: not scored
     __syncthreads();
+    if (trace && tid == 0) trace[blockIdx.x * 4 + 2] = gtimer_s();
     const int kprime = topk - 1;  // n_pages > topk, so kprime < n_cand
     if (kprime > 0) block_select<NW * 32>(keys, n_cand, kprime, out);
     if (tid == 0) {
         out[kprime] = n_pages - 1;
         s.n_sel[hx] = topk;
+        if (trace) trace[blockIdx.x * 4 + 3] = gtimer_s();
     }
 }
 
