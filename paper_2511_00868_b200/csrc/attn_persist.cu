@@ -29,6 +29,16 @@ FC_DEVINL uint32_t p_ld_acquire(const uint32_t *p) {
     return v;
 }
 
+// Optional per-CTA timeline (globaltimer ns) for profiling: [grid][33][4];
+// [li] = layer top, consumption start (barrier passed, q loaded),
+// consumption end, outputs published; [32] = entry.  Null in production.
+__device__ unsigned long long *g_persist_trace = nullptr;
+FC_DEVINL unsigned long long p_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 // One warp's share of one layer of its head: the head, its range of
 // attended entries and (lane i) the physical block of entry j0 + i.
 struct PersistPlan {
@@ -74,12 +84,15 @@ attn_persist_kernel(StoreView s, RunArgs a, int S) {
     const int64_t qoff = ((int64_t)b * s.H * G + (int64_t)h * G) * D;
     uint32_t *bar = a.bar + 2 * a.l0;
 
+    unsigned long long *trace = g_persist_trace ? g_persist_trace + (size_t)blockIdx.x * 33 * 4 : nullptr;
+    if (trace && tid == 0) trace[32 * 4] = p_gtimer();
     if (tid < NW * NST) mbar_init(&bars[tid], 1);
     fence_mbar_init();
     __syncthreads();
     if (a.nl == 1) griddep_launch_dependents();
     if (a.first_dep) griddep_wait();
 
+    bool cl_wait_pending = false;  // split cluster barrier: a deferred wait
     PersistPlan cur = persist_plan(s, a, a.l0, bh, kw, nwt, lane), nxt{};
     bool nxt_ready = false;
     int issued = 0, cons = 0, il = 0, ie = 0;  // issue pointer: layer offset (0 cur, 1 next), entry
@@ -112,6 +125,8 @@ attn_persist_kernel(StoreView s, RunArgs a, int S) {
     typename std::conditional<sizeof(T) == 2, Bf16Warp<D>, F32Warp<D>>::type st;
     for (int li = 0; li < a.nl; ++li) {
         const int l = a.l0 + li;
+        const bool tr = trace != nullptr && tid == 0 && li < 32;
+        if (tr) trace[li * 4] = p_gtimer();
         if (li + 1 < a.nl) {  // plan the next layer while this one's pages are in flight
             nxt = persist_plan(s, a, l + 1, bh, kw, nwt, lane);
             nxt_ready = true;
@@ -145,6 +160,7 @@ attn_persist_kernel(StoreView s, RunArgs a, int S) {
                     tok_slot, lane);
         }
         const int last_fill = hd.n_tok - (hd.n_pages - 1) * kPageSize;
+        if (tr) trace[li * 4 + 1] = p_gtimer();
         for (int i = 0; i < cur.n_e; ++i) {
             const int blk = __shfl_sync(0xffffffffu, cur.blk, i);
             const int stg = cons % NST;
@@ -163,6 +179,8 @@ attn_persist_kernel(StoreView s, RunArgs a, int S) {
         }
         // ---- merge the warps (scratch, not the ring: it holds the next layer)
         st.finalize();
+        __syncwarp();
+        if (tr) trace[li * 4 + 2] = p_gtimer();
         for (int g = lane; g < 16; g += 32) { s_wm[w][g] = -INFINITY; s_wl[w][g] = 0.f; }
         __syncwarp();
         st.store_partial(scratch + (size_t)w * G * D, s_wm[w], s_wl[w], G, lane);
@@ -192,31 +210,61 @@ attn_persist_kernel(StoreView s, RunArgs a, int S) {
                 if (e % D == 0) { cm[g] = M; cl[g] = L; }
             }
         }
+        const bool last_layer = li + 1 == a.nl;
         if (S > 1) {
+            // cluster merge into rank 0.  Intermediate layers: every rank
+            // arrives (release) once its state is written; only rank 0 waits
+            // (acquire) and pulls the states; the others go straight on — their
+            // state stays intact until rank 0 has published (the grid barrier
+            // orders their next write after it).  The last layer syncs twice
+            // so no rank exits while rank 0 still reads its shared memory.
             cg::cluster_group cluster = cg::this_cluster();
-            cluster.sync();
+            if (cl_wait_pending) {
+                asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+                cl_wait_pending = false;
+            }
+            asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+            if (rank == 0 || last_layer) {
+                asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+            } else {
+                cl_wait_pending = true;
+            }
             if (rank == 0 && n_att > 0) {
+                // every rank's row maxima / sums into local shared memory once
+                // (one remote load per (rank, row)), then per element only the
+                // ranks' accumulator values are read remotely
+                float *s_rm = scratch;                 // [S][16] (the scratch is free again)
+                float *s_rl = scratch + 16 * 16;      // [S][16]
+                for (int i = tid; i < S * 16; i += NW * 32) {
+                    const int r = i >> 4, g = i & 15;
+                    s_rm[i] = g < G ? cluster.map_shared_rank(cm, r)[g] : -INFINITY;
+                    s_rl[i] = g < G ? cluster.map_shared_rank(cl, r)[g] : 0.f;
+                }
+                __syncthreads();
                 for (int e = tid; e < G * D; e += NW * 32) {
                     const int g = e / D;
                     float M = -INFINITY;
-                    for (int r = 0; r < S; ++r) M = fmaxf(M, cluster.map_shared_rank(cm, r)[g]);
+                    for (int r = 0; r < S; ++r) M = fmaxf(M, s_rm[r * 16 + g]);
                     float L = 0.f, O = 0.f;
+#pragma unroll 8
                     for (int r = 0; r < S; ++r) {
-                        const float mr = cluster.map_shared_rank(cm, r)[g];
+                        const float mr = s_rm[r * 16 + g];
                         const float f = mr == -INFINITY ? 0.f : exp2f(mr - M);
-                        L += cluster.map_shared_rank(cl, r)[g] * f;
+                        L += s_rl[r * 16 + g] * f;
                         O += cluster.map_shared_rank(cstate, r)[e] * f;
                     }
                     out[e] = T(O / L);
                     if (lse && e % D == 0) lse[g] = (M + log2f(L)) * 0.69314718055994531f;
                 }
             }
-            cluster.sync();  // rank 0 done reading every rank's state
+            if (last_layer) cluster.sync();  // rank 0 done reading every rank's state
         }
         if (li + 1 < a.nl) {  // publish: this CTA's outputs of layer l are written
-            __threadfence();
+            // every output store of the CTA precedes thread 0's release (bar.sync
+            // orders them; red.release is cumulative over what it observed)
             __syncthreads();
             if (tid == 0) p_red_release_add(bar, 1u);
+            if (tr) trace[li * 4 + 3] = p_gtimer();
             cur = nxt;
             nxt_ready = false;
             if (il == 1) il = 0; else { il = 0; ie = 0; }
@@ -317,6 +365,8 @@ static cudaError_t launch_persist_t(const StoreView &s, const RunArgs &a, int S,
     cfg.numAttrs = S > 1 ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, attn_persist_kernel<T, D, NST, NW>, s, a, S);
 }
+
+cudaError_t set_persist_trace(void *p) { return cudaMemcpyToSymbol(g_persist_trace, &p, sizeof(p)); }
 
 cudaError_t launch_attn_persist(const StoreView &s, int dtype, const RunArgs &a, int S, cudaStream_t st) {
 #define FC_PL(T, DD, N, W) launch_persist_t<T, DD, N, W>(s, a, S, st)

@@ -67,6 +67,7 @@ const char *fc_last_error(void) { return g_last_error; }
  * attention kernel into a device buffer [grid][4] u64, or null to disable */
 int fc_debug_attn_trace(void *device_buf) { return cuda_status(set_attn_trace(device_buf)); }
 int fc_debug_run_trace(void *device_buf) { return cuda_status(set_run_trace(device_buf)); }
+int fc_debug_persist_trace(void *device_buf) { return cuda_status(set_persist_trace(device_buf)); }
 int fc_debug_score_trace(void *device_buf) { return cuda_status(set_score_trace(device_buf)); }
 /* test hook: scoring kernel choice, -1 auto, 0 balanced, 1 head-aligned */
 int fc_debug_score_mode(int mode) { set_score_mode(mode); return FC_OK; }

@@ -67,6 +67,7 @@ cudaError_t launch_attn(const StoreView &, int, const AttnArgs &, int, cudaStrea
 size_t attn_workspace_bytes(const StoreView &, int, int);
 cudaError_t set_attn_trace(void *);
 cudaError_t set_run_trace(void *);
+cudaError_t set_persist_trace(void *);
 cudaError_t set_score_trace(void *);
 void set_score_mode(int);
 void set_attn_mode(int);
