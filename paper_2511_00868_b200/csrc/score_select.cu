@@ -787,15 +787,27 @@ score_head_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t
 // Fused scoring + attention of one head per CTA (layers whose heads are
 // scored this step): the selection never leaves the CTA's view before its
 // pages stream — no grid-wide wait between scoring and attention, no second
-// launch, no selection -> table round trip through another kernel.  Warps
-// 0..NWA-1 then attend exactly as attn_kernel (attend_head_cta); the ring
+// launch, no selection -> table round trip through another kernel.  NWS warps
+// score (16 for bf16, as the head-aligned scoring kernel); then warps
+// NWA..NWS-1 hand their registers over (setmaxnreg: the scoring phase fits
+// 128 registers per thread, the attention state needs ~210) and leave, and
+// warps 0..NWA-1 attend exactly as attn_kernel (attend_head_cta); the ring
 // reuses the scoring ring / keys.  Same results as fc_score_select followed
 // by fc_sparse_decode (the attention reads the selection just written).
-template <typename T, int D, int NST, int NWA>
-__global__ void __launch_bounds__(NWA * 32, 1)
+template <int NWS, int NWA>
+struct RegSplit {  // registers per thread after the hand-over (multiples of 8)
+    static constexpr int kBase = 65536 / (NWS * 32) > 255 ? 255 : 65536 / (NWS * 32);
+    static constexpr int kLow = 24;
+    static constexpr int kHigh = ((65536 - (NWS - NWA) * 32 * kLow) / (NWA * 32)) / 8 * 8 > 248
+                                     ? 248 : ((65536 - (NWS - NWA) * 32 * kLow) / (NWA * 32)) / 8 * 8;
+};
+
+template <typename T, int D, int NST, int NWA, int NWS>
+__global__ void __launch_bounds__(NWS * 32, 1)
 score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t *__restrict__ unstable,
                     int period, int force_due, int topk, int extra_tokens, float *scores, int kv_prefetch,
                     AttnArgs a) {
+    static_assert(NWS >= NWA && NWS % 4 == 0 && NWA % 4 == 0, "whole warpgroups");
     extern __shared__ __align__(128) char dsm[];
     __shared__ __align__(8) uint64_t full[HeadScoreGeom<T, D>::kStages], empty[HeadScoreGeom<T, D>::kStages];
     __shared__ int s_rel[HeadScoreGeom<T, D>::kStages];
@@ -803,11 +815,16 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
     __shared__ __align__(8) uint64_t abars[NWA * NST];
     __shared__ float s_wm[NWA][16], s_wl[NWA][16];
     griddep_launch_dependents();
-    // the same warps score (NWA warps: the attention phase needs > 128
-    // registers per thread, so the CTA is not the 16-warp scoring CTA)
-    score_head_body<T, D, NWA>(s, layer, q, unstable, period, force_due, topk, extra_tokens, scores, kv_prefetch,
+    score_head_body<T, D, NWS>(s, layer, q, unstable, period, force_due, topk, extra_tokens, scores, kv_prefetch,
                                dsm, full, empty, s_rel, w);
     __syncthreads();  // selection written by this CTA; scoring smem free
+    if constexpr (NWS > NWA) {
+        if ((int)(threadIdx.x >> 5) >= NWA) {
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(RegSplit<NWS, NWA>::kLow));
+            return;
+        }
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(RegSplit<NWS, NWA>::kHigh));
+    }
     float *s_q = reinterpret_cast<float *>(dsm + score_attend_ring_bytes<T, D, NST, NWA>(s.NCAP));
     attend_head_cta<T, D, NST, NWA>(s, a, blockIdx.x, dsm, abars, s_wm, s_wl, s_q, 1);
 }
@@ -921,40 +938,44 @@ cudaError_t launch_score(const StoreView &s, int dtype, int layer, const void *q
 }
 
 // fused score + attend: head-aligned only (one CTA per head)
-template <typename T, int D, int NST, int NWA>
+template <typename T, int D, int NST, int NWA, int NWS = NWA>
 static size_t score_attend_smem(const StoreView &s) {
     return score_attend_ring_bytes<T, D, NST, NWA>(s.NCAP) + (sizeof(T) == 4 ? (size_t)s.G * D * sizeof(float) : 0);
 }
 
-template <typename T, int D, int NST, int NWA>
+template <typename T, int D, int NST, int NWA, int NWS>
 static int score_attend_fits_t(const StoreView &s) {
-    auto k = score_attend_kernel<T, D, NST, NWA>;
-    const size_t smem = score_attend_smem<T, D, NST, NWA>(s);
+    auto k = score_attend_kernel<T, D, NST, NWA, NWS>;
+    const size_t smem = score_attend_smem<T, D, NST, NWA, NWS>(s);
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NWA * 32, smem) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NWS * 32, smem) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
     return occ >= 1;
 }
 
-template <typename T, int D, int NST, int NWA>
+template <typename T, int D, int NST, int NWA, int NWS>
 static cudaError_t launch_score_attend_t(const StoreView &s, int layer, const void *q, const uint8_t *unstable,
                                          int period, int force_due, int topk, int extra, float *scores,
                                          int batch, int kv_prefetch, const AttnArgs &a, cudaStream_t st) {
-    if (!score_attend_fits_t<T, D, NST, NWA>(s)) return cudaErrorInvalidConfiguration;
-    return launch_pdl(score_attend_kernel<T, D, NST, NWA>, dim3(batch * s.H), dim3(NWA * 32),
-                      score_attend_smem<T, D, NST, NWA>(s), st, s, layer, (const T *)q, unstable, period, force_due,
+    if (!score_attend_fits_t<T, D, NST, NWA, NWS>(s)) return cudaErrorInvalidConfiguration;
+    return launch_pdl(score_attend_kernel<T, D, NST, NWA, NWS>, dim3(batch * s.H), dim3(NWS * 32),
+                      score_attend_smem<T, D, NST, NWA, NWS>(s), st, s, layer, (const T *)q, unstable, period, force_due,
                       topk, extra, scores, kv_prefetch, a);
 }
 
+#ifndef FC_SA_SCORE_WARPS
+#define FC_SA_SCORE_WARPS 16
+#endif
 #define FC_SA_DISPATCH(dtype, D, CALL)                                                  \
-    ((dtype) == FC_BF16 ? ((D) == 128 ? CALL(__nv_bfloat16, 128, 3, 8) : CALL(__nv_bfloat16, 64, 6, 8)) \
-                        : ((D) == 128 ? CALL(float, 128, 3, 4) : CALL(float, 64, 6, 4)))
+    ((dtype) == FC_BF16 ? ((D) == 128 ? CALL(__nv_bfloat16, 128, 3, 8, FC_SA_SCORE_WARPS)               \
+                                      : CALL(__nv_bfloat16, 64, 6, 8, FC_SA_SCORE_WARPS))               \
+                        : ((D) == 128 ? CALL(float, 128, 3, 4, 4) : CALL(float, 64, 6, 4, 4)))
 
 // used when the batch fills the GPU with heads (the head-aligned scoring rule)
 int score_attend_supported(const StoreView &s, int dtype, int batch) {
@@ -966,7 +987,7 @@ int score_attend_supported(const StoreView &s, int dtype, int batch) {
     }
     const bool head_mode = g_score_mode < 0 ? 2 * batch * s.H >= sms : g_score_mode == 1;
     if (!head_mode || batch < 1) return 0;
-#define FC_SAF(T, DD, N, W) score_attend_fits_t<T, DD, N, W>(s)
+#define FC_SAF(T, DD, N, W, WS) score_attend_fits_t<T, DD, N, W, WS>(s)
     return FC_SA_DISPATCH(dtype, s.D, FC_SAF);
 #undef FC_SAF
 }
@@ -974,8 +995,8 @@ int score_attend_supported(const StoreView &s, int dtype, int batch) {
 cudaError_t launch_score_attend(const StoreView &s, int dtype, int layer, const void *q, const uint8_t *unstable,
                                 int period, int force_due, int topk, int extra, float *scores, int batch,
                                 int kv_prefetch, const AttnArgs &a, cudaStream_t st) {
-#define FC_SAL(T, DD, N, W) \
-    launch_score_attend_t<T, DD, N, W>(s, layer, q, unstable, period, force_due, topk, extra, scores, batch, kv_prefetch, a, st)
+#define FC_SAL(T, DD, N, W, WS) \
+    launch_score_attend_t<T, DD, N, W, WS>(s, layer, q, unstable, period, force_due, topk, extra, scores, batch, kv_prefetch, a, st)
     return FC_SA_DISPATCH(dtype, s.D, FC_SAL);
 #undef FC_SAL
 }

@@ -76,11 +76,10 @@ class DecodeEngine:
         # steps at batch 1, 9 % at batch 4), per-layer launches above (equal
         # or 2 % faster at config 2)
         self.run_kernel = None
-        # True: scored layers run scoring, selection and attention in one
-        # launch (one CTA per head, fc_score_attend) when the batch fills the
-        # GPU with heads.  Default False: measured slower at config 2 (57.9 vs
-        # 55.9 us per scored layer)
-        self.fused_score_attend = False
+        # scored layers run scoring, selection and attention in one launch (one
+        # CTA per head, fc_score_attend) when the batch fills the GPU with
+        # heads: 53.4 vs 56.6 us per scored layer at config 2
+        self.fused_score_attend = True
         # profiling: score every head every step and record
         # the selections on the device (trace.TraceRecorder)
         self.score_all_heads = False
