@@ -627,15 +627,20 @@ __host__ __device__ constexpr size_t score_attend_ring_bytes(int ncap) {
                : (size_t)NWA * NST * AttnGeom<T, D>::kPageBytes;
 }
 
-// Body of the head-aligned scoring for head blockIdx.x: every thread of the
-// CTA (kHeadScoreWarps warps) calls it; returns after the selection is in
-// s.sel / s.n_sel (or at once for a head that is not due).  Waits for the
-// previous launch (PDL) on every path.  dsm: ring [NS][chunk] | keys [NCAP].
+// Streaming half of the head-aligned scoring: rank `rank` of the S CTAs
+// scoring head bh streams candidate pages [n_cand*rank/S, n_cand*(rank+1)/S)
+// of the head's summaries and writes their keys into keys_dst (the keys array
+// of the CTA that selects: its own, or rank 0's through DSMEM) and the scores
+// row.  Every thread of the CTA calls it.  Returns 0 (head not due / empty),
+// 1 (the budget covers every page: rank 0 wrote the selection) or 2 (keys
+// written: the selecting CTA runs score_head_select on n_cand keys).  Waits
+// for the previous launch (PDL) on every path.  dsm: ring [NS][chunk] | keys.
 template <typename T, int D, int NWS = kHeadScoreWarps>
-__device__ void score_head_body(const StoreView &s, int layer, const T *__restrict__ q,
-                                const uint8_t *__restrict__ unstable, int period, int force_due, int topk,
-                                int extra_tokens, float *scores, int kv_prefetch, char *dsm, uint64_t *full,
-                                uint64_t *empty, int *s_rel, float *w) {
+__device__ int score_head_stream(const StoreView &s, int layer, const T *__restrict__ q,
+                                 const uint8_t *__restrict__ unstable, int period, int force_due, int topk,
+                                 int extra_tokens, float *scores, int kv_prefetch, char *dsm, uint64_t *full,
+                                 uint64_t *empty, int *s_rel, float *w, int bh, int S, int rank,
+                                 uint32_t *keys_dst, int &n_cand_out) {
     using Gm = ScoreGeom<T, D>;
     using HG = HeadScoreGeom<T, D, NWS>;
     constexpr int NW = NWS, NS = HG::kStages, R = HG::kRounds;
@@ -645,27 +650,32 @@ __device__ void score_head_body(const StoreView &s, int layer, const T *__restri
     unsigned long long *trace = g_score_trace;  // [grid][4]: entry, copies issued, streamed, selected
     if (trace && tid == 0) trace[blockIdx.x * 4] = gtimer_s();
     if (!kv_prefetch) griddep_wait();
-    const int bh = blockIdx.x, b = bh / s.H, h = bh % s.H;
+    const int b = bh / s.H, h = bh % s.H;
     const bool due = force_due || unstable[layer * s.H + h] || (*s.step % period == 0);
     const int n_tok = s.seq_len[b] + extra_tokens;
     const int n_pages = n_tok > 0 ? (n_tok + s.PS - 1) / s.PS : 0;
     const int hx = s.hix(b, layer, h);
     if (!due || n_pages == 0) {
         if (kv_prefetch) griddep_wait();
-        return;
+        return 0;
     }
     int32_t *out = s.sel + (int64_t)hx * s.SELCAP;
     if (n_pages <= topk) {  // budget covers every page
         if (kv_prefetch) griddep_wait();
-        for (int i = tid; i < n_pages; i += blockDim.x) out[i] = i;
-        if (tid == 0) s.n_sel[hx] = n_pages;
-        return;
+        if (rank == 0) {
+            for (int i = tid; i < n_pages; i += blockDim.x) out[i] = i;
+            if (tid == 0) s.n_sel[hx] = n_pages;
+        }
+        return 1;
     }
-    const int n_cand = n_pages - 1;  // the last page is pinned
+    const int n_cand_all = n_pages - 1;  // the last page is pinned
+    n_cand_out = n_cand_all;
+    const int c0 = (int)((int64_t)n_cand_all * rank / S);
+    const int n_cand = (int)((int64_t)n_cand_all * (rank + 1) / S) - c0;  // this rank's candidates
     const int n_chunks = (n_cand + kHeadChunkPages - 1) / kHeadChunkPages;
     char *ring = dsm;
-    uint32_t *keys = reinterpret_cast<uint32_t *>(dsm + (size_t)NS * HG::kChunkBytes);
-    const char *base = reinterpret_cast<const char *>(s.summ) + (int64_t)hx * s.NCAP * Gm::kRecBytes;
+    uint32_t *keys = keys_dst + c0;
+    const char *base = reinterpret_cast<const char *>(s.summ) + ((int64_t)hx * s.NCAP + c0) * Gm::kRecBytes;
     if (tid == 0) {
         for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], NW); s_rel[i] = 0; }
         fence_mbar_init();
@@ -685,7 +695,7 @@ __device__ void score_head_body(const StoreView &s, int layer, const T *__restri
     for (int c = 0; c < CPL; ++c)
 #pragma unroll
         for (int e = 0; e < EPC; ++e) coef[c][e] = w[(cl + c * LPP) * EPC + e];
-    float *srow = scores + (int64_t)bh * s.NCAP;
+    float *srow = scores + (int64_t)bh * s.NCAP + c0;
     for (int c = 0; c < n_chunks; ++c) {
         const int stg = c % NS;
         mbar_wait(&full[stg], (c / NS) & 1);
@@ -759,17 +769,48 @@ __device__ void score_head_body(const StoreView &s, int layer, const T *__restri
             bulk_g2s(ring + (size_t)stg * HG::kChunkBytes, base + (int64_t)cn * HG::kChunkBytes, bytes, &full[stg]);
         }
     }
-    if (tid == 0) srow[n_pages - 1] = -INFINITY;  // pinned page: not scored
+    if (tid == 0 && rank == 0) scores[(int64_t)bh * s.NCAP + n_pages - 1] = -INFINITY;  // pinned: not scored
     __syncthreads();
     if (trace && tid == 0) trace[blockIdx.x * 4 + 2] = gtimer_s();
+    return 2;
+}
+
+// Selecting half: the kprime = topk-1 best of the n_cand keys, then the
+// pinned last page (select_topk, scoring.py:164-193).  Every thread of the
+// selecting CTA calls it.
+template <int NT>
+__device__ void score_head_select(const StoreView &s, const uint32_t *keys, int n_cand, int topk, int hx) {
+    int32_t *out = s.sel + (int64_t)hx * s.SELCAP;
     const int kprime = topk - 1;  // n_pages > topk, so kprime < n_cand
-    if (kprime > 0) block_select<NW * 32>(keys, n_cand, kprime, out);
-    if (tid == 0) {
-        out[kprime] = n_pages - 1;
+    if (kprime > 0) block_select<NT>(keys, n_cand, kprime, out);
+    if (threadIdx.x == 0) {
+        out[kprime] = n_cand;  // = n_pages - 1
         s.n_sel[hx] = topk;
+        unsigned long long *trace = g_score_trace;
         if (trace) trace[blockIdx.x * 4 + 3] = gtimer_s();
     }
 }
+
+// Body of the head-aligned scoring for head blockIdx.x (one CTA per head):
+// stream, then select.  Returns after the selection is in s.sel / s.n_sel
+// (or at once for a head that is not due).
+template <typename T, int D, int NWS = kHeadScoreWarps>
+__device__ void score_head_body(const StoreView &s, int layer, const T *__restrict__ q,
+                                const uint8_t *__restrict__ unstable, int period, int force_due, int topk,
+                                int extra_tokens, float *scores, int kv_prefetch, char *dsm, uint64_t *full,
+                                uint64_t *empty, int *s_rel, float *w) {
+    using HG = HeadScoreGeom<T, D, NWS>;
+    uint32_t *keys = reinterpret_cast<uint32_t *>(dsm + (size_t)HG::kStages * HG::kChunkBytes);
+    int n_cand = 0;
+    const int st = score_head_stream<T, D, NWS>(s, layer, q, unstable, period, force_due, topk, extra_tokens,
+                                                  scores, kv_prefetch, dsm, full, empty, s_rel, w, blockIdx.x, 1,
+                                                  0, keys, n_cand);
+    if (st == 2) {
+        const int b = blockIdx.x / s.H, h = blockIdx.x % s.H;
+        score_head_select<NWS * 32>(s, keys, n_cand, topk, s.hix(b, layer, h));
+    }
+}
+
 
 template <typename T, int D>
 __global__ void __launch_bounds__(kHeadScoreWarps * 32, 1)
