@@ -9,6 +9,7 @@
 #pragma once
 #include "launchers.cuh"
 #include <type_traits>
+#include <cooperative_groups.h>
 
 namespace fc {
 
@@ -410,16 +411,19 @@ FC_DEVINL void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" :
 // s_q: fp32 q [G][D] (fp32 only).  Every read this needs must already be
 // visible (the caller waited for the previous launch / wrote sel itself).
 template <typename T, int D, int NST, int NW>
-FC_DEVINL void attend_head_cta(const StoreView &s, const AttnArgs &a, int bh, char *ring, uint64_t *bars,
-                               float (*s_wm)[16], float (*s_wl)[16], float *s_q, int bar_id) {
+FC_DEVINL int attend_head_cta(const StoreView &s, const AttnArgs &a, int bh, char *ring, uint64_t *bars,
+                              float (*s_wm)[16], float (*s_wl)[16], float *s_q, int bar_id, int S = 1,
+                              int rank = 0, float *cstate = nullptr) {
     using Gm = AttnGeom<T, D>;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     constexpr int NT = NW * 32;
     const int G = s.G;
     const HeadInfo hd = head_info(s, a, bh);
     const int n_att = hd.n_att;
-    const int j0 = (int)((int64_t)n_att * w / NW);
-    const int n_e = (int)((int64_t)n_att * (w + 1) / NW) - j0;
+    // S > 1: the head's pages are cut over the S CTAs of a cluster (rank-major)
+    const int kw = rank * NW + w, nwt = S * NW;
+    const int j0 = (int)((int64_t)n_att * kw / nwt);
+    const int n_e = (int)((int64_t)n_att * (kw + 1) / nwt) - j0;
     const int b = bh / s.H, h = bh % s.H;
     const int64_t qoff = ((int64_t)b * s.H * G + (int64_t)h * G) * D;
     const int last_fill = hd.n_tok - (hd.n_pages - 1) * kPageSize;
@@ -519,13 +523,49 @@ FC_DEVINL void attend_head_cta(const StoreView &s, const AttnArgs &a, int bh, ch
             float L = 0.f, O = 0.f;
 #pragma unroll
             for (int ww = 0; ww < NW; ++ww) {
-                const float f = exp2f(s_wm[ww][g] - M);
+                // a CTA whose warps hold no page (S > 1) has M = -inf
+                const float f = M == -INFINITY ? 0.f : exp2f(s_wm[ww][g] - M);
                 L += s_wl[ww][g] * f;
                 O += scratch[(size_t)ww * G * D + e] * f;
             }
-            out[e] = T(O / L);
-            if (lse && e % D == 0) lse[g] = (M + log2f(L)) * 0.69314718055994531f;
+            if (S == 1) {
+                out[e] = T(O / L);
+                if (lse && e % D == 0) lse[g] = (M + log2f(L)) * 0.69314718055994531f;
+            } else {  // this CTA's state for the cluster merge: acc [G][D] | m [16] | l [16]
+                cstate[e] = O;
+                if (e % D == 0) { cstate[G * D + g] = M; cstate[G * D + 16 + g] = L; }
+            }
         }
+    }
+    return n_att;
+}
+
+// Cluster merge of a head attended by S CTAs (attend_head_cta with S > 1):
+// rank 0's first nt threads combine every rank's state through DSMEM and
+// write the output.  Caller: a cluster barrier before and after.
+template <typename T, int D>
+FC_DEVINL void merge_head_cluster(const StoreView &s, const AttnArgs &a, int bh, float *cstate, int S, int nt) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int G = s.G;
+    const int b = bh / s.H, h = bh % s.H;
+    T *out = reinterpret_cast<T *>(a.out) + ((int64_t)b * s.H * G + (int64_t)h * G) * D;
+    float *lse = a.lse ? a.lse + (int64_t)bh * G : nullptr;
+    for (int e = threadIdx.x; e < G * D; e += nt) {
+        const int g = e / D;
+        float M = -INFINITY;
+        for (int r = 0; r < S; ++r) M = fmaxf(M, cluster.map_shared_rank(cstate, r)[G * D + g]);
+        float L = 0.f, O = 0.f;
+#pragma unroll 4
+        for (int r = 0; r < S; ++r) {
+            const float *cr = cluster.map_shared_rank(cstate, r);
+            const float mr = cr[G * D + g];
+            const float f = mr == -INFINITY ? 0.f : exp2f(mr - M);
+            L += cr[G * D + 16 + g] * f;
+            O += cr[e] * f;
+        }
+        out[e] = T(O / L);
+        if (lse && e % D == 0) lse[g] = (M + log2f(L)) * 0.69314718055994531f;
     }
 }
 

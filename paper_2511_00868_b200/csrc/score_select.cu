@@ -847,27 +847,52 @@ template <typename T, int D, int NST, int NWA, int NWS>
 __global__ void __launch_bounds__(NWS * 32, 1)
 score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t *__restrict__ unstable,
                     int period, int force_due, int topk, int extra_tokens, float *scores, int kv_prefetch,
-                    AttnArgs a) {
+                    AttnArgs a, int S) {
     static_assert(NWS >= NWA && NWS % 4 == 0 && NWA % 4 == 0, "whole warpgroups");
+    namespace cg = cooperative_groups;
+    using HG = HeadScoreGeom<T, D, NWS>;
     extern __shared__ __align__(128) char dsm[];
-    __shared__ __align__(8) uint64_t full[HeadScoreGeom<T, D>::kStages], empty[HeadScoreGeom<T, D>::kStages];
-    __shared__ int s_rel[HeadScoreGeom<T, D>::kStages];
+    __shared__ __align__(8) uint64_t full[HG::kStages], empty[HG::kStages];
+    __shared__ int s_rel[HG::kStages];
     __shared__ float w[2 * D];
     __shared__ __align__(8) uint64_t abars[NWA * NST];
     __shared__ float s_wm[NWA][16], s_wl[NWA][16];
     griddep_launch_dependents();
-    score_head_body<T, D, NWS>(s, layer, q, unstable, period, force_due, topk, extra_tokens, scores, kv_prefetch,
-                               dsm, full, empty, s_rel, w);
-    __syncthreads();  // selection written by this CTA; scoring smem free
+    // S CTAs (a cluster) per head: every rank scores its share of the pages
+    // into rank 0's keys (DSMEM), rank 0 selects, every rank attends its
+    // share of the selection, rank 0 merges the ranks' states (DSMEM)
+    const int bh = blockIdx.x / S, rank = blockIdx.x % S;
+    const int b = bh / s.H, h = bh % s.H, hx = s.hix(b, layer, h);
+    uint32_t *keys = reinterpret_cast<uint32_t *>(dsm + (size_t)HG::kStages * HG::kChunkBytes);
+    uint32_t *keys_dst = keys;
+    if (S > 1) keys_dst = cg::this_cluster().map_shared_rank(keys, 0);
+    int n_cand = 0;
+    const int st = score_head_stream<T, D, NWS>(s, layer, q, unstable, period, force_due, topk, extra_tokens,
+                                                  scores, kv_prefetch, dsm, full, empty, s_rel, w, bh, S, rank,
+                                                  keys_dst, n_cand);
+    if (S > 1) cg::this_cluster().sync();  // every rank's keys are in rank 0
+    if (st == 2 && rank == 0) score_head_select<NWS * 32>(s, keys, n_cand, topk, hx);
+    if (S > 1) cg::this_cluster().sync();  // the selection (global) is visible to every rank
+    else __syncthreads();                  // selection written by this CTA; scoring smem free
+    const bool attends = (int)(threadIdx.x >> 5) < NWA;
     if constexpr (NWS > NWA) {
-        if ((int)(threadIdx.x >> 5) >= NWA) {
+        if (!attends) {
             asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(RegSplit<NWS, NWA>::kLow));
-            return;
+            if (S == 1) return;  // (with S > 1 they stay for the cluster barriers)
+        } else {
+            asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(RegSplit<NWS, NWA>::kHigh));
         }
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(RegSplit<NWS, NWA>::kHigh));
     }
     float *s_q = reinterpret_cast<float *>(dsm + score_attend_ring_bytes<T, D, NST, NWA>(s.NCAP));
-    attend_head_cta<T, D, NST, NWA>(s, a, blockIdx.x, dsm, abars, s_wm, s_wl, s_q, 1);
+    // the CTA's state for the cluster merge lives past the attention scratch
+    float *cstate = reinterpret_cast<float *>(dsm) + (size_t)NWA * s.G * D;
+    int n_att = 0;
+    if (attends) n_att = attend_head_cta<T, D, NST, NWA>(s, a, bh, dsm, abars, s_wm, s_wl, s_q, 1, S, rank, cstate);
+    if (S > 1) {
+        cg::this_cluster().sync();  // every rank's state written
+        if (rank == 0 && attends && n_att > 0) merge_head_cluster<T, D>(s, a, bh, cstate, S, NWA * 32);
+        cg::this_cluster().sync();  // rank 0 done reading every rank's shared memory
+    }
 }
 
 // standalone select over caller scores: grid n_heads, block kScoreThreads
@@ -1000,14 +1025,71 @@ static int score_attend_fits_t(const StoreView &s) {
     return occ >= 1;
 }
 
+// CTAs per head: 1 when the batch fills the GPU with heads (the head-aligned
+// rule); otherwise the largest power of two <= 16 that keeps one wave with
+// every cluster co-resident.  0: does not fit.
+template <typename T, int D, int NST, int NWA, int NWS>
+static int score_attend_split_t(const StoreView &s, int batch) {
+    if (!score_attend_fits_t<T, D, NST, NWA, NWS>(s)) return 0;
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int heads = batch * s.H;
+    if (g_score_mode == 1 || (g_score_mode < 0 && 2 * heads >= sms)) return 1;
+    if (g_score_mode == 0) return 0;
+    auto k = score_attend_kernel<T, D, NST, NWA, NWS>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int best = 0;
+    for (int S = 2; S <= 16 && heads * S <= sms; S *= 2) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(heads * S);
+        cfg.blockDim = dim3(NWS * 32);
+        cfg.dynamicSmemBytes = score_attend_smem<T, D, NST, NWA, NWS>(s);
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = S;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&clusters, k, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        if (clusters >= heads) best = S;
+    }
+    return best;
+}
+
 template <typename T, int D, int NST, int NWA, int NWS>
 static cudaError_t launch_score_attend_t(const StoreView &s, int layer, const void *q, const uint8_t *unstable,
                                          int period, int force_due, int topk, int extra, float *scores,
                                          int batch, int kv_prefetch, const AttnArgs &a, cudaStream_t st) {
-    if (!score_attend_fits_t<T, D, NST, NWA, NWS>(s)) return cudaErrorInvalidConfiguration;
-    return launch_pdl(score_attend_kernel<T, D, NST, NWA, NWS>, dim3(batch * s.H), dim3(NWS * 32),
-                      score_attend_smem<T, D, NST, NWA, NWS>(s), st, s, layer, (const T *)q, unstable, period, force_due,
-                      topk, extra, scores, kv_prefetch, a);
+    const int S = score_attend_split_t<T, D, NST, NWA, NWS>(s, batch);
+    if (S < 1) return cudaErrorInvalidConfiguration;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(batch * s.H * S);
+    cfg.blockDim = dim3(NWS * 32);
+    cfg.dynamicSmemBytes = score_attend_smem<T, D, NST, NWA, NWS>(s);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = S;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = S > 1 ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, score_attend_kernel<T, D, NST, NWA, NWS>, s, layer, (const T *)q, unstable,
+                              period, force_due, topk, extra, scores, kv_prefetch, a, S);
 }
 
 #ifndef FC_SA_SCORE_WARPS
@@ -1018,17 +1100,10 @@ static cudaError_t launch_score_attend_t(const StoreView &s, int layer, const vo
                                       : CALL(__nv_bfloat16, 64, 6, 8, FC_SA_SCORE_WARPS))               \
                         : ((D) == 128 ? CALL(float, 128, 3, 4, 4) : CALL(float, 64, 6, 4, 4)))
 
-// used when the batch fills the GPU with heads (the head-aligned scoring rule)
+// CTAs per head of the fused kernel for this batch (0: not supported)
 int score_attend_supported(const StoreView &s, int dtype, int batch) {
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const bool head_mode = g_score_mode < 0 ? 2 * batch * s.H >= sms : g_score_mode == 1;
-    if (!head_mode || batch < 1) return 0;
-#define FC_SAF(T, DD, N, W, WS) score_attend_fits_t<T, DD, N, W, WS>(s)
+    if (batch < 1) return 0;
+#define FC_SAF(T, DD, N, W, WS) score_attend_split_t<T, DD, N, W, WS>(s, batch)
     return FC_SA_DISPATCH(dtype, s.D, FC_SAF);
 #undef FC_SAF
 }

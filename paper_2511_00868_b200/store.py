@@ -167,8 +167,9 @@ class KVStore:
             extra_tokens, int(kv_prefetch), self.scores.data_ptr(), self.score_counters.data_ptr(),
             batch, self.stream()), "fc_score_select")
 
-    def score_attend_supported(self, batch: int) -> bool:
-        return bool(self.lib.fc_score_attend_supported(self.cptr, batch))
+    def score_attend_supported(self, batch: int) -> int:
+        """CTAs per head fc_score_attend uses for this batch (0: unsupported)."""
+        return int(self.lib.fc_score_attend_supported(self.cptr, batch))
 
     def score_attend(self, layer: int, q: torch.Tensor, unstable: torch.Tensor, period: int, topk: int,
                      out: torch.Tensor, batch: int, *, force_due: bool = False, extra_tokens: int = 1,

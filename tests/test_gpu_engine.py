@@ -197,6 +197,24 @@ def test_engine_fused_tiered(head_aligned_scoring):
                          dtype=torch.bfloat16, seed=19, use_graph=True, tiering=True, fused=True)
 
 
+@pytest.mark.parametrize("dtype,D,G", [(torch.bfloat16, 128, 4), (torch.float32, 128, 4),
+                                       (torch.bfloat16, 64, 7), (torch.float32, 64, 2)])
+def test_engine_fused_clusters_match_oracle(dtype, D, G):
+    """fc_score_attend at small batches: each head is scored, selected and
+    attended by a cluster of CTAs (keys gathered in rank 0 through DSMEM,
+    rank 0 selects, every rank attends its share, DSMEM merge)."""
+    worst, ties, eng = run_engine_vs_oracle(B=3, L=2, H=2, G=G, D=D, T0=1500, steps=10, K=8,
+                                            R=4, frac=0.5, dtype=dtype, seed=20, use_graph=True,
+                                            ragged=True, fused=True)
+    assert eng.store.score_attend_supported(eng.B) > 1  # a cluster per head
+    assert ties <= 2
+
+
+def test_engine_fused_clusters_tiered():
+    run_engine_vs_oracle(B=2, L=2, H=4, G=4, D=128, T0=700, steps=16, K=6, R=4, frac=0.5,
+                         dtype=torch.bfloat16, seed=21, use_graph=True, tiering=True, fused=True)
+
+
 def test_engine_head_aligned_tiered(head_aligned_scoring):
     run_engine_vs_oracle(B=2, L=2, H=4, G=4, D=128, T0=400, steps=16, K=6, R=4, frac=0.5,
                          dtype=torch.bfloat16, seed=12, use_graph=True, tiering=True)
