@@ -641,6 +641,12 @@ __device__ int score_head_stream(const StoreView &s, int layer, const T *__restr
                                  int extra_tokens, float *scores, int kv_prefetch, char *dsm, uint64_t *full,
                                  uint64_t *empty, int *s_rel, float *w, int bh, int S, int rank,
                                  uint32_t *keys_dst, int &n_cand_out) {
+    // S > 1: the caller arrived on the cluster barrier at entry; wait on it
+    // before the first write into another CTA's shared memory (a peer may not
+    // have started yet) — and on every other way out
+    auto cluster_wait = [&]() {
+        if (S > 1) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    };
     using Gm = ScoreGeom<T, D>;
     using HG = HeadScoreGeom<T, D, NWS>;
     constexpr int NW = NWS, NS = HG::kStages, R = HG::kRounds;
@@ -657,6 +663,7 @@ __device__ int score_head_stream(const StoreView &s, int layer, const T *__restr
     const int hx = s.hix(b, layer, h);
     if (!due || n_pages == 0) {
         if (kv_prefetch) griddep_wait();
+        cluster_wait();
         return 0;
     }
     int32_t *out = s.sel + (int64_t)hx * s.SELCAP;
@@ -666,6 +673,7 @@ __device__ int score_head_stream(const StoreView &s, int layer, const T *__restr
             for (int i = tid; i < n_pages; i += blockDim.x) out[i] = i;
             if (tid == 0) s.n_sel[hx] = n_pages;
         }
+        cluster_wait();
         return 1;
     }
     const int n_cand_all = n_pages - 1;  // the last page is pinned
@@ -696,6 +704,7 @@ __device__ int score_head_stream(const StoreView &s, int layer, const T *__restr
 #pragma unroll
         for (int e = 0; e < EPC; ++e) coef[c][e] = w[(cl + c * LPP) * EPC + e];
     float *srow = scores + (int64_t)bh * s.NCAP + c0;
+    cluster_wait();  // every CTA of the cluster has started: keys_dst is valid
     for (int c = 0; c < n_chunks; ++c) {
         const int stg = c % NS;
         mbar_wait(&full[stg], (c / NS) & 1);
@@ -838,7 +847,7 @@ score_head_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t
 template <int NWS, int NWA>
 struct RegSplit {  // registers per thread after the hand-over (multiples of 8)
     static constexpr int kBase = 65536 / (NWS * 32) > 255 ? 255 : 65536 / (NWS * 32);
-    static constexpr int kLow = 24;
+    static constexpr int kLow = 32;
     static constexpr int kHigh = ((65536 - (NWS - NWA) * 32 * kLow) / (NWA * 32)) / 8 * 8 > 248
                                      ? 248 : ((65536 - (NWS - NWA) * 32 * kLow) / (NWA * 32)) / 8 * 8;
 };
@@ -863,6 +872,7 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
     // share of the selection, rank 0 merges the ranks' states (DSMEM)
     const int bh = blockIdx.x / S, rank = blockIdx.x % S;
     const int b = bh / s.H, h = bh % s.H, hx = s.hix(b, layer, h);
+    if (S > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // waited in the stream
     uint32_t *keys = reinterpret_cast<uint32_t *>(dsm + (size_t)HG::kStages * HG::kChunkBytes);
     uint32_t *keys_dst = keys;
     if (S > 1) keys_dst = cg::this_cluster().map_shared_rank(keys, 0);
