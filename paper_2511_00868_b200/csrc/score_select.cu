@@ -847,16 +847,19 @@ score_head_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t
 template <int NWS, int NWA>
 struct RegSplit {  // registers per thread after the hand-over (multiples of 8)
     static constexpr int kBase = 65536 / (NWS * 32) > 255 ? 255 : 65536 / (NWS * 32);
-    static constexpr int kLow = 32;
+    static constexpr int kLow = 24;
     static constexpr int kHigh = ((65536 - (NWS - NWA) * 32 * kLow) / (NWA * 32)) / 8 * 8 > 248
                                      ? 248 : ((65536 - (NWS - NWA) * 32 * kLow) / (NWA * 32)) / 8 * 8;
 };
 
-template <typename T, int D, int NST, int NWA, int NWS>
+template <typename T, int D, int NST, int NWA, int NWS, bool CL>
 __global__ void __launch_bounds__(NWS * 32, 1)
 score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t *__restrict__ unstable,
                     int period, int force_due, int topk, int extra_tokens, float *scores, int kv_prefetch,
-                    AttnArgs a, int S) {
+                    AttnArgs a, int S_arg) {
+    // CL = false: one CTA per head (S = 1, no cluster code compiled in: the
+    // attention phase keeps its registers); CL = true: a cluster of S_arg
+    const int S = CL ? S_arg : 1;
     static_assert(NWS >= NWA && NWS % 4 == 0 && NWA % 4 == 0, "whole warpgroups");
     namespace cg = cooperative_groups;
     using HG = HeadScoreGeom<T, D, NWS>;
@@ -872,23 +875,23 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
     // share of the selection, rank 0 merges the ranks' states (DSMEM)
     const int bh = blockIdx.x / S, rank = blockIdx.x % S;
     const int b = bh / s.H, h = bh % s.H, hx = s.hix(b, layer, h);
-    if (S > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // waited in the stream
+    if constexpr (CL) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // waited in the stream
     uint32_t *keys = reinterpret_cast<uint32_t *>(dsm + (size_t)HG::kStages * HG::kChunkBytes);
     uint32_t *keys_dst = keys;
-    if (S > 1) keys_dst = cg::this_cluster().map_shared_rank(keys, 0);
+    if constexpr (CL) keys_dst = cg::this_cluster().map_shared_rank(keys, 0);
     int n_cand = 0;
     const int st = score_head_stream<T, D, NWS>(s, layer, q, unstable, period, force_due, topk, extra_tokens,
                                                   scores, kv_prefetch, dsm, full, empty, s_rel, w, bh, S, rank,
                                                   keys_dst, n_cand);
-    if (S > 1) cg::this_cluster().sync();  // every rank's keys are in rank 0
+    if constexpr (CL) cg::this_cluster().sync();  // every rank's keys are in rank 0
     if (st == 2 && rank == 0) score_head_select<NWS * 32>(s, keys, n_cand, topk, hx);
-    if (S > 1) cg::this_cluster().sync();  // the selection (global) is visible to every rank
-    else __syncthreads();                  // selection written by this CTA; scoring smem free
+    if constexpr (CL) cg::this_cluster().sync();  // the selection (global) is visible to every rank
+    else __syncthreads();                         // selection written by this CTA; scoring smem free
     const bool attends = (int)(threadIdx.x >> 5) < NWA;
     if constexpr (NWS > NWA) {
         if (!attends) {
             asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(RegSplit<NWS, NWA>::kLow));
-            if (S == 1) return;  // (with S > 1 they stay for the cluster barriers)
+            if constexpr (!CL) return;  // (in a cluster they stay for the cluster barriers)
         } else {
             asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(RegSplit<NWS, NWA>::kHigh));
         }
@@ -896,9 +899,11 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
     float *s_q = reinterpret_cast<float *>(dsm + score_attend_ring_bytes<T, D, NST, NWA>(s.NCAP));
     // the CTA's state for the cluster merge lives past the attention scratch
     float *cstate = reinterpret_cast<float *>(dsm) + (size_t)NWA * s.G * D;
-    int n_att = 0;
-    if (attends) n_att = attend_head_cta<T, D, NST, NWA>(s, a, bh, dsm, abars, s_wm, s_wl, s_q, 1, S, rank, cstate);
-    if (S > 1) {
+    if constexpr (!CL) {
+        attend_head_cta<T, D, NST, NWA>(s, a, bh, dsm, abars, s_wm, s_wl, s_q, 1);
+    } else {
+        int n_att = 0;
+        if (attends) n_att = attend_head_cta<T, D, NST, NWA>(s, a, bh, dsm, abars, s_wm, s_wl, s_q, 1, S, rank, cstate);
         cg::this_cluster().sync();  // every rank's state written
         if (rank == 0 && attends && n_att > 0) merge_head_cluster<T, D>(s, a, bh, cstate, S, NWA * 32);
         cg::this_cluster().sync();  // rank 0 done reading every rank's shared memory
@@ -1019,9 +1024,9 @@ static size_t score_attend_smem(const StoreView &s) {
     return score_attend_ring_bytes<T, D, NST, NWA>(s.NCAP) + (sizeof(T) == 4 ? (size_t)s.G * D * sizeof(float) : 0);
 }
 
-template <typename T, int D, int NST, int NWA, int NWS>
+template <typename T, int D, int NST, int NWA, int NWS, bool CL = false>
 static int score_attend_fits_t(const StoreView &s) {
-    auto k = score_attend_kernel<T, D, NST, NWA, NWS>;
+    auto k = score_attend_kernel<T, D, NST, NWA, NWS, CL>;
     const size_t smem = score_attend_smem<T, D, NST, NWA, NWS>(s);
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
         cudaGetLastError();
@@ -1040,7 +1045,8 @@ static int score_attend_fits_t(const StoreView &s) {
 // every cluster co-resident.  0: does not fit.
 template <typename T, int D, int NST, int NWA, int NWS>
 static int score_attend_split_t(const StoreView &s, int batch) {
-    if (!score_attend_fits_t<T, D, NST, NWA, NWS>(s)) return 0;
+    if (!score_attend_fits_t<T, D, NST, NWA, NWS, false>(s) || !score_attend_fits_t<T, D, NST, NWA, NWS, true>(s))
+        return 0;
     static int sms = 0;
     if (sms == 0) {
         int dev = 0;
@@ -1050,7 +1056,7 @@ static int score_attend_split_t(const StoreView &s, int batch) {
     const int heads = batch * s.H;
     if (g_score_mode == 1 || (g_score_mode < 0 && 2 * heads >= sms)) return 1;
     if (g_score_mode == 0) return 0;
-    auto k = score_attend_kernel<T, D, NST, NWA, NWS>;
+    auto k = score_attend_kernel<T, D, NST, NWA, NWS, true>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
         cudaGetLastError();
         return 0;
@@ -1098,8 +1104,11 @@ static cudaError_t launch_score_attend_t(const StoreView &s, int layer, const vo
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = S > 1 ? 2 : 1;
-    return cudaLaunchKernelEx(&cfg, score_attend_kernel<T, D, NST, NWA, NWS>, s, layer, (const T *)q, unstable,
-                              period, force_due, topk, extra, scores, kv_prefetch, a, S);
+    if (S > 1)
+        return cudaLaunchKernelEx(&cfg, score_attend_kernel<T, D, NST, NWA, NWS, true>, s, layer, (const T *)q,
+                                  unstable, period, force_due, topk, extra, scores, kv_prefetch, a, S);
+    return cudaLaunchKernelEx(&cfg, score_attend_kernel<T, D, NST, NWA, NWS, false>, s, layer, (const T *)q, unstable,
+                              period, force_due, topk, extra, scores, kv_prefetch, a, 1);
 }
 
 #ifndef FC_SA_SCORE_WARPS
