@@ -891,10 +891,13 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
     if constexpr (NWS > NWA) {
         if (!attends) {
             asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(RegSplit<NWS, NWA>::kLow));
-            if constexpr (!CL) return;  // (in a cluster they stay for the cluster barriers)
-        } else {
-            asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(RegSplit<NWS, NWA>::kHigh));
+            if constexpr (CL) {  // the cluster's two merge barriers, in as few registers as possible
+                asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+                asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+            }
+            return;
         }
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(RegSplit<NWS, NWA>::kHigh));
     }
     float *s_q = reinterpret_cast<float *>(dsm + score_attend_ring_bytes<T, D, NST, NWA>(s.NCAP));
     // the CTA's state for the cluster merge lives past the attention scratch
@@ -902,11 +905,13 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
     if constexpr (!CL) {
         attend_head_cta<T, D, NST, NWA>(s, a, bh, dsm, abars, s_wm, s_wl, s_q, 1);
     } else {
-        int n_att = 0;
-        if (attends) n_att = attend_head_cta<T, D, NST, NWA>(s, a, bh, dsm, abars, s_wm, s_wl, s_q, 1, S, rank, cstate);
-        cg::this_cluster().sync();  // every rank's state written
-        if (rank == 0 && attends && n_att > 0) merge_head_cluster<T, D>(s, a, bh, cstate, S, NWA * 32);
-        cg::this_cluster().sync();  // rank 0 done reading every rank's shared memory
+        // (only attending warps get here when NWS > NWA)
+        const int n_att = attend_head_cta<T, D, NST, NWA>(s, a, bh, dsm, abars, s_wm, s_wl, s_q, 1, S, rank, cstate);
+        // every rank's state written
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (rank == 0 && n_att > 0) merge_head_cluster<T, D>(s, a, bh, cstate, S, NWA * 32);
+        // rank 0 done reading every rank's shared memory
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
 }
 
