@@ -206,14 +206,15 @@ int fc_sparse_decode(const fc_store *s, int layer, const void *q,
                      void *stream);
 
 /* fc_score_select followed by fc_sparse_decode of the same layer, fused:
- * one CTA per (row, head) scores and selects (as fc_score_select:
- * score_pages / select_topk / rerank_due, scoring.py:93-202) and then, in
- * the same CTA, attends over the selection it just wrote (as
- * fc_sparse_decode: sparse_decode, attention.py:85-111, fused update_minmax,
- * scoring.py:59-69).  Identical results to the two calls; no grid-wide wait
- * between them.  Supported when the batch has at least ~half as many heads
- * as SMs (fc_score_attend_supported); otherwise FC_E_UNSUPPORTED and the
- * caller issues the two calls. */
+ * per (row, head) one CTA — or, for small batches, a cluster of CTAs whose
+ * keys meet in rank 0's shared memory — scores and selects (as
+ * fc_score_select: score_pages / select_topk / rerank_due, scoring.py:93-202)
+ * and then attends over the selection it just wrote (as fc_sparse_decode:
+ * sparse_decode, attention.py:85-111, fused update_minmax, scoring.py:59-69).
+ * Same results as the two calls; no grid-wide wait between them.
+ * fc_score_attend_supported returns the CTAs per head it uses for this batch,
+ * 0 when the geometry does not fit (FC_E_UNSUPPORTED: the caller issues the
+ * two calls). */
 int fc_score_attend_supported(const fc_store *s, int batch);
 int fc_score_attend(const fc_store *s, int layer, const void *q,
                     const uint8_t *unstable, int period, int force_due,
