@@ -640,11 +640,11 @@ void set_attn_mode(int m) { g_attn_mode = m; }
 #define FC_ATTN_SMAX kMaxClusterCtas  // largest automatic cluster size
 #endif
 int attn_split(const StoreView &s, int dtype, int batch, int max_pages, int n_ctas) {
-    if (n_ctas > 0) return n_ctas;  // explicit split (profiling)
     const int n_heads = batch * s.H;
 #define FC_OCC(T, DD, N, W) attn_ctas_per_sm_t<T, DD, N, W>(s)
-    const int occ = FC_ATTN_DISPATCH(dtype, s.D, FC_OCC);
+    const int occ = FC_ATTN_DISPATCH(dtype, s.D, FC_OCC);  // (also sets the kernel's smem attribute)
 #undef FC_OCC
+    if (n_ctas > 0) return n_ctas;  // explicit split (profiling, tests)
     const int64_t slots = (int64_t)occ * num_sms();
     if (g_attn_mode != 0 && (int64_t)n_heads * 2 <= slots) {  // far fewer heads than CTA slots: balanced all-SM variant
 #define FC_BOCC(T, DD, N, W) attn_bal_ctas_per_sm_t<T, DD, N, W>(s, n_heads)

@@ -199,3 +199,44 @@ def test_run_kernel_small_batch_clusters_vs_oracle(B, run_mode):
             want = O.gqa_sparse_decode(q[l, b, h * G:(h + 1) * G], k, v, PS, pages)
             got = o[l, b, h * G:(h + 1) * G]
             assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 2e-2, (b, l, h)
+
+
+def test_fused_one_cta_bitwise_equal_to_two_launches():
+    """fc_score_attend with one CTA per head (head-aligned mode) computes the
+    same page keys as the head-aligned scoring kernel and attends with the
+    same warp decomposition as fc_sparse_decode: selections, outputs and LSE
+    bit-identical to the two launches."""
+    import ctypes
+    from paper_2511_00868_b200 import _lib
+    from paper_2511_00868_b200.engine import DecodeEngine
+    from paper_2511_00868_b200.stability import HeadProfile
+    from paper_2511_00868_b200.synthetic import device_normal
+    lib = _lib.load()
+    lib.fc_debug_score_mode.argtypes = [ctypes.c_int]
+    lib.fc_debug_score_mode(1)  # head-aligned: one CTA per head in both paths
+    try:
+        B, L, H, G, D, T, K = 4, 1, 4, 4, 128, 3000, 16
+        eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=T + 64,
+                           topk_pages=K, rerank_period=4, profile=HeadProfile.first_n(L, H, 1.0))
+        for b in range(B):
+            eng.prefill_layer(b, 0, device_normal((H, T + 11 * b, D), seed=b),
+                              device_normal((H, T + 11 * b, D), seed=50 + b), alloc=True)
+        st = eng.store
+        q = device_normal(tuple(eng.q[0].shape), seed=7)
+        res = []
+        for fused in (False, True):
+            out = torch.zeros_like(eng.out[0])
+            lse = torch.zeros(B * H * G, dtype=torch.float32, device=q.device)
+            if fused:
+                st.score_attend(0, q, eng.unstable, 4, K, out, B, force_due=True, extra_tokens=1, lse=lse)
+            else:
+                st.score_select(0, q, eng.unstable, 4, K, B, force_due=True, extra_tokens=1)
+                st.sparse_decode(0, q, out, B, max_pages=eng.att_bound, lse=lse, extra_tokens=1,
+                                 attend_appended=False, n_ctas=1)  # one CTA per head, as fused
+            torch.cuda.synchronize()
+            st.check_errors()
+            res.append((st.sel.clone(), st.n_sel.clone(), out, lse))
+        for x, y in zip(*res):
+            assert torch.equal(x, y)
+    finally:
+        lib.fc_debug_score_mode(-1)
