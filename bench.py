@@ -335,6 +335,19 @@ def run_ours(args, cfg):
                                                      force_due=True, extra_tokens=1))
     sc_ms = sc_s * 1e3
     sc_bytes = eng.scoring_bytes(0, R)
+    # a scored layer as the step runs it: one fused score + select + attend
+    # launch (every head due), same method
+    fused = None
+    if eng.fused_score_attend and eng.store.score_attend_supported(B):
+        fu_s = time_launches(lambda l: eng.store.score_attend(
+            l, eng.q[l], eng.unstable, R, K, eng.out[l], B, force_due=True, extra_tokens=1, kv_prefetch=l > 0,
+            k_new=eng.k_new[l], v_new=eng.v_new[l]))
+        fu_bytes = sc_bytes + att_alg
+        fused = {"kernel": "fc_score_attend (score_attend_kernel: scoring, selection and attention of a head "
+                           "in one CTA / cluster), all heads due, 32 launches back to back",
+                 "us": fu_s * 1e6, "alg_bytes": fu_bytes, "achieved_gbs": fu_bytes / fu_s / 1e9,
+                 "frac": fu_bytes / fu_s / 1e9 / peak,
+                 "ctas_per_head": eng.store.score_attend_supported(B)}
 
     # ---- end to end through the public API with pinned host buffers
     e2e = None
@@ -398,6 +411,7 @@ def run_ours(args, cfg):
         "scoring": {"kernel": "fc_score_select (score_head_kernel: one CTA per head, bulk-copy ring + in-CTA select), all heads due, 32 launches back to back",
                     "us": sc_ms * 1e3, "alg_bytes": sc_bytes,
                     "achieved_gbs": sc_bytes / (sc_ms / 1e3) / 1e9},
+        "scored_layer": fused,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
         "e2e": e2e,
