@@ -69,6 +69,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=CFG2["batch"])
     ap.add_argument("--ctx", type=int, default=CFG2["ctx"])
     ap.add_argument("--layers", type=int, default=CFG2["layers"])
+    ap.add_argument("--serve", action="store_true",
+                    help="serving loop (SURVEY §8 f4): continuous batching of a synthetic request stream "
+                         "at config 2's model shape; prints serving metrics, not the headline metric")
     ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=2,
                     help="2: the metric's config (default); 3: long generation with host offload; "
                          "4: 128k ctx, 64 requests request-parallel (per-GPU share); "
@@ -649,8 +652,60 @@ def run_config5(args):
     print(json.dumps(line), flush=True)
 
 
+def run_serve(args):
+    """Continuous batching at config 2's shape: 48 requests (prompts 8k-32k
+    tokens, 32-256 output tokens, arrivals every 2 ms) over 16 rows, every
+    prefill and decode step on the GPU, the clock advanced by their measured
+    device times (paper_2511_00868_b200.serving)."""
+    import torch
+    from paper_2511_00868_b200.engine import DecodeEngine
+    from paper_2511_00868_b200.serving import Request, ServingLoop
+    from paper_2511_00868_b200.stability import HeadProfile
+    cfg = CFG2
+    L, H, G, D, K, R = cfg["layers"], cfg["kv_heads"], cfg["group"], cfg["head_dim"], cfg["topk"], cfg["period"]
+    B = cfg["batch"]
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(7)
+    n_req = 48
+    reqs = [Request(i, 0.002 * i, int(rng.integers(8192, 32768)), int(rng.integers(32, 257))) for i in range(n_req)]
+    cap = max(r.prompt_tokens + r.output_tokens for r in reqs) + 32
+    prof = HeadProfile.first_n(L, H, cfg["unstable_fraction"], model_id="llama3.1-8b-shaped")
+    # the pool holds 12 requests at their largest: admission, not row count, bounds the batch
+    n_blocks = 12 * L * H * (cap // 16 + 1) + 1
+    eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=cap, topk_pages=K,
+                       rerank_period=R, profile=prof, dtype=torch.bfloat16, device=dev, n_blocks=n_blocks)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(11)
+
+    def make_prompt(req):
+        g = torch.Generator(device=dev)
+        g.manual_seed(5000 + req.id)
+        k = torch.randn((L, H, req.prompt_tokens, D), generator=g, device=dev, dtype=torch.bfloat16)
+        v = torch.randn((L, H, req.prompt_tokens, D), generator=g, device=dev, dtype=torch.bfloat16)
+        return k, v
+
+    def feed(e):
+        e.q.normal_(generator=gen)
+        e.k_new.normal_(generator=gen)
+        e.v_new.normal_(generator=gen)
+
+    loop = ServingLoop(eng, reqs, make_prompt, feed)
+    m = loop.run()
+    line = {"metric": "serving: decode tokens/s, TTFT, TPOT (continuous batching, device-timed)",
+            "value": m.throughput_tokens_per_s, "unit": "tokens/s", "n_gpus": 1,
+            "higher_is_better": True, "dtype": "bf16", "data": "synthetic N(0,1) prompts and decode inputs",
+            "config": {"workload": "config2 model shape, 48 requests, prompts 8k-32k, outputs 32-256, "
+                                   "arrivals every 2 ms, 16 rows, pool for 12 requests at their largest",
+                       "ctx_cap": cap},
+            "metrics": {f: getattr(m, f) for f in m.__dataclass_fields__}}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
+    if args.serve:
+        run_serve(args)
+        return
     cfg = dict(CFG2)
     cfg.update(batch=args.batch, ctx=args.ctx, layers=args.layers)
     if args.impl == "reference":

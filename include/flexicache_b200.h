@@ -89,6 +89,12 @@ const char *fc_last_error(void);
 
 /* ---- (4) allocation and step bookkeeping ------------------------------- */
 
+/* Release every page of request row `row` (all layers, all heads) to the
+ * free list, empty its selections and mark it free (seq_len = -1; a free row
+ * is skipped by every kernel, fc_step_advance included): a finished request
+ * in the serving loop.  Free-list order is not deterministic. */
+int fc_free_row(const fc_store *s, int row, void *stream);
+
 /* Allocate logical pages [first_page, first_page+n_pages) for every
  * (layer, head) of request row `row`, popping the device free list in
  * (layer, head, page) order — the order of the reference prefill, which

@@ -55,6 +55,7 @@ _SIGNATURES = {
     "fc_version": (ctypes.c_char_p, []),
     "fc_last_error": (ctypes.c_char_p, []),
     "fc_alloc_pages": (_i, [_p, _i, _i, _i, _p]),
+    "fc_free_row": (_i, [_p, _i, _p]),
     "fc_step_advance": (_i, [_p, _i, _p]),
     "fc_kv_prefill": (_i, [_p, _i, _i, _p, _p, _i, _p]),
     "fc_kv_append": (_i, [_p, _i, _p, _p, _i, _p]),

@@ -78,6 +78,12 @@ int fc_debug_attn_mode(int mode) { set_attn_mode(mode); return FC_OK; }
  * kernel when it fits (default), 1 warp-balanced persistent kernel */
 int fc_debug_run_mode(int mode) { set_run_mode(mode); return FC_OK; }
 
+int fc_free_row(const fc_store *s, int row, void *stream) {
+    FC_CHECK(check_store(s));
+    if (row < 0 || row >= s->batch_cap) return invalid("row out of range");
+    return cuda_status(launch_free_row(make_view(s), row, (cudaStream_t)stream));
+}
+
 int fc_alloc_pages(const fc_store *s, int row, int first_page, int n_pages, void *stream) {
     FC_CHECK(check_store(s));
     if (row < 0 || row >= s->batch_cap) return invalid("row out of range");

@@ -44,7 +44,7 @@ __global__ void step_advance_kernel(StoreView s, int batch) {
     __shared__ int s_fail;
     const int b = threadIdx.x;
     int need = 0, len = 0;
-    if (b < batch) {
+    if (b < batch && s.seq_len[b] >= 0) {  // seq_len < 0: a free row (serving loop), left alone
         len = s.seq_len[b] + 1;
         if (len % s.PS == 0) {
             if (len / s.PS < s.NCAP) need = 1;
@@ -84,7 +84,7 @@ __global__ void step_advance_kernel(StoreView s, int batch) {
         }
     }
     __syncthreads();
-    if (b < batch) s.seq_len[b] = len;
+    if (b < batch && s.seq_len[b] >= 0) s.seq_len[b] = len;
     if (threadIdx.x == 0) {
         if (!s_fail) *s.free_top = top - s_total * LH;
         *s.step += 1;
@@ -107,6 +107,33 @@ __global__ void evict_pages_kernel(StoreView s, const int32_t *pages, int n) {
         s.table[off] = FC_NULL_BLOCK;
     }
     *s.free_top = top;
+}
+
+// Release every page of request row `row` (all layers and heads) to the free
+// list and mark the row free (seq_len = -1, empty selections): the end of a
+// request in the serving loop (the reference's _finish releases its table
+// row, simulator.py).  One CTA per (layer, head); blocks are pushed with
+// warp-aggregated atomics (free-list order is not deterministic here).
+__global__ void free_row_kernel(StoreView s, int row) {
+    const int lh = blockIdx.x, l = lh / s.H, h = lh % s.H;
+    const int hx = s.hix(row, l, h);
+    int32_t *trow = s.table + s.table_off(hx, 0);
+    const int lane = threadIdx.x & 31;
+    for (int p0 = 0; p0 < s.NCAP; p0 += blockDim.x) {
+        const int p = p0 + threadIdx.x;
+        const int blk = p < s.NCAP ? trow[p] : FC_NULL_BLOCK;
+        const bool live = blk != FC_NULL_BLOCK;
+        const unsigned m = __ballot_sync(0xffffffffu, live);
+        int base = 0;
+        if (lane == 0 && m) base = atomicAdd(s.free_top, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (live) {
+            s.free_stack[base + __popc(m & ((1u << lane) - 1u))] = blk;
+            trow[p] = FC_NULL_BLOCK;
+        }
+    }
+    if (threadIdx.x == 0) s.n_sel[hx] = 0;
+    if (lh == 0 && threadIdx.x == 0) s.seq_len[row] = -1;
 }
 
 // ---------------------------------------------------------------------------
@@ -224,6 +251,11 @@ cudaError_t launch_alloc_pages(const StoreView &s, int row, int first, int n, cu
 
 cudaError_t launch_step_advance(const StoreView &s, int batch, cudaStream_t st) {
     step_advance_kernel<<<1, 1024, 0, st>>>(s, batch);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_free_row(const StoreView &s, int row, cudaStream_t st) {
+    free_row_kernel<<<s.L * s.H, 256, 0, st>>>(s, row);
     return cudaGetLastError();
 }
 

@@ -52,6 +52,7 @@ cudaError_t launch_attn_persist(const StoreView &, int, const RunArgs &, int, cu
 
 cudaError_t launch_alloc_pages(const StoreView &, int, int, int, cudaStream_t);
 cudaError_t launch_step_advance(const StoreView &, int, cudaStream_t);
+cudaError_t launch_free_row(const StoreView &, int, cudaStream_t);
 cudaError_t launch_evict_pages(const StoreView &, const int32_t *, int, cudaStream_t);
 cudaError_t launch_prefill(const StoreView &, int, int, int, const void *, const void *, int, cudaStream_t);
 cudaError_t launch_append(const StoreView &, int, int, const void *, const void *, int, cudaStream_t);

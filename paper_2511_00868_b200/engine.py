@@ -124,6 +124,41 @@ class DecodeEngine:
         self.store.seq_len[row] = T
         self.seq_host[row] = T
 
+    # -- rows joining and leaving (serving loop, f4) -------------------------------
+
+    def start_serving(self) -> None:
+        """Every row free (seq_len = -1: skipped by every kernel); requests
+        then join with admit() and leave with retire()."""
+        if self.tiering:
+            raise NotImplementedError("the serving loop runs the all-resident engine")
+        self.store.seq_len.fill_(-1)
+        self.seq_host = [-1] * self.B
+        self.selected = True            # initial selections are made per admitted row
+        self._initial_rows = set()
+
+    def admit(self, row: int, keys: torch.Tensor, values: torch.Tensor) -> None:
+        """Prefill request row ``row`` (keys/values [L, H, T, d]); its initial
+        selection is made at its first decode step, with that step's query."""
+        if self.seq_host[row] >= 0:
+            raise ValueError(f"row {row} is busy")
+        self.prefill(row, keys, values)
+        self._initial_rows.add(row)
+
+    def retire(self, row: int) -> None:
+        """A finished request: every page of its row back to the free list."""
+        self.store.free_row(row)
+        self.seq_host[row] = -1
+        self._initial_rows.discard(row)
+
+    def _initial_selections(self) -> None:
+        # every head of a newly admitted row selects with this step's query
+        # (the batch graph then re-scores only the heads that are due)
+        for row in sorted(self._initial_rows):
+            for layer in range(self.L):
+                self.store.score_select_row(row, layer, self.q[layer, row], self.unstable, self.R, self.K,
+                                            force_due=True, extra_tokens=1)
+        self._initial_rows.clear()
+
     def prefill_layer(self, row: int, layer: int, k: torch.Tensor, v: torch.Tensor,
                       alloc: bool) -> None:
         """Layer-at-a-time prefill (bench scale); ``alloc`` on the first layer."""
@@ -245,6 +280,8 @@ class DecodeEngine:
                 self.store.evict_unselected(self.unstable, self.B)
             self.selected = True
         else:
+            if getattr(self, "_initial_rows", None):
+                self._initial_selections()
             if rerank and self.tiering and self.stager is not None:
                 self.stager.wait()  # staged promotions have landed
             if use_graph:
@@ -260,7 +297,7 @@ class DecodeEngine:
                     and any((self.t + ld) % self.R == 0 for ld in self.stager.leads)):
                 self.stager.predict(self.q, self.B, self._stable_layers)
         self.t += 1
-        self.seq_host = [s + 1 for s in self.seq_host]
+        self.seq_host = [s + 1 if s >= 0 else s for s in self.seq_host]
         return self.out
 
     def attach_recorder(self, recorder) -> None:

@@ -1,0 +1,183 @@
+"""Serving loop on the real decode path.
+
+The reference's ``Simulator`` (simulator.py:230-600) schedules requests over
+a cost model: admission while the committed fast-tier bytes fit
+(``_commit_bytes`` / ``_admissible``, simulator.py:253-284), prefill, batched
+decode steps, finish, and the ``Metrics`` of simulator.py:87-131.  This loop
+keeps that control flow but runs every step on the GPU: requests occupy the
+rows of a ``DecodeEngine`` (``start_serving`` / ``admit`` / ``retire``), the
+clock advances by the MEASURED device time of each prefill and decode step
+(CUDA events), and TTFT / TPOT / throughput come from those times.
+
+Differences from the simulator, by construction:
+* all-resident engine (no pinned-host tier; FlexiCache admission counts the
+  whole KV of a request, the DENSE commit of simulator.py:257-258, since no
+  page leaves HBM);
+* the rerank schedule is the engine's global step counter (every row reranks
+  at t % R == 0), not a per-request t;
+* no reload pauses (nothing is reloaded).
+Prompts and decode inputs are synthetic (the reference has no model either).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field, fields
+
+import torch
+
+from .store import PAGE_SIZE
+
+
+@dataclass
+class Request:
+    """One request: arrival time (s), prompt and output lengths (tokens)."""
+    id: int
+    arrival_s: float
+    prompt_tokens: int
+    output_tokens: int
+
+
+@dataclass
+class ServingMetrics:
+    """The reference's ``Metrics`` fields this loop measures (simulator.py:87-131)."""
+    n_requests: int = 0
+    finished: int = 0
+    queued_at_end: int = 0
+    total_tokens: int = 0
+    output_tokens: int = 0
+    sim_time_s: float = 0.0
+    throughput_tokens_per_s: float = 0.0
+    ttft_mean_s: float = 0.0
+    ttft_p50_s: float = 0.0
+    ttft_p95_s: float = 0.0
+    ttft_p99_s: float = 0.0
+    tpot_mean_s: float = 0.0
+    tpot_p50_s: float = 0.0
+    tpot_p95_s: float = 0.0
+    tpot_p99_s: float = 0.0
+    peak_batch: int = 0
+    peak_fast_bytes: int = 0
+    decode_steps: int = 0
+
+    def to_text(self) -> str:
+        return "".join(f"{f.name} = {getattr(self, f.name)}\n" for f in fields(self))
+
+
+def _pct(xs, p):
+    if not xs:
+        return 0.0
+    s = sorted(xs)
+    k = min(len(s) - 1, max(0, math.ceil(p / 100.0 * len(s)) - 1))
+    return s[k]
+
+
+@dataclass
+class _Active:
+    req: Request
+    row: int
+    emitted: int = 0
+    first_token_s: float = 0.0
+    step_times: list = field(default_factory=list)
+
+
+class ServingLoop:
+    """Continuous batching of ``requests`` over ``engine``'s rows.
+
+    ``make_prompt(req)`` returns (keys, values) [L, H, T, d] on the device;
+    ``feed(engine)`` writes the step's q / k_new / v_new (synthetic inputs).
+    """
+
+    def __init__(self, engine, requests, make_prompt, feed, *, fast_capacity_blocks: int | None = None,
+                 timer=None):
+        self.eng = engine
+        self.timer = timer if timer is not None else self._time  # timer(fn) -> seconds
+        self.pending = sorted(requests, key=lambda r: (r.arrival_s, r.id))
+        self.make_prompt = make_prompt
+        self.feed = feed
+        st = engine.store
+        self.page_bytes = st.page_bytes
+        self.LH = engine.L * engine.H
+        self.capacity = (st.n_blocks - 1) if fast_capacity_blocks is None else fast_capacity_blocks
+        self.committed = 0
+        self.now = 0.0
+        self.m = ServingMetrics(n_requests=len(requests))
+        self._ttft, self._tpot = [], []
+
+    def _commit_blocks(self, req: Request) -> int:
+        # the whole KV of the request stays in HBM: every page it will ever
+        # hold, for every (layer, head) (DENSE commit, simulator.py:257-258)
+        max_tokens = req.prompt_tokens + req.output_tokens
+        return (max_tokens // PAGE_SIZE + 1) * self.LH
+
+    def _time(self, fn) -> float:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        return a.elapsed_time(b) / 1e3
+
+    def run(self, max_steps: int = 1 << 30) -> ServingMetrics:
+        eng = self.eng
+        eng.start_serving()
+        free_rows = list(range(eng.B))
+        active: dict[int, _Active] = {}
+        ready: list[Request] = []
+        steps = 0
+        while (self.pending or ready or active) and steps < max_steps:
+            while self.pending and self.pending[0].arrival_s <= self.now:
+                ready.append(self.pending.pop(0))
+            # admission while a row is free and the commitment fits (_admissible)
+            while ready and free_rows:
+                need = self._commit_blocks(ready[0])
+                if need > self.capacity:
+                    raise ValueError(f"request {ready[0].id} cannot fit even alone ({need} blocks)")
+                if self.committed + need > self.capacity:
+                    break
+                req = ready.pop(0)
+                row = free_rows.pop(0)
+                self.committed += need
+                keys, values = self.make_prompt(req)
+                self.now += self.timer(lambda: eng.admit(row, keys, values))
+                active[row] = _Active(req, row)
+                self._ttft.append(self.now - req.arrival_s)  # prefill emits the first token
+                active[row].emitted = 1
+                active[row].first_token_s = self.now
+                self.m.total_tokens += req.prompt_tokens
+            self.m.peak_batch = max(self.m.peak_batch, len(active))
+            in_use = (eng.store.n_blocks - 1 - eng.store.free_count()) * self.page_bytes
+            self.m.peak_fast_bytes = max(self.m.peak_fast_bytes, in_use)
+            if not active:  # idle: jump to the next arrival
+                if self.pending:
+                    self.now = max(self.now, self.pending[0].arrival_s)
+                continue
+            self.feed(eng)
+            dt = self.timer(eng.step)
+            eng.store.check_errors()
+            self.now += dt
+            steps += 1
+            for row in list(active):
+                a = active[row]
+                a.emitted += 1
+                a.step_times.append(dt)
+                self.m.output_tokens += 1
+                if a.emitted >= a.req.output_tokens:
+                    eng.retire(row)
+                    self.committed -= self._commit_blocks(a.req)
+                    free_rows.append(row)
+                    self._tpot.extend(a.step_times)
+                    self.m.finished += 1
+                    del active[row]
+        m = self.m
+        m.queued_at_end = len(self.pending) + len(ready)
+        m.decode_steps = steps
+        m.sim_time_s = self.now
+        m.throughput_tokens_per_s = m.output_tokens / self.now if self.now > 0 else 0.0
+        if self._ttft:
+            m.ttft_mean_s = sum(self._ttft) / len(self._ttft)
+            m.ttft_p50_s, m.ttft_p95_s, m.ttft_p99_s = (_pct(self._ttft, p) for p in (50, 95, 99))
+        if self._tpot:
+            m.tpot_mean_s = sum(self._tpot) / len(self._tpot)
+            m.tpot_p50_s, m.tpot_p95_s, m.tpot_p99_s = (_pct(self._tpot, p) for p in (50, 95, 99))
+        return m

@@ -124,6 +124,38 @@ class KVStore:
         _lib.check(self.lib.fc_alloc_pages(self.cptr, row, first_page, n_pages, self.stream()),
                    "fc_alloc_pages")
 
+    def free_row(self, row: int) -> None:
+        """Release every page of request row ``row`` and mark it free
+        (seq_len = -1: skipped by every kernel) — fc_free_row."""
+        _lib.check(self.lib.fc_free_row(self.cptr, row, self.stream()), "fc_free_row")
+
+    def row_view(self, row: int) -> int:
+        """An fc_store of the single request row ``row`` (batch_cap 1, the
+        per-row buffers offset to it; pool, free list and step shared): a
+        call through it touches that row only (e.g. the initial selection of
+        a request admitted mid-stream)."""
+        views = self.__dict__.setdefault("_row_views", {})
+        if row not in views:
+            if not 0 <= row < self.B:
+                raise ValueError("row out of range")
+            c = _lib.FcStore.from_buffer_copy(self._c)
+            c.batch_cap = 1
+            c.table = self.table[row].data_ptr()
+            c.summaries = self.summaries[row].data_ptr()
+            c.seq_len = self.seq_len[row:row + 1].data_ptr()
+            c.sel = self.sel[row].data_ptr()
+            c.n_sel = self.n_sel[row].data_ptr()
+            views[row] = c
+        return ctypes.addressof(views[row])
+
+    def score_select_row(self, row: int, layer: int, q_row: torch.Tensor, unstable: torch.Tensor, period: int,
+                         topk: int, *, force_due: bool = True, extra_tokens: int = 1) -> None:
+        """fc_score_select of one request row (q_row: [Hq, d] of that row)."""
+        _lib.check(self.lib.fc_score_select(
+            self.row_view(row), layer, q_row.data_ptr(), unstable.data_ptr(), period, int(force_due), topk,
+            extra_tokens, 0, self.scores.data_ptr(), self.score_counters.data_ptr(), 1, self.stream()),
+            "fc_score_select")
+
     def step_advance(self, batch: int) -> None:
         _lib.check(self.lib.fc_step_advance(self.cptr, batch, self.stream()), "fc_step_advance")
 

@@ -1,0 +1,85 @@
+"""Serving-loop control flow (admission under the fast-tier budget, finish,
+metrics) with a stand-in engine — no GPU (the loop itself is host code;
+tests/test_gpu_serving.py runs it on the decode path)."""
+
+from paper_2511_00868_b200.serving import Request, ServingLoop
+
+
+class _Store:
+    def __init__(self, n_blocks):
+        self.n_blocks = n_blocks
+        self.used = 0
+        self.page_bytes = 8192
+
+    def free_count(self):
+        return self.n_blocks - 1 - self.used
+
+    def check_errors(self):
+        pass
+
+
+class _Engine:
+    """Rows, prefill / free bookkeeping and a step counter, no kernels."""
+
+    def __init__(self, B, L, H, n_blocks):
+        self.B, self.L, self.H = B, L, H
+        self.store = _Store(n_blocks)
+        self.rows = {}
+        self.steps = 0
+        self.max_active = 0
+
+    def start_serving(self):
+        self.rows = {}
+
+    def admit(self, row, keys, values):
+        assert row not in self.rows
+        T = keys
+        self.rows[row] = T
+        self.store.used += (T // 16 + 1) * self.L * self.H
+
+    def retire(self, row):
+        T = self.rows.pop(row)
+        self.store.used -= (T // 16 + 1) * self.L * self.H
+
+    def step(self):
+        self.steps += 1
+        self.max_active = max(self.max_active, len(self.rows))
+
+
+def _run(requests, B=2, n_blocks=10_000, step_s=0.01, prefill_s=0.05):
+    eng = _Engine(B, 2, 2, n_blocks)
+    times = iter([])
+
+    def timer(fn):
+        name = getattr(fn, "__name__", "")
+        fn()
+        return step_s if name == "step" else prefill_s
+    loop = ServingLoop(eng, requests, make_prompt=lambda r: (r.prompt_tokens, r.prompt_tokens),
+                       feed=lambda e: None, timer=timer)
+    del times
+    return loop.run(), eng
+
+
+def test_every_request_finishes_and_tokens_add_up():
+    reqs = [Request(i, 0.0, 100 + 10 * i, 5 + i) for i in range(5)]
+    m, eng = _run(reqs, B=2)
+    assert m.finished == 5 and m.queued_at_end == 0
+    assert m.output_tokens == sum(r.output_tokens - 1 for r in reqs)  # prefill emits the first token
+    assert m.peak_batch == 2 and eng.max_active == 2
+    assert eng.rows == {}
+    assert m.throughput_tokens_per_s > 0 and m.tpot_mean_s == 0.01
+
+
+def test_admission_waits_for_budget():
+    # each request commits (160 // 16 + 1) * 4 = 44 blocks: the budget holds one
+    reqs = [Request(i, 0.0, 150, 3) for i in range(3)]
+    m, eng = _run(reqs, B=3, n_blocks=60)
+    assert m.finished == 3 and m.peak_batch == 1
+
+
+def test_idle_until_arrival_and_ttft():
+    reqs = [Request(0, 1.0, 64, 2)]
+    m, _ = _run(reqs, B=1)
+    assert m.finished == 1
+    assert abs(m.ttft_mean_s - 0.05) < 1e-12          # arrives at 1.0, prefilled by 1.05
+    assert abs(m.sim_time_s - (1.0 + 0.05 + 0.01)) < 1e-12
