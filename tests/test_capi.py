@@ -54,3 +54,38 @@ def test_unsupported_geometry_rejected():
     rc = lib.fc_step_advance(ctypes.byref(s), 1, None)
     with pytest.raises(ValueError, match="head_dim 96"):
         _lib.check(rc, "fc_step_advance")
+
+
+def _fake_store(**kw):
+    """A valid-looking descriptor (non-null dummy pointers): argument checks
+    run, no kernel is launched."""
+    geo = dict(batch_cap=2, layers=4, kv_heads=2, group=4, head_dim=128, page_size=16, pages_cap=64,
+               sel_cap=16, dtype=_lib.FC_BF16, n_blocks=128)
+    geo.update(kw)
+    return _lib.FcStore(*geo.values(), *([64] * 10))
+
+
+@pytest.mark.parametrize("call,msg", [
+    (lambda lib, s: lib.fc_sparse_decode_layers(s, 3, 2, 64, 0, None, None, 0, 64, 0, None, 0, 0.1, 1, 0, 0,
+                                                8, 64, 1 << 20, 1, None), "layer run out of range"),
+    (lambda lib, s: lib.fc_sparse_decode_layers(s, 0, 2, 64, 0, None, None, 0, 64, 0, None, 0, 0.1, 1, 0, 0,
+                                                8, 64, 1 << 20, 1, None), "layer strides"),
+    (lambda lib, s: lib.fc_sparse_decode_layers(s, 0, 1, 64, 0, None, None, 0, 64, 0, None, 0, -1.0, 1, 0, 0,
+                                                8, 64, 1 << 20, 1, None), "scale must be positive"),
+    (lambda lib, s: lib.fc_score_attend(s, 9, 64, 64, 4, 0, 8, 1, 0, 64, None, None, 64, None, 0.1, 0, 1, None),
+     "layer out of range"),
+    (lambda lib, s: lib.fc_score_attend(s, 0, 64, 64, 0, 0, 8, 1, 0, 64, None, None, 64, None, 0.1, 0, 1, None),
+     "period must be >= 1"),
+    (lambda lib, s: lib.fc_score_attend(s, 0, 64, 64, 4, 0, 8, 1, 0, 64, 64, None, 64, None, 0.1, 0, 1, None),
+     "k_new and v_new go together"),
+    (lambda lib, s: lib.fc_free_row(s, 5, None), "row out of range"),
+    (lambda lib, s: lib.fc_stage_plan(s, 64, 64, 64, 64, 64, 64, 64, 0, 1, 0, None), "capacity must be >= 1"),
+    (lambda lib, s: lib.fc_stage_fetch(s, 64, 64, 64, 8, 64, 7, None), "pass must be in 0..3"),
+    (lambda lib, s: lib.fc_fetch_pages_staged(s, 0, 64, 64, 64, 8, None, 64, None, None), "null buffer"),
+])
+def test_new_entry_points_validate_without_gpu(call, msg):
+    lib = _lib.load()
+    s = _fake_store()
+    rc = call(lib, ctypes.byref(s))
+    with pytest.raises(ValueError, match=msg):
+        _lib.check(rc, "call")
