@@ -72,6 +72,8 @@ def parse():
     ap.add_argument("--serve", action="store_true",
                     help="serving loop (SURVEY §8 f4): continuous batching of a synthetic request stream "
                          "at config 2's model shape; prints serving metrics, not the headline metric")
+    ap.add_argument("--tiered", action="store_true",
+                    help="with --serve: the two-tier engine (pinned-host slow tier, FlexiCache admission)")
     ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=2,
                     help="2: the metric's config (default); 3: long generation with host offload; "
                          "4: 128k ctx, 64 requests request-parallel (per-GPU share); "
@@ -673,7 +675,8 @@ def run_serve(args):
     # the pool holds 12 requests at their largest: admission, not row count, bounds the batch
     n_blocks = 12 * L * H * (cap // 16 + 1) + 1
     eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=cap, topk_pages=K,
-                       rerank_period=R, profile=prof, dtype=torch.bfloat16, device=dev, n_blocks=n_blocks)
+                       rerank_period=R, profile=prof, dtype=torch.bfloat16, device=dev, n_blocks=n_blocks,
+                       tiering=args.tiered)
     gen = torch.Generator(device=dev)
     gen.manual_seed(11)
 
@@ -696,7 +699,7 @@ def run_serve(args):
             "higher_is_better": True, "dtype": "bf16", "data": "synthetic N(0,1) prompts and decode inputs",
             "config": {"workload": "config2 model shape, 48 requests, prompts 8k-32k, outputs 32-256, "
                                    "arrivals every 2 ms, 16 rows, pool for 12 requests at their largest",
-                       "ctx_cap": cap},
+                       "ctx_cap": cap, "tiered": bool(args.tiered)},
             "metrics": {f: getattr(m, f) for f in m.__dataclass_fields__}}
     print(json.dumps(line), flush=True)
 

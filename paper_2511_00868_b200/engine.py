@@ -129,8 +129,6 @@ class DecodeEngine:
     def start_serving(self) -> None:
         """Every row free (seq_len = -1: skipped by every kernel); requests
         then join with admit() and leave with retire()."""
-        if self.tiering:
-            raise NotImplementedError("the serving loop runs the all-resident engine")
         self.store.seq_len.fill_(-1)
         self.seq_host = [-1] * self.B
         self.selected = True            # initial selections are made per admitted row
@@ -142,6 +140,8 @@ class DecodeEngine:
         if self.seq_host[row] >= 0:
             raise ValueError(f"row {row} is busy")
         self.prefill(row, keys, values)
+        if self.tiering:  # post-prefill offload of every full stable-head page (tiering.py:122-139)
+            self.tier.offload_after_prefill(row, keys.shape[2] // PAGE_SIZE)
         self._initial_rows.add(row)
 
     def retire(self, row: int) -> None:
@@ -149,6 +149,8 @@ class DecodeEngine:
         self.store.free_row(row)
         self.seq_host[row] = -1
         self._initial_rows.discard(row)
+        if self.tiering:
+            self.tier.release_row(row)
 
     def _initial_selections(self) -> None:
         # every head of a newly admitted row selects with this step's query
@@ -157,6 +159,8 @@ class DecodeEngine:
             for layer in range(self.L):
                 self.store.score_select_row(row, layer, self.q[layer, row], self.unstable, self.R, self.K,
                                             force_due=True, extra_tokens=1)
+            if self.tiering:  # stable heads keep only their selection in HBM
+                self.store.evict_unselected_row(row, self.unstable)
         self._initial_rows.clear()
 
     def prefill_layer(self, row: int, layer: int, k: torch.Tensor, v: torch.Tensor,

@@ -9,13 +9,17 @@ rows of a ``DecodeEngine`` (``start_serving`` / ``admit`` / ``retire``), the
 clock advances by the MEASURED device time of each prefill and decode step
 (CUDA events), and TTFT / TPOT / throughput come from those times.
 
+With a two-tier engine, admission uses FlexiCache's commit (unstable heads
+every page, stable heads their selection, simulator.py:253-266), an
+admitted request's full stable-head pages are offloaded after its prefill
+and evicted after its initial selection, and reranks fetch promoted pages
+(staged ahead, tiering.ReloadStager).  With an all-resident engine the
+commit is the request's whole KV (simulator.py:257-258).
+
 Differences from the simulator, by construction:
-* all-resident engine (no pinned-host tier; FlexiCache admission counts the
-  whole KV of a request, the DENSE commit of simulator.py:257-258, since no
-  page leaves HBM);
 * the rerank schedule is the engine's global step counter (every row reranks
   at t % R == 0), not a per-request t;
-* no reload pauses (nothing is reloaded).
+* no reload pauses: promoted pages are fetched inside the rerank step.
 Prompts and decode inputs are synthetic (the reference has no model either).
 """
 
@@ -76,6 +80,7 @@ def _pct(xs, p):
 class _Active:
     req: Request
     row: int
+    commit: int = 0
     emitted: int = 0
     first_token_s: float = 0.0
     step_times: list = field(default_factory=list)
@@ -105,10 +110,30 @@ class ServingLoop:
         self._ttft, self._tpot = [], []
 
     def _commit_blocks(self, req: Request) -> int:
-        # the whole KV of the request stays in HBM: every page it will ever
-        # hold, for every (layer, head) (DENSE commit, simulator.py:257-258)
-        max_tokens = req.prompt_tokens + req.output_tokens
-        return (max_tokens // PAGE_SIZE + 1) * self.LH
+        n_max = (req.prompt_tokens + req.output_tokens) // PAGE_SIZE + 1
+        if not self.eng.tiering:
+            # all-resident: every page the request will ever hold, for every
+            # (layer, head) (DENSE commit, simulator.py:257-258)
+            return n_max * self.LH
+        # two-tier (FlexiCache commit, simulator.py:253-266): unstable heads keep
+        # every page, stable heads their selection + the pages appended between
+        # reranks; at least the prompt until its post-prefill eviction
+        n_unstable = int(self.eng.unstable.sum().item())
+        n_stable = self.LH - n_unstable
+        slack = self.eng.R // PAGE_SIZE + 2
+        steady = n_unstable * n_max + n_stable * (min(self.eng.K, n_max) + slack)
+        peak = (req.prompt_tokens // PAGE_SIZE + 1 + slack) * self.LH
+        return max(steady, peak)
+
+    def _steady_blocks(self, req: Request) -> int:
+        """The commitment once the prompt's unselected stable-head pages left
+        HBM (_finish_prefill_offload releases the rest, simulator.py:389-408)."""
+        if not self.eng.tiering:
+            return self._commit_blocks(req)
+        n_max = (req.prompt_tokens + req.output_tokens) // PAGE_SIZE + 1
+        n_unstable = int(self.eng.unstable.sum().item())
+        slack = self.eng.R // PAGE_SIZE + 2
+        return n_unstable * n_max + (self.LH - n_unstable) * (min(self.eng.K, n_max) + slack)
 
     def _time(self, fn) -> float:
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -140,7 +165,7 @@ class ServingLoop:
                 self.committed += need
                 keys, values = self.make_prompt(req)
                 self.now += self.timer(lambda: eng.admit(row, keys, values))
-                active[row] = _Active(req, row)
+                active[row] = _Active(req, row, commit=need)
                 self._ttft.append(self.now - req.arrival_s)  # prefill emits the first token
                 active[row].emitted = 1
                 active[row].first_token_s = self.now
@@ -162,9 +187,13 @@ class ServingLoop:
                 a.emitted += 1
                 a.step_times.append(dt)
                 self.m.output_tokens += 1
+                steady = self._steady_blocks(a.req)
+                if a.commit > steady:  # its first step selected and evicted: the peak is released
+                    self.committed -= a.commit - steady
+                    a.commit = steady
                 if a.emitted >= a.req.output_tokens:
                     eng.retire(row)
-                    self.committed -= self._commit_blocks(a.req)
+                    self.committed -= a.commit
                     free_rows.append(row)
                     self._tpot.extend(a.step_times)
                     self.m.finished += 1

@@ -404,6 +404,11 @@ class KVStore:
                                               _ptr(slow_resident), batch, self.stream()),
                    "fc_offload_filled")
 
+    def evict_unselected_row(self, row: int, unstable: torch.Tensor) -> None:
+        """fc_evict_unselected of one request row (through its row view)."""
+        _lib.check(self.lib.fc_evict_unselected(self.row_view(row), unstable.data_ptr(), 1, self.stream()),
+                   "fc_evict_unselected")
+
     def evict_unselected(self, unstable: torch.Tensor, batch: int) -> None:
         _lib.check(self.lib.fc_evict_unselected(self.cptr, unstable.data_ptr(), batch, self.stream()),
                    "fc_evict_unselected")

@@ -102,6 +102,14 @@ class TierStore:
         """Fetch promoted pages (copy list from fc_rerank_recycle) host -> HBM."""
         self.store.fetch_pages(layer, self.host, copies, n_copies)
 
+    def release_row(self, row: int) -> None:
+        """A finished request: its slow-tier pages are no longer needed (the
+        ledger entries and the bytes they held are released; the row may host
+        a new request, whose write-once ledger starts empty)."""
+        for key in [k for k in self._counts if k[0] == row]:
+            self.slow_bytes_used -= len(self._counts.pop(key)) * self.page_bytes
+        self.slow_resident[row].zero_()
+
     def offload_counts(self, row: int, head: HeadId) -> dict:
         return dict(self._counts.get((row, HeadId(*head)), {}))
 

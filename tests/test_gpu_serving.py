@@ -21,11 +21,11 @@ def _cuda():
         pytest.skip("needs a CUDA device")
 
 
-def _setup(B=3, L=2, H=2, G=4, D=128, K=8, R=4, cap=2000):
+def _setup(B=3, L=2, H=2, G=4, D=128, K=8, R=4, cap=2000, tiering=False):
     from paper_2511_00868_b200.engine import DecodeEngine
     from paper_2511_00868_b200.stability import HeadProfile
     eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=cap,
-                       topk_pages=K, rerank_period=R, profile=HeadProfile.first_n(L, H, 0.5))
+                       topk_pages=K, rerank_period=R, profile=HeadProfile.first_n(L, H, 0.5), tiering=tiering)
     return eng
 
 
@@ -61,10 +61,13 @@ def test_serving_loop_requests_finish_and_blocks_return():
     assert bool((eng.store.table == 0).all())
 
 
-def test_request_joining_mid_stream_matches_oracle():
+@pytest.mark.parametrize("tiering", [False, True])
+def test_request_joining_mid_stream_matches_oracle(tiering):
     """Row 1 joins while row 0 is decoding; its first decode steps (initial
-    selection with its own query, then the batch graph) match the oracle."""
-    eng = _setup(B=2, K=6)
+    selection with its own query, then the batch graph; two-tier: offload
+    after prefill, eviction after the initial selection, reranks fetching
+    promoted pages) match the oracle."""
+    eng = _setup(B=2, K=6, tiering=tiering)
     L, H, G, D = eng.L, eng.H, eng.G, eng.D
     rng = np.random.default_rng(3)
     eng.start_serving()
@@ -74,7 +77,7 @@ def test_request_joining_mid_stream_matches_oracle():
         v = O.bf16_round(rng.standard_normal((L, H, T, D)))
         prompts[row] = [k, v]
     eng.admit(0, torch.as_tensor(prompts[0][0]).cuda().bfloat16(), torch.as_tensor(prompts[0][1]).cuda().bfloat16())
-    for step in range(7):
+    for step in range(10):
         if step == 3:
             eng.admit(1, torch.as_tensor(prompts[1][0]).cuda().bfloat16(),
                       torch.as_tensor(prompts[1][1]).cuda().bfloat16())
@@ -109,3 +112,48 @@ def test_request_joining_mid_stream_matches_oracle():
     eng.retire(1)
     torch.cuda.synchronize()
     assert eng.store.free_count() == eng.store.n_blocks - 1
+
+
+def test_tiered_serving_admits_more_requests():
+    """Two-tier serving: FlexiCache's commit (stable heads keep their
+    selection) admits more requests into the same pool than the
+    all-resident commit; requests finish, the pool and the slow-tier ledger
+    are released, no device error."""
+    from paper_2511_00868_b200.engine import DecodeEngine
+    from paper_2511_00868_b200.serving import Request, ServingLoop
+    from paper_2511_00868_b200.stability import HeadProfile
+    B, L, H, G, D, K, R = 4, 2, 4, 4, 128, 6, 4
+    T = 1600
+    per_req_dense = ((T + 20) // PS + 1) * L * H
+    n_blocks = 2 * per_req_dense + 1          # all-resident: two requests at a time
+    peaks = {}
+    for tiering in (False, True):
+        eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=T + 64,
+                           topk_pages=K, rerank_period=R, profile=HeadProfile.first_n(L, H, 0.25),
+                           n_blocks=n_blocks, tiering=tiering)
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(9)
+
+        def make_prompt(req):
+            g = torch.Generator(device="cuda")
+            g.manual_seed(77 + req.id)
+            k = torch.randn((L, H, req.prompt_tokens, D), generator=g, device="cuda").bfloat16()
+            v = torch.randn((L, H, req.prompt_tokens, D), generator=g, device="cuda").bfloat16()
+            return k, v
+
+        def feed(e):
+            e.q.normal_(generator=gen)
+            e.k_new.normal_(generator=gen)
+            e.v_new.normal_(generator=gen)
+
+        reqs = [Request(i, 0.0, T, 12 + 4 * i) for i in range(6)]
+        m = ServingLoop(eng, reqs, make_prompt, feed).run()
+        torch.cuda.synchronize()
+        eng.store.check_errors()
+        assert m.finished == len(reqs)
+        assert eng.store.free_count() == eng.store.n_blocks - 1
+        if tiering:
+            assert eng.tier.slow_bytes_used == 0 and not eng.tier._counts
+            assert int(eng.fetched_pages.item()) > 0
+        peaks[tiering] = m.peak_batch
+    assert peaks[False] == 2 and peaks[True] > 2

@@ -23,6 +23,7 @@ class _Engine:
 
     def __init__(self, B, L, H, n_blocks):
         self.B, self.L, self.H = B, L, H
+        self.tiering = False
         self.store = _Store(n_blocks)
         self.rows = {}
         self.steps = 0
