@@ -149,7 +149,18 @@ int fc_score_select(const fc_store *s, int layer, const void *q, const uint8_t *
     if (!q || !unstable || !scores_out || !counters) return invalid("null buffer");
     if (s->pages_cap > kMaxPagesCap) return FC_E_CAPACITY;  /* block_select keys <= 48*256 */
     if (batch == 0) return FC_OK;
-    return cuda_status(launch_score(make_view(s), s->dtype, layer, q, unstable, period, force_due, topk,
+    const StoreView v = make_view(s);
+    if (score_attend_supported(v, s->dtype, batch) > 1) {
+        // small batches: a cluster of CTAs per head (the fused kernel's scoring
+        // half: keys meet in rank 0's shared memory, rank 0 selects)
+        AttnArgs a = {};
+        a.layer = layer;
+        a.out = nullptr;
+        return cuda_status(launch_score_attend(v, s->dtype, layer, q, unstable, period, force_due, topk,
+                                               extra_tokens, scores_out, batch, kv_prefetch ? 1 : 0, a,
+                                               (cudaStream_t)stream));
+    }
+    return cuda_status(launch_score(v, s->dtype, layer, q, unstable, period, force_due, topk,
                                     extra_tokens, scores_out, counters, 1, batch, kv_prefetch ? 1 : 0,
                                     (cudaStream_t)stream));
 }

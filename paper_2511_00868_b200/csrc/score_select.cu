@@ -887,6 +887,7 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
     if (st == 2 && rank == 0) score_head_select<NWS * 32>(s, keys, n_cand, topk, hx);
     if constexpr (CL) cg::this_cluster().sync();  // the selection (global) is visible to every rank
     else __syncthreads();                         // selection written by this CTA; scoring smem free
+    if (a.out == nullptr) return;                 // scoring only (fc_score_select at small batches)
     const bool attends = (int)(threadIdx.x >> 5) < NWA;
     if constexpr (NWS > NWA) {
         if (!attends) {
