@@ -74,6 +74,9 @@ def parse():
                          "at config 2's model shape; prints serving metrics, not the headline metric")
     ap.add_argument("--tiered", action="store_true",
                     help="with --serve: the two-tier engine (pinned-host slow tier, FlexiCache admission)")
+    ap.add_argument("--query-rho", type=float, default=0.0,
+                    help="with --serve: decode queries follow q_t = rho q_(t-1) + sqrt(1-rho^2) eps per row "
+                         "(0: independent N(0,1) every step — every rerank re-selects almost every page)")
     ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=2,
                     help="2: the metric's config (default); 3: long generation with host offload; "
                          "4: 128k ctx, 64 requests request-parallel (per-GPU share); "
@@ -687,11 +690,20 @@ def run_serve(args):
         v = torch.randn((L, H, req.prompt_tokens, D), generator=g, device=dev, dtype=torch.bfloat16)
         return k, v
 
+    rho = float(getattr(args, "query_rho", 0.0))
+    noise = torch.empty_like(eng.q)
+
     def feed(e):
-        e.q.normal_(generator=gen)
+        if rho > 0:  # temporally correlated queries: selections drift between reranks
+            noise.normal_(generator=gen)
+            e.q.mul_(rho).add_(noise, alpha=(1 - rho * rho) ** 0.5)
+        else:
+            e.q.normal_(generator=gen)
         e.k_new.normal_(generator=gen)
         e.v_new.normal_(generator=gen)
 
+    if rho > 0:
+        eng.q.normal_(generator=gen)
     loop = ServingLoop(eng, reqs, make_prompt, feed)
     m = loop.run()
     line = {"metric": "serving: decode tokens/s, TTFT, TPOT (continuous batching, device-timed)",
@@ -699,7 +711,7 @@ def run_serve(args):
             "higher_is_better": True, "dtype": "bf16", "data": "synthetic N(0,1) prompts and decode inputs",
             "config": {"workload": "config2 model shape, 48 requests, prompts 8k-32k, outputs 32-256, "
                                    "arrivals every 2 ms, 16 rows, pool for 12 requests at their largest",
-                       "ctx_cap": cap, "tiered": bool(args.tiered)},
+                       "ctx_cap": cap, "tiered": bool(args.tiered), "query_rho": rho},
             "metrics": {f: getattr(m, f) for f in m.__dataclass_fields__}}
     print(json.dumps(line), flush=True)
 

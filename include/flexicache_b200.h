@@ -295,6 +295,20 @@ int fc_rerank_recycle(const fc_store *s, int layer, const int32_t *old_sel,
                       int extra_tokens, const uint8_t *slow_resident,
                       int32_t *copies, int max_copies, int32_t *n_copies,
                       void *workspace, int batch, void *stream);
+/* fc_rerank_recycle with an optional per-row mask row_skip [B_cap] uint8:
+ * rows with row_skip[b] != 0 are treated as not due (no diff, no copies).
+ * The serving loop sets it for requests whose post-prefill offload is still
+ * in flight: they hold every page, so their resident set is not their old
+ * selection (tiering.py:122-139 runs that offload in the background;
+ * simulator.py:389-408 releases the pages only when it finishes).
+ * row_skip = NULL is fc_rerank_recycle. */
+int fc_rerank_recycle_rows(const fc_store *s, int layer, const int32_t *old_sel,
+                           const int32_t *n_old, const uint8_t *unstable,
+                           int period, int force_due, int old_has_tail,
+                           int extra_tokens, const uint8_t *slow_resident,
+                           const uint8_t *row_skip, int32_t *copies,
+                           int max_copies, int32_t *n_copies,
+                           void *workspace, int batch, void *stream);
 
 /* Copy promoted pages from the pinned host slow tier into their HBM blocks:
  * copies [n][4] = (row, head, logical page, dest block) for layer `layer`;
@@ -353,6 +367,11 @@ int fc_stage_clear(const fc_store *s, int32_t *staged_map,
  * (TierStore._record write-once ledger, tiering.py:99-157). */
 int fc_offload_pages(const fc_store *s, void *host_pages, const int32_t *pages,
                      int n_pages, void *stream);
+/* fc_offload_pages on at most max_ctas CTAs (0 = as many as fill the GPU):
+ * a background offload that leaves the other SMs to decode steps running
+ * concurrently on another stream (the post-prefill offload in serving). */
+int fc_offload_pages_ctas(const fc_store *s, void *host_pages, const int32_t *pages,
+                          int n_pages, int max_ctas, void *stream);
 
 /* Per-step incremental offload of stable heads (tiering.py:141-157, driven
  * as simulator._append_token, simulator.py:467-477): for rows [0, batch)

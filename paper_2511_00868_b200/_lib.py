@@ -75,8 +75,10 @@ _SIGNATURES = {
                                      _p, _sz, _i, _p]),
     "fc_rerank_workspace_size": (_sz, [_p]),
     "fc_rerank_recycle": (_i, [_p, _i, _p, _p, _p, _i, _i, _i, _i, _p, _p, _i, _p, _p, _i, _p]),
+    "fc_rerank_recycle_rows": (_i, [_p, _i, _p, _p, _p, _i, _i, _i, _i, _p, _p, _p, _i, _p, _p, _i, _p]),
     "fc_fetch_pages": (_i, [_p, _i, _p, _p, _p, _i, _p]),
     "fc_offload_pages": (_i, [_p, _p, _p, _i, _p]),
+    "fc_offload_pages_ctas": (_i, [_p, _p, _p, _i, _i, _p]),
     "fc_fetch_pages_staged": (_i, [_p, _i, _p, _p, _p, _i, _p, _p, _p, _p]),
     "fc_stage_promoted": (_i, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _i, _p, _i, _p]),
     "fc_stage_clear": (_i, [_p, _p, _p, _p, _i, _p]),

@@ -331,6 +331,15 @@ int fc_rerank_recycle(const fc_store *s, int layer, const int32_t *old_sel, cons
                       const uint8_t *unstable, int period, int force_due, int old_has_tail,
                       int extra_tokens, const uint8_t *slow_resident, int32_t *copies, int max_copies, int32_t *n_copies,
                       void *workspace, int batch, void *stream) {
+    return fc_rerank_recycle_rows(s, layer, old_sel, n_old, unstable, period, force_due, old_has_tail, extra_tokens,
+                                  slow_resident, nullptr, copies, max_copies, n_copies, workspace, batch, stream);
+}
+
+int fc_rerank_recycle_rows(const fc_store *s, int layer, const int32_t *old_sel, const int32_t *n_old,
+                           const uint8_t *unstable, int period, int force_due, int old_has_tail,
+                           int extra_tokens, const uint8_t *slow_resident, const uint8_t *row_skip,
+                           int32_t *copies, int max_copies, int32_t *n_copies, void *workspace, int batch,
+                           void *stream) {
     FC_CHECK(check_store(s));
     if (layer < 0 || layer >= s->layers) return invalid("layer out of range");
     if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
@@ -340,8 +349,8 @@ int fc_rerank_recycle(const fc_store *s, int layer, const int32_t *old_sel, cons
     if (s->sel_cap > 1024) return FC_E_CAPACITY;
     if (batch == 0) return FC_OK;
     return cuda_status(launch_rerank(make_view(s), layer, old_sel, n_old, unstable, period, force_due,
-                                     old_has_tail, extra_tokens, slow_resident, copies, max_copies, n_copies, workspace, batch,
-                                     (cudaStream_t)stream));
+                                     old_has_tail, extra_tokens, slow_resident, row_skip, copies, max_copies, n_copies,
+                                     workspace, batch, (cudaStream_t)stream));
 }
 
 int fc_fetch_pages(const fc_store *s, int layer, const void *host_pages, const int32_t *copies,
@@ -417,12 +426,19 @@ int fc_stage_clear(const fc_store *s, int32_t *staged_map, const int32_t *stage_
 }
 
 int fc_offload_pages(const fc_store *s, void *host_pages, const int32_t *pages, int n_pages, void *stream) {
+    return fc_offload_pages_ctas(s, host_pages, pages, n_pages, 0, stream);
+}
+
+int fc_offload_pages_ctas(const fc_store *s, void *host_pages, const int32_t *pages, int n_pages, int max_ctas,
+                          void *stream) {
     FC_CHECK(check_store(s));
     if (!host_pages || !pages) return invalid("null buffer");
     if (n_pages < 0) return invalid("n_pages must be >= 0");
+    if (max_ctas < 0) return invalid("max_ctas must be >= 0");
     if (n_pages == 0) return FC_OK;
     const int pb = 2 * s->page_size * s->head_dim * (s->dtype == FC_BF16 ? 2 : 4);
-    return cuda_status(launch_offload(make_view(s), host_pages, pages, n_pages, pb, (cudaStream_t)stream));
+    return cuda_status(launch_offload(make_view(s), host_pages, pages, n_pages, pb, max_ctas,
+                                      (cudaStream_t)stream));
 }
 
 int fc_offload_filled(const fc_store *s, void *host_pages, const uint8_t *unstable, uint8_t *slow_resident,

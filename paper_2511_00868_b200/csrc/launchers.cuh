@@ -79,7 +79,8 @@ cudaError_t launch_trace_overlap(const uint32_t *, const uint32_t *, int, int, i
 int attn_split(const StoreView &, int, int, int, int);
 size_t rerank_workspace_bytes(const StoreView &);
 cudaError_t launch_rerank(const StoreView &, int, const int32_t *, const int32_t *, const uint8_t *, int,
-                          int, int, int, const uint8_t *, int32_t *, int, int32_t *, void *, int, cudaStream_t);
+                          int, int, int, const uint8_t *, const uint8_t *, int32_t *, int, int32_t *, void *, int,
+                          cudaStream_t);
 cudaError_t launch_fetch(const StoreView &, int, const void *, const int32_t *, const int32_t *, int, int,
                          const int32_t *, const void *, int32_t *, cudaStream_t);
 cudaError_t launch_stage(const StoreView &, const int32_t *, const int32_t *, const uint8_t *, const uint8_t *,
@@ -89,7 +90,7 @@ cudaError_t launch_stage_plan(const StoreView &, const int32_t *, const int32_t 
 cudaError_t launch_stage_fetch(const StoreView &, const void *, const int32_t *, const int32_t *, int, void *, int,
                                int, cudaStream_t);
 cudaError_t launch_stage_clear(const StoreView &, int32_t *, const int32_t *, int32_t *, int, cudaStream_t);
-cudaError_t launch_offload(const StoreView &, void *, const int32_t *, int, int, cudaStream_t);
+cudaError_t launch_offload(const StoreView &, void *, const int32_t *, int, int, int, cudaStream_t);
 cudaError_t launch_offload_filled(const StoreView &, void *, const uint8_t *, uint8_t *, int, int, cudaStream_t);
 cudaError_t launch_evict_unselected(const StoreView &, const uint8_t *, int, int, cudaStream_t);
 

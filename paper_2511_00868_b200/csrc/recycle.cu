@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(kRecycleWarps * 32)
 rerank_diff_kernel(StoreView s, int layer, const int32_t *__restrict__ old_sel,
                    const int32_t *__restrict__ n_old_arr, const uint8_t *__restrict__ unstable,
                    int period, int force_due, int old_has_tail, int extra_tokens,
-                   const uint8_t *__restrict__ slow_resident,
+                   const uint8_t *__restrict__ slow_resident, const uint8_t *__restrict__ row_skip,
                    int32_t *copies, int max_copies, int32_t *n_copies, RerankWs ws, int batch) {
     // per warp: old list | new list | old blocks | evicted | evicted blocks |
     // promoted, sel_cap + slack entries each
@@ -67,7 +67,10 @@ rerank_diff_kernel(StoreView s, int layer, const int32_t *__restrict__ old_sel,
     if (bh >= batch * s.H) return;
     const int b = bh / s.H, h = bh % s.H;
     int32_t *cnt = ws.cnt(bh);
-    const bool due = !unstable[layer * s.H + h] && (force_due || (*s.step % period == 0));
+    // rows in row_skip still hold every page (post-prefill offload in flight):
+    // their resident set is not the old selection, so nothing moves
+    const bool due = !unstable[layer * s.H + h] && (force_due || (*s.step % period == 0)) &&
+                     !(row_skip && row_skip[b]);
     if (!due) {
         if (lane == 0) { cnt[0] = 0; cnt[1] = 0; }
         return;
@@ -454,8 +457,9 @@ size_t rerank_workspace_bytes(const StoreView &s) {
 
 cudaError_t launch_rerank(const StoreView &s, int layer, const int32_t *old_sel, const int32_t *n_old,
                           const uint8_t *unstable, int period, int force_due, int old_has_tail,
-                          int extra_tokens, const uint8_t *slow_resident, int32_t *copies, int max_copies,
-                          int32_t *n_copies, void *workspace, int batch, cudaStream_t st) {
+                          int extra_tokens, const uint8_t *slow_resident, const uint8_t *row_skip,
+                          int32_t *copies, int max_copies, int32_t *n_copies, void *workspace, int batch,
+                          cudaStream_t st) {
     RerankWs ws{reinterpret_cast<int32_t *>(workspace)};
     const int heads = batch * s.H;
     const size_t smem = (size_t)kRecycleWarps * 6 * (s.SELCAP + kRecycleSlack) * sizeof(int32_t);
@@ -466,8 +470,8 @@ cudaError_t launch_rerank(const StoreView &s, int layer, const int32_t *old_sel,
     }
     cudaError_t e = launch_pdl(rerank_diff_kernel, dim3((heads + kRecycleWarps - 1) / kRecycleWarps),
                                dim3(kRecycleWarps * 32), smem, st, s, layer, old_sel, n_old, unstable, period,
-                               force_due, old_has_tail, extra_tokens, slow_resident, copies, max_copies, n_copies,
-                               ws, batch);
+                               force_due, old_has_tail, extra_tokens, slow_resident, row_skip, copies, max_copies,
+                               n_copies, ws, batch);
     if (e != cudaSuccess) return e;
     return launch_pdl(rerank_commit_kernel, dim3(1), dim3(1024), 0, st, s, layer, copies, max_copies, n_copies, ws,
                       batch);
@@ -541,8 +545,8 @@ cudaError_t launch_evict_unselected(const StoreView &s, const uint8_t *unstable,
 }
 
 cudaError_t launch_offload(const StoreView &s, void *host_pages, const int32_t *pages, int n,
-                           int page_bytes, cudaStream_t st) {
-    const int grid = max(1, min(n, 148 * 8));
+                           int page_bytes, int max_ctas, cudaStream_t st) {
+    const int grid = max(1, min(n, max_ctas > 0 ? max_ctas : 148 * 8));
     offload_kernel<<<grid, kCopyThreads, 0, st>>>(s, (char *)host_pages, pages, n, page_bytes);
     return cudaGetLastError();
 }

@@ -110,6 +110,16 @@ class DecodeEngine:
             from .tiering import ReloadStager
             self.stager = ReloadStager(self.store, self.tier, self.unstable, topk_pages,
                                        leads=(min(2, max(1, rerank_period - 1)),))
+            # serving (admit): the post-prefill offload runs on a side stream; a
+            # row keeps every page, and reranks skip it (row_skip), until that
+            # copy has finished — then its unselected stable-head pages are
+            # evicted (simulator.py:389-408 releases them at offload end)
+            self.row_skip = torch.zeros(batch, dtype=torch.uint8, device=self.device)
+            self.offload_stream = None
+            self._evict_pending: dict[int, tuple] = {}  # row -> (offload done event, step admitted)
+            self.evict_hold_steps = 0  # test hook: keep an eviction pending at least this many steps
+            # CTAs of that background copy: the rest of the GPU keeps decoding
+            self.offload_ctas = 16
 
     # -- prefill ----------------------------------------------------------------
 
@@ -140,12 +150,43 @@ class DecodeEngine:
         if self.seq_host[row] >= 0:
             raise ValueError(f"row {row} is busy")
         self.prefill(row, keys, values)
-        if self.tiering:  # post-prefill offload of every full stable-head page (tiering.py:122-139)
-            self.tier.offload_after_prefill(row, keys.shape[2] // PAGE_SIZE)
+        if self.tiering:
+            # post-prefill offload of every full stable-head page, in the
+            # background (tiering.py:122-139): decode steps continue meanwhile
+            cur = torch.cuda.current_stream(self.device)
+            if self.offload_stream is None:
+                self.offload_stream = torch.cuda.Stream(self.device)
+            self.offload_stream.wait_stream(cur)
+            with torch.cuda.stream(self.offload_stream):
+                self.tier.offload_after_prefill(row, keys.shape[2] // PAGE_SIZE, self.offload_ctas)
+                done = torch.cuda.Event()
+                done.record()
+            self.row_skip[row] = 1
+            self._evict_pending[row] = (done, self.t)
         self._initial_rows.add(row)
+
+    def eviction_pending(self, row: int) -> bool:
+        """True while ``row`` still holds every page (its post-prefill
+        offload has not finished, or its initial selection is not made)."""
+        return self.tiering and row in self._evict_pending
+
+    def _drain_evictions(self) -> None:
+        # rows whose offload finished and whose initial selection exists keep
+        # only their selection from now on (in stream order before this step)
+        cur = torch.cuda.current_stream(self.device)
+        for row, (done, t0) in list(self._evict_pending.items()):
+            if row in self._initial_rows or self.t - t0 < self.evict_hold_steps or not done.query():
+                continue
+            cur.wait_event(done)
+            self.store.evict_unselected_row(row, self.unstable)
+            self.row_skip[row] = 0
+            del self._evict_pending[row]
 
     def retire(self, row: int) -> None:
         """A finished request: every page of its row back to the free list."""
+        if self.tiering and row in self._evict_pending:  # its blocks may still be read by the offload
+            torch.cuda.current_stream(self.device).wait_event(self._evict_pending.pop(row)[0])
+            self.row_skip[row] = 0
         self.store.free_row(row)
         self.seq_host[row] = -1
         self._initial_rows.discard(row)
@@ -159,9 +200,9 @@ class DecodeEngine:
             for layer in range(self.L):
                 self.store.score_select_row(row, layer, self.q[layer, row], self.unstable, self.R, self.K,
                                             force_due=True, extra_tokens=1)
-            if self.tiering:  # stable heads keep only their selection in HBM
-                self.store.evict_unselected_row(row, self.unstable)
         self._initial_rows.clear()
+        # (two-tier: stable heads keep only their selection once the
+        # post-prefill offload is done, _drain_evictions)
 
     def prefill_layer(self, row: int, layer: int, k: torch.Tensor, v: torch.Tensor,
                       alloc: bool) -> None:
@@ -217,7 +258,7 @@ class DecodeEngine:
                 nc = self.n_copies[layer:layer + 1]
                 st.rerank_recycle(layer, self.old_sel[layer], self.n_old[layer], self.unstable, self.R,
                                   self.copies[layer], nc, self.B, old_has_tail=False, extra_tokens=1,
-                                  slow_resident=self.tier.slow_resident)
+                                  slow_resident=self.tier.slow_resident, row_skip=self.row_skip)
                 if self.stager is not None:
                     self.stager.fetch(layer, self.copies[layer], nc)
                 else:
@@ -286,6 +327,8 @@ class DecodeEngine:
         else:
             if getattr(self, "_initial_rows", None):
                 self._initial_selections()
+            if self.tiering and self._evict_pending:
+                self._drain_evictions()
             if rerank and self.tiering and self.stager is not None:
                 self.stager.wait()  # staged promotions have landed
             if use_graph:

@@ -12,8 +12,10 @@ clock advances by the MEASURED device time of each prefill and decode step
 With a two-tier engine, admission uses FlexiCache's commit (unstable heads
 every page, stable heads their selection, simulator.py:253-266), an
 admitted request's full stable-head pages are offloaded after its prefill
-and evicted after its initial selection, and reranks fetch promoted pages
-(staged ahead, tiering.ReloadStager).  With an all-resident engine the
+on a side stream while decode continues, evicted (and the peak commit
+released) once that copy finished and the initial selection exists — reranks
+leave the row alone until then — and reranks fetch promoted pages (staged
+ahead, tiering.ReloadStager).  With an all-resident engine the
 commit is the request's whole KV (simulator.py:257-258).
 
 Differences from the simulator, by construction:
@@ -63,6 +65,8 @@ class ServingMetrics:
     peak_batch: int = 0
     peak_fast_bytes: int = 0
     decode_steps: int = 0
+    reload_bytes: int = 0
+    promoted_fraction: float = 0.0
 
     def to_text(self) -> str:
         return "".join(f"{f.name} = {getattr(self, f.name)}\n" for f in fields(self))
@@ -108,6 +112,7 @@ class ServingLoop:
         self.now = 0.0
         self.m = ServingMetrics(n_requests=len(requests))
         self._ttft, self._tpot = [], []
+        self._rerank_slots = 0
 
     def _commit_blocks(self, req: Request) -> int:
         n_max = (req.prompt_tokens + req.output_tokens) // PAGE_SIZE + 1
@@ -178,6 +183,14 @@ class ServingLoop:
                     self.now = max(self.now, self.pending[0].arrival_s)
                 continue
             self.feed(eng)
+            if eng.tiering and eng.is_rerank_step():
+                # rerank slots of rows that recycle (simulator.py:532): stable
+                # heads x their target, rows past their post-prefill offload
+                n_stable = self.LH - int(eng.unstable.sum().item())
+                for row, a in active.items():
+                    if not eng.eviction_pending(row):
+                        pages = (eng.seq_host[row] + 1 + PAGE_SIZE - 1) // PAGE_SIZE
+                        self._rerank_slots += n_stable * min(eng.K, pages)
             dt = self.timer(eng.step)
             eng.store.check_errors()
             self.now += dt
@@ -188,7 +201,8 @@ class ServingLoop:
                 a.step_times.append(dt)
                 self.m.output_tokens += 1
                 steady = self._steady_blocks(a.req)
-                if a.commit > steady:  # its first step selected and evicted: the peak is released
+                if a.commit > steady and not eng.eviction_pending(row):
+                    # selected, offloaded and evicted: the peak is released
                     self.committed -= a.commit - steady
                     a.commit = steady
                 if a.emitted >= a.req.output_tokens:
@@ -203,6 +217,10 @@ class ServingLoop:
         m.decode_steps = steps
         m.sim_time_s = self.now
         m.throughput_tokens_per_s = m.output_tokens / self.now if self.now > 0 else 0.0
+        if eng.tiering:  # promoted pages fetched over the host link (simulator.py:535-541, :600)
+            promoted = int(eng.fetched_pages.item())
+            m.reload_bytes = promoted * self.page_bytes
+            m.promoted_fraction = promoted / self._rerank_slots if self._rerank_slots else 0.0
         if self._ttft:
             m.ttft_mean_s = sum(self._ttft) / len(self._ttft)
             m.ttft_p50_s, m.ttft_p95_s, m.ttft_p99_s = (_pct(self._ttft, p) for p in (50, 95, 99))

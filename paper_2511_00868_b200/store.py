@@ -287,13 +287,14 @@ class KVStore:
                        unstable: torch.Tensor, period: int, copies: torch.Tensor,
                        n_copies: torch.Tensor, batch: int, *, force_due: bool = False,
                        old_has_tail: bool = True, extra_tokens: int = 1,
-                       slow_resident: torch.Tensor | None = None) -> None:
+                       slow_resident: torch.Tensor | None = None,
+                       row_skip: torch.Tensor | None = None) -> None:
         ws = self.rerank_workspace()
-        _lib.check(self.lib.fc_rerank_recycle(
+        _lib.check(self.lib.fc_rerank_recycle_rows(
             self.cptr, layer, old_sel.data_ptr(), n_old.data_ptr(), unstable.data_ptr(), period,
-            int(force_due), int(old_has_tail), extra_tokens, _ptr(slow_resident),
+            int(force_due), int(old_has_tail), extra_tokens, _ptr(slow_resident), _ptr(row_skip),
             copies.data_ptr(), copies.shape[0], n_copies.data_ptr(), ws.data_ptr(), batch,
-            self.stream()), "fc_rerank_recycle")
+            self.stream()), "fc_rerank_recycle_rows")
 
     def trace_capture(self, trace_sel: torch.Tensor, trace_pool: torch.Tensor, step_base: int,
                       topk: int, batch: int, extra_tokens: int = 0) -> None:
@@ -413,6 +414,6 @@ class KVStore:
         _lib.check(self.lib.fc_evict_unselected(self.cptr, unstable.data_ptr(), batch, self.stream()),
                    "fc_evict_unselected")
 
-    def offload_pages(self, host_pages: torch.Tensor, pages: torch.Tensor) -> None:
-        _lib.check(self.lib.fc_offload_pages(self.cptr, host_pages.data_ptr(), pages.data_ptr(),
-                                             pages.shape[0], self.stream()), "fc_offload_pages")
+    def offload_pages(self, host_pages: torch.Tensor, pages: torch.Tensor, max_ctas: int = 0) -> None:
+        _lib.check(self.lib.fc_offload_pages_ctas(self.cptr, host_pages.data_ptr(), pages.data_ptr(),
+                                                  pages.shape[0], max_ctas, self.stream()), "fc_offload_pages_ctas")

@@ -14,6 +14,7 @@ latency/bandwidth cost model (tiering.py:29-39) is replaced by measurement.
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from .config import HeadId
@@ -46,47 +47,68 @@ class TierStore:
         self.slow_bytes_used = 0
         self.stable = tuple(profile.stable)
 
-    def _record(self, row: int, head: HeadId, pages) -> list:
-        counts = self._counts.setdefault((row, HeadId(*head)), {})
-        out = []
-        for p in pages:
-            p = int(p)
-            if counts.get(p, 0):
-                raise ConsistencyError(f"page {p} of {head} offloaded twice for request row {row}")
-            counts[p] = 1
-            out.append(p)
-        n_bytes = len(out) * self.page_bytes
+    def _record(self, row: int, head: HeadId, pages) -> np.ndarray:
+        # ledger: per (row, head) a count per logical page (numpy, so a
+        # post-prefill offload of thousands of pages is one vector check)
+        key = (row, HeadId(*head))
+        counts = self._counts.get(key)
+        if counts is None:
+            counts = self._counts[key] = np.zeros(self.store.NCAP, dtype=np.uint8)
+        pages = np.asarray(pages, dtype=np.int64).reshape(-1)
+        if pages.size and (counts[pages].any() or np.bincount(pages, minlength=1).max() > 1):
+            dup = next(int(p) for p in pages if counts[p] or (pages == p).sum() > 1)
+            raise ConsistencyError(f"page {dup} of {head} offloaded twice for request row {row}")
+        n_bytes = int(pages.size) * self.page_bytes
         if self.slow_bytes_used + n_bytes > self.capacity_bytes:
             raise AdmissionError(f"slow tier capacity exceeded: {self.slow_bytes_used + n_bytes} "
                                  f"> {self.capacity_bytes}")
+        counts[pages] = 1
         self.slow_bytes_used += n_bytes
-        return out
+        return pages
 
-    def _offload(self, entries) -> int:
+    def _offload(self, entries, max_ctas: int = 0) -> int:
         if len(entries) == 0:
             return 0
         t = torch.as_tensor(entries, dtype=torch.int32).reshape(-1, 4).to(self.store.device)
-        self.store.offload_pages(self.host, t)
+        self.store.offload_pages(self.host, t, max_ctas)
         r, l, h, p = t.long().unbind(1)
         self.slow_resident[r, l, h, p] = 1
         return t.shape[0] * self.page_bytes
 
-    def offload_after_prefill(self, row: int, full_pages: int) -> int:
-        """One background copy of every full stable-head page (tiering.py:122-139)."""
+    def offload_after_prefill(self, row: int, full_pages: int, max_ctas: int = 0) -> int:
+        """One background copy of every full stable-head page (tiering.py:122-139);
+        ``max_ctas`` bounds the SMs the copy occupies (0: the whole GPU)."""
         if full_pages < 0:
             raise ValueError("full_pages must be non-negative")
         for head in self.stable:
-            if self._counts.get((row, head)):
+            c = self._counts.get((row, head))
+            if c is not None and c.any():
                 raise ConsistencyError(f"request row {row} already ran its post-prefill offload")
-        import numpy as np
-        blocks = []
         for head in self.stable:
-            pages = np.asarray(self._record(row, head, range(full_pages)), dtype=np.int32)
-            if pages.size:
-                e = np.empty((pages.size, 4), dtype=np.int32)
-                e[:, 0], e[:, 1], e[:, 2], e[:, 3] = row, head.layer, head.head, pages
-                blocks.append(e)
-        return self._offload(np.concatenate(blocks) if blocks else [])
+            self._record(row, head, np.arange(full_pages))
+        if full_pages == 0 or not self.stable:
+            return 0
+        # the copy list (row, layer, head, page) built on the device
+        dev = self.store.device
+        if getattr(self, "_stable_dev", None) is None:
+            self._stable_dev = torch.tensor([[h.layer, h.head] for h in self.stable], dtype=torch.int32,
+                                            device=dev)
+            mask = torch.zeros((self.store.L, self.store.H, 1), dtype=torch.bool)
+            for h in self.stable:
+                mask[h.layer, h.head] = True
+            self._stable_mask = mask.to(dev)
+        heads = self._stable_dev
+        n = len(self.stable) * full_pages
+        e = torch.empty((len(self.stable), full_pages, 4), dtype=torch.int32, device=dev)
+        e[..., 0] = row
+        e[..., 1] = heads[:, :1]
+        e[..., 2] = heads[:, 1:]
+        e[..., 3] = torch.arange(full_pages, dtype=torch.int32, device=dev)
+        e = e.view(n, 4)
+        self.store.offload_pages(self.host, e, max_ctas)
+        # (a masked fill: advanced-index assignment would synchronise the stream)
+        self.slow_resident[row, :, :, :full_pages].masked_fill_(self._stable_mask, 1)
+        return n * self.page_bytes
 
     def incremental_offload(self, row: int, head: HeadId, page: int, *, page_full: bool = True) -> int:
         """Copy one page that just became full (tiering.py:141-157)."""
@@ -107,14 +129,15 @@ class TierStore:
         ledger entries and the bytes they held are released; the row may host
         a new request, whose write-once ledger starts empty)."""
         for key in [k for k in self._counts if k[0] == row]:
-            self.slow_bytes_used -= len(self._counts.pop(key)) * self.page_bytes
+            self.slow_bytes_used -= int(self._counts.pop(key).sum()) * self.page_bytes
         self.slow_resident[row].zero_()
 
     def offload_counts(self, row: int, head: HeadId) -> dict:
-        return dict(self._counts.get((row, HeadId(*head)), {}))
+        c = self._counts.get((row, HeadId(*head)))
+        return {} if c is None else {int(p): int(c[p]) for p in np.flatnonzero(c)}
 
     def slow_pages(self, row: int, head: HeadId) -> set:
-        return set(self._counts.get((row, HeadId(*head)), {}))
+        return set(self.offload_counts(row, head))
 
 
 class ReloadStager:

@@ -61,13 +61,17 @@ def test_serving_loop_requests_finish_and_blocks_return():
     assert bool((eng.store.table == 0).all())
 
 
-@pytest.mark.parametrize("tiering", [False, True])
-def test_request_joining_mid_stream_matches_oracle(tiering):
+@pytest.mark.parametrize("tiering,hold", [(False, 0), (True, 0), (True, 6)])
+def test_request_joining_mid_stream_matches_oracle(tiering, hold):
     """Row 1 joins while row 0 is decoding; its first decode steps (initial
     selection with its own query, then the batch graph; two-tier: offload
-    after prefill, eviction after the initial selection, reranks fetching
-    promoted pages) match the oracle."""
+    after prefill on a side stream, eviction once it finished, reranks
+    fetching promoted pages) match the oracle.  hold > 0 keeps each row's
+    eviction pending for that many steps, so reranks (t = 4, 8) run while a
+    row still holds every page (fc_rerank_recycle_rows skips it)."""
     eng = _setup(B=2, K=6, tiering=tiering)
+    if tiering:
+        eng.evict_hold_steps = hold
     L, H, G, D = eng.L, eng.H, eng.G, eng.D
     rng = np.random.default_rng(3)
     eng.start_serving()
@@ -90,6 +94,15 @@ def test_request_joining_mid_stream_matches_oracle(tiering):
         eng.step()
         torch.cuda.synchronize()
         eng.store.check_errors()
+        if tiering and hold:
+            # admitted at t = 1 and t = 4: evicted from t = 7 and t = 10 on
+            assert eng.eviction_pending(0) == (eng.t - 1 < 7)
+            assert eng.eviction_pending(1) == (step >= 3 and eng.t - 1 < 10)
+            if eng.t - 1 >= 7:  # row 0 evicted: stable heads keep only their selection
+                res = (eng.store.table[0] != 0).sum(-1).cpu()
+                ns = eng.store.n_sel[0].cpu()
+                st_mask = ~eng.unstable.bool().cpu().view(eng.L, eng.H)
+                assert bool((res[st_mask] <= ns[st_mask] + 1).all())  # + the next page
         sel, n_sel = eng.store.sel.cpu().numpy(), eng.store.n_sel.cpu().numpy()
         out = eng.out.double().cpu().numpy()
         for row in (0, 1):
