@@ -82,6 +82,11 @@ def _fake_store(**kw):
     (lambda lib, s: lib.fc_stage_plan(s, 64, 64, 64, 64, 64, 64, 64, 0, 1, 0, None), "capacity must be >= 1"),
     (lambda lib, s: lib.fc_stage_fetch(s, 64, 64, 64, 8, 64, 7, None), "pass must be in 0..3"),
     (lambda lib, s: lib.fc_fetch_pages_staged(s, 0, 64, 64, 64, 8, None, 64, None, None), "null buffer"),
+    (lambda lib, s: lib.fc_offload_pages_ctas(s, 64, 64, 4, -1, None), "max_ctas must be >= 0"),
+    (lambda lib, s: lib.fc_rerank_recycle_rows(s, 9, 64, 64, 64, 4, 0, 0, 1, None, 64, 64, 8, 64, 64, 1, None),
+     "layer out of range"),
+    (lambda lib, s: lib.fc_rerank_recycle_rows(s, 0, 64, 64, 64, 0, 0, 0, 1, None, 64, 64, 8, 64, 64, 1, None),
+     "period must be >= 1"),
 ])
 def test_new_entry_points_validate_without_gpu(call, msg):
     lib = _lib.load()
