@@ -225,10 +225,19 @@ def run_ours(args, cfg):
     L, H, G, D = cfg["layers"], cfg["kv_heads"], cfg["group"], cfg["head_dim"]
     B, T, K, R = cfg["batch"], cfg["ctx"], cfg["topk"], cfg["period"]
     prof = HeadProfile.first_n(L, H, cfg["unstable_fraction"], model_id="llama3.1-8b-shaped")
+    if os.environ.get("FC_PROFILE") == "spread":  # profiling knob: the same fraction, spread over every layer
+        from paper_2511_00868_b200.config import HeadId
+        n = round(cfg["unstable_fraction"] * H)
+        prof = HeadProfile(model_id="llama3.1-8b-shaped", n_layers=L, n_heads_per_layer=H, fraction=n / H,
+                           unstable=tuple(HeadId(l, h) for l in range(L) for h in range(n)))
     total_steps = 1 + args.warmup + args.steps + args.warmup + args.steps + 4
     eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D,
                        ctx_cap_tokens=T + total_steps + 16, topk_pages=K, rerank_period=R,
                        profile=prof, dtype=torch.bfloat16, device=dev)
+    if os.environ.get("FC_MIXED") == "0":  # profiling knob: uniform fused launches only
+        eng.mixed_clusters = False
+    if os.environ.get("FC_FUSED") == "0":  # profiling knob: scoring and attention as two launches
+        eng.fused_score_attend = False
     # prefill: 4 distinct random [H, T, d] sources, rotated over (row, layer)
     seed0 = 12345 + 1000 * rank
     srcs = [(device_normal((H, T, D), seed=seed0 + 2 * i, device=dev),
@@ -405,6 +414,11 @@ def run_ours(args, cfg):
                    "rerank_period": R, "unstable_fraction": cfg["unstable_fraction"],
                    "parallelism": f"request-parallel x{world}",
                    "l2": "inputs larger than L2 (5+ GiB touched per step vs 126 MB L2)",
+                   "unstable_heads": ("spread: the first round(u*H) KV heads of every layer"
+                                      if os.environ.get("FC_PROFILE") == "spread" else
+                                      "first round(u*L*H) flat heads (the reference fixture, conftest.py:21-33)"),
+                   **({"mixed_clusters": False} if os.environ.get("FC_MIXED") == "0" else {}),
+                   **({"fused_score_attend": False} if os.environ.get("FC_FUSED") == "0" else {}),
                    **({"share": cfg["share"]} if "share" in cfg else {})},
         "gpu_launches": launches,
         "step_ms": step_stats,

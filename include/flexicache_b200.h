@@ -228,6 +228,28 @@ int fc_score_attend(const fc_store *s, int layer, const void *q,
                     float *scores_out, const void *k_new, const void *v_new,
                     void *out, float *lse, float scale, int attend_appended,
                     int batch, void *stream);
+/* fc_score_attend over an explicit CTA map (mixed clusters): n_ctas CTAs in
+ * clusters of `cluster` (2..16); cta_map [n_ctas] int32 gives each CTA its
+ * (row * kv_heads + head): the `cluster` CTAs of a cluster that all name the
+ * same head split it as fc_score_attend's clusters do; an entry with bit 30
+ * set attends that head alone (scoring and selecting it too when it is due);
+ * -1 leaves the CTA idle.  Every (row, head) in [0, batch * kv_heads) must
+ * appear exactly once (a split cluster counts once).  Results are identical
+ * to fc_score_attend for any such map; the map only balances the work — e.g.
+ * the heads scored this step get a cluster each and the others share
+ * clusters one per CTA, or every head is split and the scored ones are
+ * listed first (clusters start in map order; a grid larger than one wave
+ * runs in waves — clusters never wait on each other).
+ * fc_score_attend_map_fits: 1 when a cluster of `cluster` CTAs of this
+ * kernel fits on the device (n_ctas a multiple of it). */
+int fc_score_attend_map_fits(const fc_store *s, int n_ctas, int cluster);
+int fc_score_attend_map(const fc_store *s, int layer, const void *q,
+                        const uint8_t *unstable, int period, int force_due,
+                        int topk, int extra_tokens, int kv_prefetch,
+                        float *scores_out, const void *k_new,
+                        const void *v_new, void *out, float *lse, float scale,
+                        int attend_appended, int batch, const int32_t *cta_map,
+                        int n_ctas, int cluster, void *stream);
 
 /* Persistent form of fc_sparse_decode for a run of consecutive layers
  * [layer_begin, layer_begin + n_layers) in ONE launch (same semantics per

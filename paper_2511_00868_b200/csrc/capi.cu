@@ -200,6 +200,46 @@ int fc_score_attend(const fc_store *s, int layer, const void *q, const uint8_t *
                                            scores_out, batch, kv_prefetch ? 1 : 0, a, (cudaStream_t)stream));
 }
 
+int fc_score_attend_map_fits(const fc_store *s, int n_ctas, int cluster) {
+    if (check_store(s) != FC_OK || s->pages_cap > kMaxPagesCap) return 0;
+    return score_attend_map_fits(make_view(s), s->dtype, n_ctas, cluster);
+}
+
+int fc_score_attend_map(const fc_store *s, int layer, const void *q, const uint8_t *unstable, int period,
+                        int force_due, int topk, int extra_tokens, int kv_prefetch, float *scores_out,
+                        const void *k_new, const void *v_new, void *out, float *lse, float scale,
+                        int attend_appended, int batch, const int32_t *cta_map, int n_ctas, int cluster,
+                        void *stream) {
+    FC_CHECK(check_store(s));
+    if (layer < 0 || layer >= s->layers) return invalid("layer out of range");
+    if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
+    if (period < 1) return invalid("period must be >= 1");
+    if (topk < 1) return invalid("k must be >= 1");
+    if (topk > s->sel_cap) return FC_E_CAPACITY;
+    if (extra_tokens < 0 || extra_tokens > 1) return invalid("extra_tokens must be 0 or 1");
+    if (!q || !unstable || !scores_out || !out || !cta_map) return invalid("null buffer");
+    if ((k_new == nullptr) != (v_new == nullptr)) return invalid("k_new and v_new go together");
+    if (k_new && extra_tokens != 1) return invalid("fused append needs extra_tokens = 1");
+    if (!(scale > 0.f) || !std::isfinite(scale)) return invalid("scale must be positive");
+    if (cluster < 2 || cluster > 16 || n_ctas < cluster || n_ctas % cluster)
+        return invalid("n_ctas must be a positive multiple of cluster (2..16)");
+    if (s->pages_cap > kMaxPagesCap) return FC_E_CAPACITY;
+    if (batch == 0) return FC_OK;
+    const StoreView v = make_view(s);
+    if (!score_attend_map_fits(v, s->dtype, n_ctas, cluster)) {
+        std::snprintf(g_last_error, sizeof(g_last_error), "mixed clusters do not fit this geometry");
+        return FC_E_UNSUPPORTED;
+    }
+    AttnArgs a = {};
+    a.layer = layer; a.q = q; a.k_new = k_new; a.v_new = v_new; a.out = out; a.lse = lse;
+    a.scale_log2 = scale * 1.4426950408889634f;
+    a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.max_splits = 1;
+    a.cta_map = cta_map; a.map_heads = batch * s->kv_heads;
+    return cuda_status(launch_score_attend_map(v, s->dtype, layer, q, unstable, period, force_due, topk,
+                                               extra_tokens, scores_out, kv_prefetch ? 1 : 0, a, n_ctas, cluster,
+                                               (cudaStream_t)stream));
+}
+
 int fc_score_pages(const fc_store *s, int layer, const void *q, int extra_tokens, float *scores_out, int batch,
                    void *stream) {
     FC_CHECK(check_store(s));

@@ -21,6 +21,10 @@ struct AttnArgs {
     float *part_m;        // [parts][16]
     float *part_l;        // [parts][16]
     float *part_o;
+    // fc_score_attend_map: per CTA a head (bit 30: attends it alone, as a
+    // cluster of one) or -1 (idle); null = CTA i / S attends head i / S
+    const int32_t *cta_map;
+    int map_heads;        // batch * H: bound of the map's head indices
 };
 
 // persistent multi-layer attention (attn_run.cu)
@@ -60,6 +64,9 @@ cudaError_t launch_gather(const StoreView &, int, int, int, int, int, void *, vo
 cudaError_t launch_score(const StoreView &, int, int, const void *, const uint8_t *, int, int, int, int,
                          float *, int32_t *, int, int, int, cudaStream_t);
 int score_attend_supported(const StoreView &, int, int);
+int score_attend_map_fits(const StoreView &, int, int, int);
+cudaError_t launch_score_attend_map(const StoreView &, int, int, const void *, const uint8_t *, int, int, int, int,
+                                    float *, int, const AttnArgs &, int, int, cudaStream_t);
 cudaError_t launch_score_attend(const StoreView &, int, int, const void *, const uint8_t *, int, int, int, int,
                                 float *, int, int, const AttnArgs &, cudaStream_t);
 cudaError_t launch_select(const float *, int, const int32_t *, int, int, int, int32_t *, int32_t *,

@@ -640,12 +640,12 @@ __device__ int score_head_stream(const StoreView &s, int layer, const T *__restr
                                  const uint8_t *__restrict__ unstable, int period, int force_due, int topk,
                                  int extra_tokens, float *scores, int kv_prefetch, char *dsm, uint64_t *full,
                                  uint64_t *empty, int *s_rel, float *w, int bh, int S, int rank,
-                                 uint32_t *keys_dst, int &n_cand_out) {
-    // S > 1: the caller arrived on the cluster barrier at entry; wait on it
-    // before the first write into another CTA's shared memory (a peer may not
-    // have started yet) — and on every other way out
+                                 uint32_t *keys_dst, int &n_cand_out, bool in_cluster = false) {
+    // in a cluster the caller arrived on the cluster barrier at entry; wait on
+    // it before the first write into another CTA's shared memory (a peer may
+    // not have started yet) — and on every other way out
     auto cluster_wait = [&]() {
-        if (S > 1) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (in_cluster) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     };
     using Gm = ScoreGeom<T, D>;
     using HG = HeadScoreGeom<T, D, NWS>;
@@ -873,16 +873,39 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
     // S CTAs (a cluster) per head: every rank scores its share of the pages
     // into rank 0's keys (DSMEM), rank 0 selects, every rank attends its
     // share of the selection, rank 0 merges the ranks' states (DSMEM)
-    const int bh = blockIdx.x / S, rank = blockIdx.x % S;
+    int bh = blockIdx.x / S, rank = blockIdx.x % S, Sh = S;  // head, rank and CTAs on it
+    if constexpr (CL) {
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // waited in the stream
+        if (a.cta_map) {  // mixed clusters (host-written map, read before the PDL wait)
+            const int e = a.cta_map[blockIdx.x];
+            bool idle = e < 0;
+            if (!idle) {
+                bh = e & ~(1 << 30);
+                if (e & (1 << 30)) { Sh = 1; rank = 0; }
+                if (bh >= a.map_heads) { set_error(s.err, FC_ERR_RUN_RANGE); idle = true; }
+            }
+            if (idle) {  // every cluster barrier of the kernel, no work
+                griddep_wait();
+                asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+                cg::this_cluster().sync();
+                cg::this_cluster().sync();
+                if (a.out == nullptr) return;
+                asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+                asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+                return;
+            }
+        }
+    }
     const int b = bh / s.H, h = bh % s.H, hx = s.hix(b, layer, h);
-    if constexpr (CL) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // waited in the stream
     uint32_t *keys = reinterpret_cast<uint32_t *>(dsm + (size_t)HG::kStages * HG::kChunkBytes);
     uint32_t *keys_dst = keys;
-    if constexpr (CL) keys_dst = cg::this_cluster().map_shared_rank(keys, 0);
+    if constexpr (CL) {
+        if (Sh > 1) keys_dst = cg::this_cluster().map_shared_rank(keys, 0);
+    }
     int n_cand = 0;
     const int st = score_head_stream<T, D, NWS>(s, layer, q, unstable, period, force_due, topk, extra_tokens,
-                                                  scores, kv_prefetch, dsm, full, empty, s_rel, w, bh, S, rank,
-                                                  keys_dst, n_cand);
+                                                  scores, kv_prefetch, dsm, full, empty, s_rel, w, bh, Sh, rank,
+                                                  keys_dst, n_cand, CL);
     if constexpr (CL) cg::this_cluster().sync();  // every rank's keys are in rank 0
     if (st == 2 && rank == 0) score_head_select<NWS * 32>(s, keys, n_cand, topk, hx);
     if constexpr (CL) cg::this_cluster().sync();  // the selection (global) is visible to every rank
@@ -907,10 +930,11 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
         attend_head_cta<T, D, NST, NWA>(s, a, bh, dsm, abars, s_wm, s_wl, s_q, 1);
     } else {
         // (only attending warps get here when NWS > NWA)
-        const int n_att = attend_head_cta<T, D, NST, NWA>(s, a, bh, dsm, abars, s_wm, s_wl, s_q, 1, S, rank, cstate);
+        const int n_att = attend_head_cta<T, D, NST, NWA>(s, a, bh, dsm, abars, s_wm, s_wl, s_q, 1, Sh, rank,
+                                                          Sh > 1 ? cstate : nullptr);
         // every rank's state written
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-        if (rank == 0 && n_att > 0) merge_head_cluster<T, D>(s, a, bh, cstate, S, NWA * 32);
+        if (Sh > 1 && rank == 0 && n_att > 0) merge_head_cluster<T, D>(s, a, bh, cstate, Sh, NWA * 32);
         // rank 0 done reading every rank's shared memory
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
@@ -1117,6 +1141,61 @@ static cudaError_t launch_score_attend_t(const StoreView &s, int layer, const vo
                               period, force_due, topk, extra, scores, kv_prefetch, a, 1);
 }
 
+// mixed clusters (fc_score_attend_map): n_ctas CTAs in clusters of S (a
+// cluster of S fits on the device)
+template <typename T, int D, int NST, int NWA, int NWS>
+static int score_attend_map_fits_t(const StoreView &s, int n_ctas, int S) {
+    if (S < 2 || S > 16 || n_ctas < S || n_ctas % S) return 0;
+    if (!score_attend_fits_t<T, D, NST, NWA, NWS, true>(s)) return 0;
+    auto k = score_attend_kernel<T, D, NST, NWA, NWS, true>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(n_ctas);
+    cfg.blockDim = dim3(NWS * 32);
+    cfg.dynamicSmemBytes = score_attend_smem<T, D, NST, NWA, NWS>(s);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = S;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, k, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    // clusters never wait on each other: a grid beyond one wave runs in waves
+    return clusters >= 1;
+}
+
+template <typename T, int D, int NST, int NWA, int NWS>
+static cudaError_t launch_score_attend_map_t(const StoreView &s, int layer, const void *q, const uint8_t *unstable,
+                                             int period, int force_due, int topk, int extra, float *scores,
+                                             int kv_prefetch, const AttnArgs &a, int n_ctas, int S,
+                                             cudaStream_t st) {
+    if (!score_attend_map_fits_t<T, D, NST, NWA, NWS>(s, n_ctas, S)) return cudaErrorInvalidConfiguration;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(n_ctas);
+    cfg.blockDim = dim3(NWS * 32);
+    cfg.dynamicSmemBytes = score_attend_smem<T, D, NST, NWA, NWS>(s);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = S;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, score_attend_kernel<T, D, NST, NWA, NWS, true>, s, layer, (const T *)q,
+                              unstable, period, force_due, topk, extra, scores, kv_prefetch, a, S);
+}
+
 #ifndef FC_SA_SCORE_WARPS
 #define FC_SA_SCORE_WARPS 16
 #endif
@@ -1140,6 +1219,21 @@ cudaError_t launch_score_attend(const StoreView &s, int dtype, int layer, const 
     launch_score_attend_t<T, DD, N, W, WS>(s, layer, q, unstable, period, force_due, topk, extra, scores, batch, kv_prefetch, a, st)
     return FC_SA_DISPATCH(dtype, s.D, FC_SAL);
 #undef FC_SAL
+}
+
+int score_attend_map_fits(const StoreView &s, int dtype, int n_ctas, int S) {
+#define FC_SAM(T, DD, N, W, WS) score_attend_map_fits_t<T, DD, N, W, WS>(s, n_ctas, S)
+    return FC_SA_DISPATCH(dtype, s.D, FC_SAM);
+#undef FC_SAM
+}
+
+cudaError_t launch_score_attend_map(const StoreView &s, int dtype, int layer, const void *q, const uint8_t *unstable,
+                                    int period, int force_due, int topk, int extra, float *scores, int kv_prefetch,
+                                    const AttnArgs &a, int n_ctas, int S, cudaStream_t st) {
+#define FC_SAML(T, DD, N, W, WS) \
+    launch_score_attend_map_t<T, DD, N, W, WS>(s, layer, q, unstable, period, force_due, topk, extra, scores, kv_prefetch, a, n_ctas, S, st)
+    return FC_SA_DISPATCH(dtype, s.D, FC_SAML);
+#undef FC_SAML
 }
 
 void set_score_mode(int m) { g_score_mode = m; }

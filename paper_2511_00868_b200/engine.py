@@ -80,6 +80,12 @@ class DecodeEngine:
         # CTA per head, fc_score_attend) when the batch fills the GPU with
         # heads: 53.4 vs 56.6 us per scored layer at config 2
         self.fused_score_attend = True
+        # plain steps of fused layers: the heads scored every step (unstable)
+        # get a cluster of CTAs each and the others one CTA each, when the
+        # bandwidth model says the uniform split is unbalanced (small batches
+        # at long context: config 4; fc_score_attend_map)
+        self.mixed_clusters = True
+        self._mixed: dict = {}
         # profiling: score every head every step and record
         # the selections on the device (trace.TraceRecorder)
         self.score_all_heads = False
@@ -242,9 +248,11 @@ class DecodeEngine:
             scored = scores(layer)
             if scored and not recycle and use_fused:
                 # one launch: every head's CTA scores, selects and attends
+                plan = self._mixed_plan(layer) if not (rerank or force_due) else None
                 st.score_attend(layer, self.q[layer], self.unstable, self.R, self.K, self.out[layer], self.B,
                                 force_due=force_due, extra_tokens=1, kv_prefetch=layer > 0,
-                                k_new=self.k_new[layer], v_new=self.v_new[layer], attend_appended=False)
+                                k_new=self.k_new[layer], v_new=self.v_new[layer], attend_appended=False,
+                                cta_map=plan[0] if plan else None, cluster=plan[1] if plan else 0)
                 if self.after_layer is not None:
                     self.after_layer(layer)
                 layer += 1
@@ -300,6 +308,18 @@ class DecodeEngine:
             self.recorder.capture()
         if self.tiering:  # write-once offload of the page that just filled
             st.offload_filled(self.tier.host, self.unstable, self.tier.slow_resident, self.B)
+
+    def _mixed_plan(self, layer: int):
+        # heads due at a plain step = the layer's unstable heads; the map is
+        # sized for the current longest row (any map gives the same results)
+        if not self.mixed_clusters:
+            return None
+        if layer not in self._mixed:
+            scored = [h for h in range(self.H) if self.profile.is_unstable(HeadId(layer, h))]
+            n_pages = (max(self.seq_host) + 1 + PAGE_SIZE - 1) // PAGE_SIZE
+            self._mixed[layer] = (self.store.mixed_cluster_map(self.B, scored, n_pages, self.K)
+                                  if scored and n_pages > 0 else None)
+        return self._mixed[layer]
 
     def _use_run(self) -> bool:
         if self.run_kernel is None:
@@ -364,6 +384,9 @@ class DecodeEngine:
     def _capture(self, rerank: bool) -> torch.cuda.CUDAGraph:
         # stream capture records the launches without executing them, so the
         # engine state is untouched; workspaces were sized by the eager first step
+        if not rerank:  # mixed-cluster maps live on the device: build them outside the capture
+            for layer in range(self.L):
+                self._mixed_plan(layer)
         torch.cuda.synchronize(self.device)
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))

@@ -207,14 +207,78 @@ class KVStore:
                      out: torch.Tensor, batch: int, *, force_due: bool = False, extra_tokens: int = 1,
                      kv_prefetch: bool = False, k_new: torch.Tensor | None = None,
                      v_new: torch.Tensor | None = None, lse: torch.Tensor | None = None,
-                     scale: float | None = None, attend_appended: bool = False) -> None:
+                     scale: float | None = None, attend_appended: bool = False,
+                     cta_map: torch.Tensor | None = None, cluster: int = 0) -> None:
         """fc_score_attend: score_select then sparse_decode of one layer, one
-        CTA per head (same results as the two calls)."""
+        CTA per head (same results as the two calls); with ``cta_map`` /
+        ``cluster`` fc_score_attend_map (mixed clusters, mixed_cluster_map)."""
         scale = 1.0 / math.sqrt(self.D) if scale is None else scale
+        if cta_map is not None:
+            _lib.check(self.lib.fc_score_attend_map(
+                self.cptr, layer, q.data_ptr(), unstable.data_ptr(), period, int(force_due), topk, extra_tokens,
+                int(kv_prefetch), self.scores.data_ptr(), _ptr(k_new), _ptr(v_new), out.data_ptr(), _ptr(lse),
+                scale, int(attend_appended), batch, cta_map.data_ptr(), cta_map.numel(), cluster,
+                self.stream()), "fc_score_attend_map")
+            return
         _lib.check(self.lib.fc_score_attend(
             self.cptr, layer, q.data_ptr(), unstable.data_ptr(), period, int(force_due), topk, extra_tokens,
             int(kv_prefetch), self.scores.data_ptr(), _ptr(k_new), _ptr(v_new), out.data_ptr(), _ptr(lse),
             scale, int(attend_appended), batch, self.stream()), "fc_score_attend")
+
+    def score_attend_map_fits(self, n_ctas: int, cluster: int) -> bool:
+        return bool(self.lib.fc_score_attend_map_fits(self.cptr, n_ctas, cluster))
+
+    def mixed_cluster_map(self, batch: int, scored_heads, n_pages: int, topk_pages: int, *,
+                          sms: int | None = None, bw_sm_gbs: float = 90.0, bw_gbs: float = 6000.0):
+        """A CTA map for fc_score_attend_map that balances a launch in which
+        only ``scored_heads`` (kv-head indices of the layer, every row) are
+        scored: each scored head gets a cluster of S CTAs, the other heads
+        one CTA each, S CTAs to a cluster.  Chosen by a bandwidth model (each
+        CTA streams at most ``bw_sm_gbs``, the launch at most ``bw_gbs``);
+        None when the uniform launch (fc_score_attend) models as fast or the
+        mixed grid does not fit.  Returns (map [n_ctas] int32 on the device,
+        cluster)."""
+        if sms is None:
+            sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+        scored = sorted(set(int(h) for h in scored_heads))
+        if not scored:
+            return None
+        n_s = batch * len(scored)
+        n_o = batch * self.H - n_s
+        att = min(n_pages, topk_pages + 2) * self.page_bytes
+        summ = n_pages * 2 * self.D * self.kv_pool.element_size()
+
+        def est(per_cta):
+            total = n_s * (summ + att) + n_o * att
+            return max(per_cta / (bw_sm_gbs * 1e3), total / (bw_gbs * 1e3))  # us
+
+        su = self.score_attend_supported(batch)
+        if su < 1:
+            return None
+        best = None
+        for S in range(2, 17):
+            clusters = n_s + (n_o + S - 1) // S
+            if clusters * S > sms or not self.score_attend_map_fits(clusters * S, S):
+                continue
+            per = max((summ + att) / S, att if n_o else 0)
+            t = (est(per), per)  # ties: the smaller per-CTA share
+            if best is None or t < best[0]:
+                best = (t, S)
+        if best is None or best[0][0] >= 0.9 * est((summ + att) / su):
+            return None
+        S = best[1]
+        m = []
+        others = []
+        for b in range(batch):
+            for h in range(self.H):
+                bh = b * self.H + h
+                if h in scored:
+                    m += [bh] * S
+                else:
+                    others.append(bh | (1 << 30))
+        others += [-1] * (-len(others) % S)
+        m += others
+        return torch.tensor(m, dtype=torch.int32, device=self.device), S
 
     def score_pages(self, layer: int, q: torch.Tensor, batch: int, *, extra_tokens: int = 0) -> None:
         _lib.check(self.lib.fc_score_pages(self.cptr, layer, q.data_ptr(), extra_tokens,

@@ -240,3 +240,87 @@ def test_fused_one_cta_bitwise_equal_to_two_launches():
             assert torch.equal(x, y)
     finally:
         lib.fc_debug_score_mode(-1)
+
+
+@pytest.mark.parametrize("force_due", [False, True])
+def test_fused_mixed_clusters_match_uniform(force_due):
+    """fc_score_attend_map (mixed clusters: scored heads split over a cluster,
+    the others one CTA each, idle padding CTAs) against the uniform one-CTA
+    launch: selections identical, outputs of heads attended alone
+    bit-identical, split heads within bf16 rounding, LSE within fp32
+    rounding.  force_due: every head is scored, so heads attended alone also
+    score and select alone."""
+    import ctypes
+    from paper_2511_00868_b200 import _lib
+    from paper_2511_00868_b200.engine import DecodeEngine
+    from paper_2511_00868_b200.stability import HeadProfile
+    from paper_2511_00868_b200.synthetic import device_normal
+    lib = _lib.load()
+    lib.fc_debug_score_mode.argtypes = [ctypes.c_int]
+    B, L, H, G, D, T, K = 2, 1, 8, 4, 128, 6000, 32
+    eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=T + 64,
+                       topk_pages=K, rerank_period=4, profile=HeadProfile.first_n(L, H, 0.25))
+    for b in range(B):
+        eng.prefill_layer(b, 0, device_normal((H, T + 11 * b, D), seed=b),
+                          device_normal((H, T + 11 * b, D), seed=50 + b), alloc=True)
+    st = eng.store
+    st.step.fill_(1)  # a plain step: only the unstable heads are due unless forced
+    unstable = [h for h in range(H) if eng.unstable.view(L, H)[0, h].item()]
+    assert len(unstable) == 2
+    q = device_normal(tuple(eng.q[0].shape), seed=7)
+
+    def run(cta_map=None, cluster=0):
+        out = torch.zeros_like(eng.out[0])
+        lse = torch.zeros(B * H * G, dtype=torch.float32, device=q.device)
+        st.sel.zero_()
+        st.n_sel.zero_()
+        st.score_attend(0, q, eng.unstable, 4, K, out, B, force_due=force_due, extra_tokens=1, lse=lse,
+                        cta_map=cta_map, cluster=cluster)
+        torch.cuda.synchronize()
+        st.check_errors()
+        return st.sel.clone(), st.n_sel.clone(), out, lse
+
+    lib.fc_debug_score_mode(1)  # uniform reference: one CTA per head
+    try:
+        ref = run()
+    finally:
+        lib.fc_debug_score_mode(-1)
+    S = 4
+    split, alone = [], []
+    for b in range(B):
+        for h in range(H):
+            (split if h in unstable else alone).append(b * H + h)
+    m = [bh for bh in split for _ in range(S)] + [bh | (1 << 30) for bh in alone]
+    m += [-1] * (-len(m) % S) + [-1] * S  # padding and one idle cluster
+    assert st.score_attend_map_fits(len(m), S)
+    got = run(torch.tensor(m, dtype=torch.int32, device="cuda"), S)
+    assert torch.equal(got[0], ref[0]) and torch.equal(got[1], ref[1])
+    o_ref, o_got = ref[2].view(B, H, G, D), got[2].view(B, H, G, D)
+    for bh in alone:
+        assert torch.equal(o_got[bh // H, bh % H], o_ref[bh // H, bh % H]), bh
+    for bh in split:
+        a, r = o_got[bh // H, bh % H].float(), o_ref[bh // H, bh % H].float()
+        assert ((a - r).norm() / r.norm()).item() < 1e-2, bh
+    assert torch.allclose(got[3], ref[3], rtol=1e-5, atol=1e-5)
+
+
+def test_mixed_cluster_map_plan():
+    """The engine's plan for a small batch at long context: every head
+    appears once, scored heads split over whole clusters, the grid fits."""
+    from paper_2511_00868_b200.store import KVStore
+    st = KVStore(batch_cap=8, layers=1, kv_heads=8, group=4, head_dim=128, pages_cap=8200, n_blocks=64,
+                 sel_cap=140, dtype=torch.bfloat16, device="cuda")
+    plan = st.mixed_cluster_map(8, [0, 1], 8192, 128)
+    assert plan is not None
+    m, S = plan
+    m = m.cpu().tolist()
+    assert len(m) % S == 0 and st.score_attend_map_fits(len(m), S)
+    heads = [e & ~(1 << 30) for e in m if e >= 0]
+    split = [e for e in m if e >= 0 and not e & (1 << 30)]
+    assert sorted(set(heads)) == list(range(64))
+    assert sorted(set(split)) == sorted(b * 8 + h for b in range(8) for h in (0, 1))
+    assert all(split.count(e) == S for e in set(split))
+    # config 2's shape (16 rows, 2 kv heads of 8 scored): no mixed grid fits one wave
+    st2 = KVStore(batch_cap=16, layers=1, kv_heads=8, group=4, head_dim=128, pages_cap=2100, n_blocks=64,
+                  sel_cap=140, dtype=torch.bfloat16, device="cuda")
+    assert st2.mixed_cluster_map(16, [0, 1], 2048, 128) is None
