@@ -495,7 +495,7 @@ FC_DEVINL int attend_head_cta(const StoreView &s, const AttnArgs &a, int bh, cha
         }
         __syncwarp();
         if (lane == 0 && ni < n_e) {
-            fence_proxy_async_smem();
+            if (FC_REFILL_FENCE) fence_proxy_async_smem();
             if (nblk > 0) {
                 mbar_arrive_expect_tx(&mybars[stg], Gm::kPageBytes);
                 bulk_g2s(myring + (size_t)stg * Gm::kPageBytes, pool + (int64_t)nblk * Gm::kPageBytes,

@@ -71,6 +71,11 @@ FC_DEVINL void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// proxy fence before a ring stage is refilled by a bulk copy (profiling knob)
+#ifndef FC_REFILL_FENCE
+#define FC_REFILL_FENCE 1
+#endif
+
 FC_DEVINL void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

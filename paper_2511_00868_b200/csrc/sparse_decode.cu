@@ -192,7 +192,7 @@ attn_kernel(StoreView s, AttnArgs a, int S) {
                 bulk_prefetch_l2(pool + (int64_t)pblk * Gm::kPageBytes, Gm::kPageBytes);
         }
         if (lane == 0 && ni < n_e) {
-            fence_proxy_async_smem();
+            if (FC_REFILL_FENCE) fence_proxy_async_smem();
             if (nblk > 0) {
                 mbar_arrive_expect_tx(&mybars[stg], Gm::kPageBytes);
                 bulk_page(myring + (size_t)stg * Gm::kPageBytes, pool + (int64_t)nblk * Gm::kPageBytes,
@@ -455,7 +455,7 @@ attn_bal_kernel(StoreView s, AttnArgs a, int n_heads) {
         }
         __syncwarp();
         if (lane == 0 && ni < n_e) {
-            fence_proxy_async_smem();
+            if (FC_REFILL_FENCE) fence_proxy_async_smem();
             if (nblk > 0) {
                 mbar_arrive_expect_tx(&mybars[stg], Gm::kPageBytes);
                 bulk_page(myring + (size_t)stg * Gm::kPageBytes, pool + (int64_t)nblk * Gm::kPageBytes,
