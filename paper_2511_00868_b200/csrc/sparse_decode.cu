@@ -180,7 +180,9 @@ attn_kernel(StoreView s, AttnArgs a, int S) {
             if (last && a.k_new != nullptr)
                 tp.apply(s, stage, reinterpret_cast<T *>(s.pool) + s.block_off(blk), tok_slot, hd.hx,
                          hd.n_pages - 1, lane);
+#ifndef FC_SKIP_PAGE_MATH  // profiling knob: the page pipeline without the math
             st.page(stage, page_is_last ? last_fill : kPageSize, a.scale_log2, lane);
+#endif
         }
         __syncwarp();
         if constexpr (FC_L2_PREFETCH > 0) {
