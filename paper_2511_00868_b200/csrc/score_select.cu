@@ -685,7 +685,10 @@ __device__ int score_head_stream(const StoreView &s, int layer, const T *__restr
     uint32_t *keys = keys_dst + c0;
     const char *base = reinterpret_cast<const char *>(s.summ) + ((int64_t)hx * s.NCAP + c0) * Gm::kRecBytes;
     if (tid == 0) {
-        for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], NW); s_rel[i] = 0; }
+        // every consuming thread arrives on `empty` (its own reads precede its
+        // arrival; a per-warp arrival after __syncwarp is ordered the same way
+        // but racecheck only credits the arriving thread)
+        for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], NW * 32); s_rel[i] = 0; }
         fence_mbar_init();
         for (int c = 0; c < min(NS, n_chunks); ++c) {
             const uint32_t bytes = min(kHeadChunkPages, n_cand - c * kHeadChunkPages) * Gm::kRecBytes;
@@ -743,7 +746,7 @@ __device__ int score_head_stream(const StoreView &s, int layer, const T *__restr
             }
         }
 #else
-        if (lane == 0) mbar_arrive(&empty[stg]);  // this warp is done reading the stage
+        mbar_arrive(&empty[stg]);  // this thread is done reading the stage
 #endif
         // transpose-reduce R values over LPP lanes
         int ridx = 0;
