@@ -694,6 +694,9 @@ def run_serve(args):
     eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=cap, topk_pages=K,
                        rerank_period=R, profile=prof, dtype=torch.bfloat16, device=dev, n_blocks=n_blocks,
                        tiering=args.tiered)
+    if args.tiered and os.environ.get("FC_STAGE_LEAD"):  # profiling knob: staging lead(s) in steps
+        eng.stager.leads = tuple(int(x) for x in os.environ["FC_STAGE_LEAD"].split(","))
+        eng.stager.lead = eng.stager.leads[0]
     gen = torch.Generator(device=dev)
     gen.manual_seed(11)
 
