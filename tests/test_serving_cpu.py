@@ -84,3 +84,68 @@ def test_idle_until_arrival_and_ttft():
     assert m.finished == 1
     assert abs(m.ttft_mean_s - 0.05) < 1e-12          # arrives at 1.0, prefilled by 1.05
     assert abs(m.sim_time_s - (1.0 + 0.05 + 0.01)) < 1e-12
+
+
+class _TieredEngine(_Engine):
+    """Two-tier stand-in: a request's post-prefill offload takes `lag` steps;
+    its eviction (and the loop's release of the peak commit) waits for it."""
+
+    def __init__(self, B, L, H, n_blocks, lag):
+        super().__init__(B, L, H, n_blocks)
+        self.tiering = True
+        self.K, self.R = 2, 4
+        self.lag = lag
+        self.pending = {}
+        self.seq_host = [-1] * B
+        import torch
+        self.unstable = torch.zeros(L * H, dtype=torch.uint8)
+        self.fetched_pages = torch.zeros(1, dtype=torch.int64)
+        self.commit_log = []
+
+    def admit(self, row, keys, values):
+        super().admit(row, keys, values)
+        self.pending[row] = self.steps + self.lag
+        self.seq_host[row] = keys
+
+    def retire(self, row):
+        super().retire(row)
+        self.pending.pop(row, None)
+        self.seq_host[row] = -1
+
+    def eviction_pending(self, row):
+        return row in self.pending
+
+    def is_rerank_step(self):
+        return (self.steps + 1) % self.R == 0
+
+    def step(self):
+        super().step()
+        for row, t in list(self.pending.items()):
+            if self.steps >= t:
+                del self.pending[row]
+
+
+def test_tiered_peak_commit_held_until_offload_lands():
+    """FlexiCache commit: the peak (whole prompt) stays committed while the
+    post-prefill offload is in flight and drops to the steady commit after
+    (simulator.py:389-408); a second request that only fits at steady state
+    is admitted only then."""
+    from paper_2511_00868_b200.serving import ServingLoop
+    eng = _TieredEngine(2, 2, 2, n_blocks=10_000, lag=3)
+    reqs = [Request(0, 0.0, 320, 12), Request(1, 0.0, 320, 4)]
+    loop = ServingLoop(eng, reqs, make_prompt=lambda r: (r.prompt_tokens, r.prompt_tokens),
+                       feed=lambda e: None, timer=lambda fn: (fn(), 0.01)[1])
+    peak, steady = loop._commit_blocks(reqs[0]), loop._steady_blocks(reqs[0])
+    assert peak > steady
+    loop.capacity = peak + steady  # both fit only once the first is at its steady commit
+    admitted_at = {}
+    orig_admit = eng.admit
+
+    def admit(row, keys, values):
+        admitted_at[row] = eng.steps
+        orig_admit(row, keys, values)
+    eng.admit = admit
+    m = loop.run()
+    assert m.finished == 2
+    assert admitted_at[0] == 0 and admitted_at[1] >= eng.lag  # waited for request 0's offload
+    assert loop.committed == 0
