@@ -122,7 +122,7 @@ attn_persist_kernel(StoreView s, RunArgs a, int S) {
     };
     pump();
 
-    typename std::conditional<sizeof(T) == 2, Bf16Warp<D>, F32Warp<D>>::type st;
+    typename std::conditional<sizeof(T) == 2, Bf16Attn<D>, F32Warp<D>>::type st;
     for (int li = 0; li < a.nl; ++li) {
         const int l = a.l0 + li;
         const bool tr = trace != nullptr && tid == 0 && li < 32;

@@ -352,7 +352,7 @@ attn_run_kernel(StoreView s, RunArgs a) {
     pump(0);
     if (trace && lane == 0) trace[32 * 8 + 1] = run_gtimer();
 
-    typename std::conditional<sizeof(T) == 2, Bf16Warp<D>, F32Warp<D>>::type st;
+    typename std::conditional<sizeof(T) == 2, Bf16Attn<D>, F32Warp<D>>::type st;
     for (int li = 0; li < a.nl; ++li) {
         const int l = a.l0 + li;
         const RunPlan P = (li & 1) ? pl[1] : pl[0];

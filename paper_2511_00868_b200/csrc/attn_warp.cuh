@@ -177,6 +177,160 @@ struct Bf16Warp {
     }
 };
 
+// bf16 tensor-core path with the page's 16 tokens as the MMA M dimension and
+// the query group as N (G <= 8): S^T = K q^T is 8 HMMAs per
+// page at d = 128 and O^T += V^T P^T another 8 (the G-rows-as-M form above
+// pads G to 16 and needs 16 + 16).  P^T reaches the B-operand layout with two
+// movmatrix transposes.  Lane l holds tokens l/4 and l/4 + 8 of query
+// columns 2(l%4) and 2(l%4) + 1; the running max / sum of a column are kept
+// (redundantly) by the 8 lanes sharing l%4.
+FC_DEVINL uint32_t movmatrix_t(uint32_t x) {
+    uint32_t y;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+
+template <int D>
+struct Bf16WarpT {
+    uint32_t qb[D / 16][2];
+    float acc[D / 16][4];  // O^T tile i: [d = i*16 + l/4 (+8)][g = 2(l%4) + {0,1}]
+    float m[2], l[2];
+
+    FC_DEVINL void init(const __nv_bfloat16 *qrow0, int G, int lane) {
+        const int g = lane >> 2, c = (lane & 3) * 2;
+        const uint32_t *q = reinterpret_cast<const uint32_t *>(qrow0 + (int64_t)g * D);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+            qb[kk][0] = g < G ? q[(kk * 16 + c) / 2] : 0u;
+            qb[kk][1] = g < G ? q[(kk * 16 + 8 + c) / 2] : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < D / 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+        m[0] = m[1] = -INFINITY;
+        l[0] = l[1] = 0.f;
+    }
+
+    FC_DEVINL void page(char *stage, int ntok, float scale_log2, int lane) {
+        constexpr int RB = D * 2;  // row bytes
+        const uint32_t kb = smem_u32(stage);
+        const uint32_t vb = kb + kPageSize * RB;
+        if (ntok < kPageSize) {  // zero V rows past the fill (P=0 there, garbage could be NaN)
+            uint4 *vz = reinterpret_cast<uint4 *>(stage + kPageSize * RB + ntok * RB);
+            const int n16 = (kPageSize - ntok) * RB / 16;
+            for (int i = lane; i < n16; i += 32) vz[i] = make_uint4(0, 0, 0, 0);
+            __syncwarp();
+        }
+        const int mi = lane >> 3, ri = lane & 7;
+        // S^T = K q^T: A = K rows (tokens) x 16 dims, two accumulator chains
+        float s[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+        {
+            const int t = (mi & 1) * 8 + ri;
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+                const int c = 2 * kk + (mi >> 1);
+                uint32_t a[4];
+                ldsm_x4(kb + t * RB + ((c ^ (t & 7)) << 4), a[0], a[1], a[2], a[3]);
+                if (kk & 1) mma_bf16_16816(s2, a, qb[kk][0], qb[kk][1]);
+                else mma_bf16_16816(s, a, qb[kk][0], qb[kk][1]);
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) s[e] += s2[e];
+        }
+        // s[0..1]: token t0 = l/4, columns 2(l%4) + {0,1}; s[2..3]: token t0 + 8
+        const int t0 = lane >> 2;
+        float x[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[e] = (t0 + (e >> 1) * 8) < ntok ? s[e] * scale_log2 : -INFINITY;
+        float alpha[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {  // query column 2(l%4) + j: max over the 16 tokens (8 lanes)
+            float mx = fmaxf(x[j], x[2 + j]);
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+            const float mn = fmaxf(m[j], mx);
+            alpha[j] = exp2f(m[j] - mn);  // m = -inf on the first page -> 0
+            m[j] = mn;
+        }
+        float p[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) p[e] = exp2f(x[e] - m[e & 1]);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) l[j] = l[j] * alpha[j] + (p[j] + p[2 + j]);  // this lane's tokens
+#pragma unroll
+        for (int i = 0; i < D / 16; ++i) {
+            acc[i][0] *= alpha[0]; acc[i][1] *= alpha[1];
+            acc[i][2] *= alpha[0]; acc[i][3] *= alpha[1];
+        }
+        // P^T as the B operand (k = token, n = column): transpose the two 8x8 blocks
+        const uint32_t b0 = movmatrix_t(pack_bf16x2(p[0], p[1]));  // tokens 0-7
+        const uint32_t b1 = movmatrix_t(pack_bf16x2(p[2], p[3]));  // tokens 8-15
+        // O^T += V^T P^T: A = V^T (16 dims x 16 tokens) via ldmatrix.trans
+        {
+            const int t = (mi >> 1) * 8 + ri;
+#pragma unroll
+            for (int i = 0; i < D / 16; ++i) {
+                const int c = 2 * i + (mi & 1);
+                uint32_t a[4];
+                ldsm_x4_t(vb + t * RB + ((c ^ (t & 7)) << 4), a[0], a[1], a[2], a[3]);
+                mma_bf16_16816(acc[i], a, b0, b1);
+            }
+        }
+    }
+
+    FC_DEVINL void finalize() {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            l[j] += __shfl_xor_sync(0xffffffffu, l[j], 4);
+            l[j] += __shfl_xor_sync(0xffffffffu, l[j], 8);
+            l[j] += __shfl_xor_sync(0xffffffffu, l[j], 16);
+        }
+    }
+
+    // partial (unnormalised acc, running max m, sum l) of columns < G
+    FC_DEVINL void store_partial(float *po, float *pm, float *pl, int G, int lane) {
+        const int d0 = lane >> 2, gc = (lane & 3) * 2;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int g = gc + j;
+            if (g < G) {
+                if (d0 == 0) { pm[g] = m[j]; pl[g] = l[j]; }
+#pragma unroll
+                for (int i = 0; i < D / 16; ++i) {
+                    po[g * D + i * 16 + d0] = acc[i][j];
+                    po[g * D + i * 16 + d0 + 8] = acc[i][2 + j];
+                }
+            }
+        }
+    }
+
+    template <typename T>
+    FC_DEVINL void store_final(T *out, float *lse, int G, int lane) {
+        const int d0 = lane >> 2, gc = (lane & 3) * 2;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int g = gc + j;
+            if (g < G) {
+                const float inv = 1.f / l[j];
+#pragma unroll
+                for (int i = 0; i < D / 16; ++i) {
+                    out[g * D + i * 16 + d0] = T(acc[i][j] * inv);
+                    out[g * D + i * 16 + d0 + 8] = T(acc[i][2 + j] * inv);
+                }
+                if (lse && d0 == 0) lse[g] = (m[j] + log2f(l[j])) * 0.69314718055994531f;
+            }
+        }
+    }
+};
+
+// the engine's bf16 path: tokens as M (FC_ATTN_TOKENS_M=0 builds the
+// G-rows-as-M form, kept for comparison; it also allows G up to 16)
+#ifndef FC_ATTN_TOKENS_M
+#define FC_ATTN_TOKENS_M 1
+#endif
+template <int D>
+using Bf16Attn = typename std::conditional<FC_ATTN_TOKENS_M != 0, Bf16WarpT<D>, Bf16Warp<D>>::type;
+
 // fp32 CUDA-core path (G <= 8).  QK: lane = (token t = lane&15, half hf = lane>>4)
 // with a staggered column order (conflict-free); PV: lane owns D/32 columns.
 template <int D>
@@ -459,7 +613,7 @@ FC_DEVINL int attend_head_cta(const StoreView &s, const AttnArgs &a, int bh, cha
         for (int i = tid; i < G * D; i += NT) s_q[i] = qg[i];
         named_bar_sync(bar_id, NT);
     }
-    typename std::conditional<sizeof(T) == 2, Bf16Warp<D>, F32Warp<D>>::type st;
+    typename std::conditional<sizeof(T) == 2, Bf16Attn<D>, F32Warp<D>>::type st;
     if constexpr (sizeof(T) == 4) st.init(s_q, G, lane);
     else st.init(reinterpret_cast<const T *>(a.q) + qoff, G, lane);
     TokenPatch<T, D> tp;

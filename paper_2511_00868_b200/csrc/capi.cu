@@ -8,6 +8,7 @@
 #include <cstring>
 
 #include "launchers.cuh"
+#include "attn_warp.cuh"
 
 using namespace fc;
 
@@ -38,7 +39,7 @@ static int check_store(const fc_store *s) {
         return FC_E_UNSUPPORTED;
     }
     if (s->dtype != FC_BF16 && s->dtype != FC_F32) return invalid("dtype must be FC_BF16 or FC_F32");
-    const int gmax = s->dtype == FC_BF16 ? 16 : 8;
+    const int gmax = (s->dtype == FC_BF16 && !FC_ATTN_TOKENS_M) ? 16 : 8;  // query group = MMA N (8)
     if (s->group < 1 || s->group > gmax) {
         std::snprintf(g_last_error, sizeof(g_last_error), "group %d outside 1..%d", s->group, gmax);
         return FC_E_UNSUPPORTED;

@@ -142,7 +142,7 @@ attn_kernel(StoreView s, AttnArgs a, int S) {
         for (int i = tid; i < G * D; i += blockDim.x) s_q[i] = qg[i];
         __syncthreads();
     }
-    typename std::conditional<sizeof(T) == 2, Bf16Warp<D>, F32Warp<D>>::type st;
+    typename std::conditional<sizeof(T) == 2, Bf16Attn<D>, F32Warp<D>>::type st;
     if constexpr (sizeof(T) == 4) st.init(s_q, G, lane);
     else st.init(reinterpret_cast<const T *>(a.q) + qoff, G, lane);
     // the warp holding the head's last entry loads the new token (and the
@@ -384,7 +384,7 @@ attn_bal_kernel(StoreView s, AttnArgs a, int n_heads) {
     if (a.kv_prefetch) griddep_wait();  // q and the new token come from the previous launch
     const unsigned long long t_issued = trace ? gtimer() : 0ull;
 
-    typename std::conditional<sizeof(T) == 2, Bf16Warp<D>, F32Warp<D>>::type st;
+    typename std::conditional<sizeof(T) == 2, Bf16Attn<D>, F32Warp<D>>::type st;
     T *out = reinterpret_cast<T *>(a.out);
     const T *qall = reinterpret_cast<const T *>(a.q);
     float *myq = s_q + (size_t)w * G * D;
