@@ -1202,8 +1202,15 @@ static cudaError_t launch_score_attend_map_t(const StoreView &s, int layer, cons
 #ifndef FC_SA_SCORE_WARPS
 #define FC_SA_SCORE_WARPS 16
 #endif
+// attention ring stages / attending warps of the fused kernel, bf16 d = 128
+#ifndef FC_SA_NST128
+#define FC_SA_NST128 3
+#endif
+#ifndef FC_SA_NWA128
+#define FC_SA_NWA128 8
+#endif
 #define FC_SA_DISPATCH(dtype, D, CALL)                                                  \
-    ((dtype) == FC_BF16 ? ((D) == 128 ? CALL(__nv_bfloat16, 128, 3, 8, FC_SA_SCORE_WARPS)               \
+    ((dtype) == FC_BF16 ? ((D) == 128 ? CALL(__nv_bfloat16, 128, FC_SA_NST128, FC_SA_NWA128, FC_SA_SCORE_WARPS) \
                                       : CALL(__nv_bfloat16, 64, 6, 8, FC_SA_SCORE_WARPS))               \
                         : ((D) == 128 ? CALL(float, 128, 3, 4, 4) : CALL(float, 64, 6, 4, 4)))
 
