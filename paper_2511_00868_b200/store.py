@@ -226,7 +226,10 @@ class KVStore:
             scale, int(attend_appended), batch, self.stream()), "fc_score_attend")
 
     def score_attend_map_fits(self, n_ctas: int, cluster: int) -> bool:
-        return bool(self.lib.fc_score_attend_map_fits(self.cptr, n_ctas, cluster))
+        cache = self.__dict__.setdefault("_map_fits", {})
+        if (n_ctas, cluster) not in cache:
+            cache[(n_ctas, cluster)] = bool(self.lib.fc_score_attend_map_fits(self.cptr, n_ctas, cluster))
+        return cache[(n_ctas, cluster)]
 
     def mixed_cluster_map(self, batch: int, scored_heads, n_pages: int, topk_pages: int, *,
                           sms: int | None = None, bw_sm_gbs: float = 90.0, bw_gbs: float = 6000.0):
@@ -239,9 +242,11 @@ class KVStore:
         mixed grid does not fit.  Returns (map [n_ctas] int32 on the device,
         cluster)."""
         if sms is None:
-            sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+            if not hasattr(self, "_sms"):
+                self._sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+            sms = self._sms
         scored = sorted(set(int(h) for h in scored_heads))
-        if not scored:
+        if not scored or len(scored) == self.H:  # nothing to balance: the uniform launch
             return None
         n_s = batch * len(scored)
         n_o = batch * self.H - n_s
