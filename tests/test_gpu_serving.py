@@ -48,7 +48,8 @@ def test_serving_loop_requests_finish_and_blocks_return():
         e.k_new.normal_(generator=gen)
         e.v_new.normal_(generator=gen)
 
-    reqs = [Request(i, 0.0005 * i, 300 + 97 * i, 4 + 3 * (i % 3)) for i in range(7)]
+    # the first three arrive together (every row busy), the rest trickle in
+    reqs = [Request(i, 0.0 if i < 3 else 0.0005 * i, 300 + 97 * i, 4 + 3 * (i % 3)) for i in range(7)]
     loop = ServingLoop(eng, reqs, make_prompt, feed)
     m = loop.run()
     assert m.finished == len(reqs) and m.queued_at_end == 0
