@@ -338,9 +338,9 @@ class BlockTable:
         seq = torch.tensor([n * 16], dtype=torch.int32, device=dev)
         copies = torch.zeros((max(promoted.size, 1), 4), dtype=torch.int32, device=dev)
         n_copies = torch.zeros(1, dtype=torch.int32, device=dev)
-        ws = torch.zeros(2 + 2 * 1024, dtype=torch.int32, device=dev)
         st = self._view(row, l, h)
         st.sel_cap = cap
+        ws = torch.zeros(self.lib.fc_rerank_workspace_size(ctypes.byref(st)) // 4, dtype=torch.int32, device=dev)
         st.sel, st.n_sel, st.seq_len = new_sel.data_ptr(), n_new.data_ptr(), seq.data_ptr()
         _lib.check(self.lib.fc_rerank_recycle(
             ctypes.byref(st), 0, old_sel.data_ptr(), n_old.data_ptr(), self._unstable0.data_ptr(),

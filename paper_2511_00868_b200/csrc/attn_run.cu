@@ -240,7 +240,7 @@ FC_DEVINL void run_merge(const float *part, int pstride, int G, int wa, int np, 
         if (g < G) {
             const float mg = mr[g];
             const float M = warp_max(mg);
-            const float f = lane < np ? exp2f(mg - M) : 0.f;
+            const float f = (lane < np && M != -INFINITY) ? exp2f(mg - M) : 0.f;
             const float L = warp_sum(lr[g] * f);
             if (lane < np) fs[lane * 16 + g] = f;
             if (lane == g) { Lrow = L; Mrow = M; }

@@ -25,11 +25,21 @@ constexpr int kRecycleWarps = 4;
 constexpr int kListCap = 1024;  // max entries of an old/new selection list
 constexpr int kRecycleSlack = 64;  // pages appended since the old selection (old_has_tail)
 
-struct RerankWs {  // per head bh: [2 counts][kListCap free blocks][kListCap alloc pages]
+// per head bh: [4 counts: surplus, deficit, pairs m, -][evicted pages][their
+// blocks][promoted pages], kListCap each, ascending.  The first m evicted /
+// promoted entries are the pairs; the surplus blocks and deficit pages follow.
+// The commit kernel reads the whole diff, so when the pool cannot cover the
+// deficits it puts every paired move back before anything else changes
+// (BlockTable.recycle validates before mutating, blocktable.py:313-331).
+constexpr int kWsPerHead = 4 + 3 * kListCap;
+struct RerankWs {
     int32_t *base;
-    __device__ __forceinline__ int32_t *cnt(int bh) const { return base + (int64_t)bh * (2 + 2 * kListCap); }
-    __device__ __forceinline__ int32_t *freed(int bh) const { return cnt(bh) + 2; }
-    __device__ __forceinline__ int32_t *alloc(int bh) const { return cnt(bh) + 2 + kListCap; }
+    __device__ __forceinline__ int32_t *cnt(int bh) const { return base + (int64_t)bh * kWsPerHead; }
+    __device__ __forceinline__ int32_t *ev_page(int bh) const { return cnt(bh) + 4; }
+    __device__ __forceinline__ int32_t *ev_blk(int bh) const { return cnt(bh) + 4 + kListCap; }
+    __device__ __forceinline__ int32_t *pr_page(int bh) const { return cnt(bh) + 4 + 2 * kListCap; }
+    __device__ __forceinline__ int32_t *freed(int bh) const { return ev_blk(bh) + cnt(bh)[2]; }
+    __device__ __forceinline__ int32_t *alloc(int bh) const { return pr_page(bh) + cnt(bh)[2]; }
 };
 
 FC_DEVINL bool sorted_contains(const int32_t *a, int n, int x) {
@@ -72,7 +82,7 @@ rerank_diff_kernel(StoreView s, int layer, const int32_t *__restrict__ old_sel,
     const bool due = !unstable[layer * s.H + h] && (force_due || (*s.step % period == 0)) &&
                      !(row_skip && row_skip[b]);
     if (!due) {
-        if (lane == 0) { cnt[0] = 0; cnt[1] = 0; }
+        if (lane == 0) { cnt[0] = 0; cnt[1] = 0; cnt[2] = 0; }
         return;
     }
     const int hx = s.hix(b, layer, h);
@@ -88,7 +98,7 @@ rerank_diff_kernel(StoreView s, int layer, const int32_t *__restrict__ old_sel,
     int32_t *trow = s.table + s.table_off(hx, 0);
     const unsigned lt = (1u << lane) - 1u;
     if (n_old_sel > s.SELCAP || n_new > s.SELCAP) {
-        if (lane == 0) { set_error(s.err, FC_ERR_SEL_CAP); cnt[0] = 0; cnt[1] = 0; }
+        if (lane == 0) { set_error(s.err, FC_ERR_SEL_CAP); cnt[0] = 0; cnt[1] = 0; cnt[2] = 0; }
         return;
     }
     for (int i = lane; i < n_old_sel; i += 32) s_old[i] = olds[i];
@@ -98,7 +108,7 @@ rerank_diff_kernel(StoreView s, int layer, const int32_t *__restrict__ old_sel,
     // blocks of the old entries: every lane's loads issued before any use
     // (this validation was a chain of dependent table reads per 32 entries)
     if (n_old > cap) {
-        if (lane == 0) { set_error(s.err, FC_ERR_SEL_CAP); cnt[0] = 0; cnt[1] = 0; }
+        if (lane == 0) { set_error(s.err, FC_ERR_SEL_CAP); cnt[0] = 0; cnt[1] = 0; cnt[2] = 0; }
         return;
     }
     for (int base = 0; base < n_old; base += 128) {
@@ -170,7 +180,7 @@ rerank_diff_kernel(StoreView s, int layer, const int32_t *__restrict__ old_sel,
         }
     }
     if (n_ev > cap || n_pr > cap || n_ev > kListCap || n_pr > kListCap) {
-        if (lane == 0) { set_error(s.err, FC_ERR_SEL_CAP); cnt[0] = 0; cnt[1] = 0; }
+        if (lane == 0) { set_error(s.err, FC_ERR_SEL_CAP); cnt[0] = 0; cnt[1] = 0; cnt[2] = 0; }
         return;
     }
     __syncwarp();
@@ -190,15 +200,12 @@ rerank_diff_kernel(StoreView s, int layer, const int32_t *__restrict__ old_sel,
             set_error(s.err, FC_ERR_SEL_CAP);
         }
     }
-    int32_t *fr = ws.freed(bh);
-    for (int i = m + lane; i < n_ev; i += 32) {  // surplus evictions
-        const int e = s_evw[i];
-        fr[i - m] = s_evblk[i];
-        trow[e] = FC_NULL_BLOCK;
-    }
-    int32_t *al = ws.alloc(bh);
-    for (int i = m + lane; i < n_pr; i += 32) al[i - m] = s_prw[i];  // deficit pages
-    if (lane == 0) { cnt[0] = n_ev - m; cnt[1] = n_pr - m; }
+    for (int i = m + lane; i < n_ev; i += 32) trow[s_evw[i]] = FC_NULL_BLOCK;  // surplus evictions
+    // the whole diff for the commit (and its undo on pool exhaustion)
+    int32_t *evp = ws.ev_page(bh), *evb = ws.ev_blk(bh), *prp = ws.pr_page(bh);
+    for (int i = lane; i < n_ev; i += 32) { evp[i] = s_evw[i]; evb[i] = s_evblk[i]; }
+    for (int i = lane; i < n_pr; i += 32) prp[i] = s_prw[i];
+    if (lane == 0) { cnt[0] = n_ev - m; cnt[1] = n_pr - m; cnt[2] = m; }
 }
 
 // one CTA: pushes of all heads (head order) then pops (head order)
@@ -212,6 +219,29 @@ rerank_commit_kernel(StoreView s, int layer, int32_t *copies, int max_copies, in
     griddep_wait();
     const int nh = batch * s.H;
     const int top0 = *s.free_top;
+    // pass 0: can the pool cover every deficit (after the surplus pushes)?
+    // If not, undo the diff kernel's moves, emit no copies and leave the free
+    // list untouched: PoolExhausted with the table as before (blocktable.py:59-71)
+    {
+        int net = 0;
+        for (int bh = threadIdx.x; bh < nh; bh += 1024) net += ws.cnt(bh)[1] - ws.cnt(bh)[0];
+        int before, total;
+        Scan(tmp).ExclusiveSum(net, before, total);
+        __syncthreads();
+        if (top0 - total < 0) {
+            for (int bh = threadIdx.x; bh < nh; bh += 1024) {
+                const int *c = ws.cnt(bh);
+                const int m = c[2], n_ev = m + c[0];
+                if (n_ev == 0 && m == 0) continue;
+                const int b = bh / s.H, h = bh % s.H;
+                int32_t *trow = s.table + s.table_off(s.hix(b, layer, h), 0);
+                for (int i = 0; i < m; ++i) trow[ws.pr_page(bh)[i]] = FC_NULL_BLOCK;
+                for (int i = 0; i < n_ev; ++i) trow[ws.ev_page(bh)[i]] = ws.ev_blk(bh)[i];
+            }
+            if (threadIdx.x == 0) { *n_copies = 0; set_error(s.err, FC_ERR_POOL_EXHAUSTED); }
+            return;
+        }
+    }
     // pass 1: pushes
     int fcarry = 0;
     for (int c0 = 0; c0 < nh; c0 += 1024) {
@@ -452,7 +482,7 @@ evict_unselected_kernel(StoreView s, const uint8_t *unstable, int batch, int ext
 // ---------------------------------------------------------------------------
 
 size_t rerank_workspace_bytes(const StoreView &s) {
-    return (size_t)s.B * s.H * (2 + 2 * kListCap) * sizeof(int32_t);
+    return (size_t)s.B * s.H * kWsPerHead * sizeof(int32_t);
 }
 
 cudaError_t launch_rerank(const StoreView &s, int layer, const int32_t *old_sel, const int32_t *n_old,

@@ -224,7 +224,9 @@ attn_kernel(StoreView s, AttnArgs a, int S) {
         float L = 0.f, O = 0.f;
 #pragma unroll
         for (int ww = 0; ww < NW; ++ww) {
-            const float f = exp2f(s_wm[ww][g] - M);  // -inf rows of idle warps give 0
+            // idle warps hold m = -inf; a CTA whose warps are all idle (a cluster
+            // rank with no attended pages) has M = -inf too: guard the -inf - -inf
+            const float f = M == -INFINITY ? 0.f : exp2f(s_wm[ww][g] - M);
             L += s_wl[ww][g] * f;
             O += scratch[(size_t)ww * G * D + e] * f;
         }
@@ -249,7 +251,8 @@ attn_kernel(StoreView s, AttnArgs a, int S) {
                 for (int r = 0; r < S; ++r) M = fmaxf(M, cluster.map_shared_rank(cm, r)[g]);
                 float L = 0.f, O = 0.f;
                 for (int r = 0; r < S; ++r) {
-                    const float f = exp2f(cluster.map_shared_rank(cm, r)[g] - M);
+                    const float mr = cluster.map_shared_rank(cm, r)[g];
+                    const float f = mr == -INFINITY ? 0.f : exp2f(mr - M);  // empty rank: 0, not NaN
                     L += cluster.map_shared_rank(cl, r)[g] * f;
                     O += cluster.map_shared_rank(cstate, r)[e] * f;
                 }
@@ -525,13 +528,13 @@ attn_bal_kernel(StoreView s, AttnArgs a, int n_heads) {
                 float L = 0.f, O = 0.f;
                 for (int k2 = 0; k2 < 2 * NW; ++k2) {
                     if (s_shead[k2] != h2) continue;
-                    const float f = exp2f(s_sm[k2][g] - M);
+                    const float f = M == -INFINITY ? 0.f : exp2f(s_sm[k2][g] - M);
                     L += s_sl[k2][g] * f;
                     O += (k2 < NW ? slotA + (size_t)k2 * G * D : slotB + (size_t)(k2 - NW) * G * D)[e] * f;
                 }
                 if (owner_wait)
                     for (int c2 = c_first; c2 < (int)blockIdx.x; ++c2) {
-                        const float f = exp2f(__ldcg(a.part_m + c2 * 16 + g) - M);
+                        const float f = M == -INFINITY ? 0.f : exp2f(__ldcg(a.part_m + c2 * 16 + g) - M);
                         L += __ldcg(a.part_l + c2 * 16 + g) * f;
                         O += __ldcg(a.part_o + ((int64_t)c2 * G * D) + e) * f;
                     }

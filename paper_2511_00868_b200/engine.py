@@ -200,6 +200,8 @@ class DecodeEngine:
         if self.tiering and row in self._evict_pending:  # its blocks may still be read by the offload
             torch.cuda.current_stream(self.device).wait_event(self._evict_pending.pop(row)[0])
             self.row_skip[row] = 0
+        if self.stager is not None:
+            self.stager.forget_row(row)
         self.store.free_row(row)
         self.seq_host[row] = -1
         self._initial_rows.discard(row)

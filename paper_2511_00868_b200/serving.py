@@ -28,7 +28,7 @@ Prompts and decode inputs are synthetic (the reference has no model either).
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field, fields
+from dataclasses import dataclass, fields
 
 import torch
 
@@ -87,7 +87,7 @@ class _Active:
     commit: int = 0
     emitted: int = 0
     first_token_s: float = 0.0
-    step_times: list = field(default_factory=list)
+    last_token_s: float = 0.0
 
 
 class ServingLoop:
@@ -179,7 +179,7 @@ class ServingLoop:
                 active[row] = _Active(req, row, commit=need)
                 self._ttft.append(self.now - req.arrival_s)  # prefill emits the first token
                 active[row].emitted = 1
-                active[row].first_token_s = self.now
+                active[row].first_token_s = active[row].last_token_s = self.now
                 self.m.total_tokens += req.prompt_tokens
             self.m.peak_batch = max(self.m.peak_batch, len(active))
             in_use = (eng.store.n_blocks - 1 - eng.store.free_count()) * self.page_bytes
@@ -204,7 +204,7 @@ class ServingLoop:
             for row in list(active):
                 a = active[row]
                 a.emitted += 1
-                a.step_times.append(dt)
+                a.last_token_s = self.now
                 self.m.output_tokens += 1
                 steady = self._steady_blocks(a.req)
                 if a.commit > steady and not eng.eviction_pending(row):
@@ -216,7 +216,11 @@ class ServingLoop:
                     self.now += self.timer(lambda: eng.retire(row))
                     self.committed -= a.commit
                     free_rows.append(row)
-                    self._tpot.extend(a.step_times)
+                    if a.emitted > 1:
+                        # per request, as the reference's _finish (simulator.py:590-592):
+                        # (last - first token) / (emitted - 1), so prefills of other
+                        # requests and retires between its tokens count
+                        self._tpot.append((a.last_token_s - a.first_token_s) / (a.emitted - 1))
                     self.m.finished += 1
                     del active[row]
         m = self.m

@@ -60,6 +60,8 @@ class TierStore:
             raise ConsistencyError(f"page {dup} of {head} offloaded twice for request row {row}")
         n_bytes = int(pages.size) * self.page_bytes
         if self.slow_bytes_used + n_bytes > self.capacity_bytes:
+            self._refresh_usage()
+        if self.slow_bytes_used + n_bytes > self.capacity_bytes:
             raise AdmissionError(f"slow tier capacity exceeded: {self.slow_bytes_used + n_bytes} "
                                  f"> {self.capacity_bytes}")
         counts[pages] = 1
@@ -129,12 +131,31 @@ class TierStore:
         ledger entries and the bytes they held are released; the row may host
         a new request, whose write-once ledger starts empty)."""
         for key in [k for k in self._counts if k[0] == row]:
-            self.slow_bytes_used -= int(self._counts.pop(key).sum()) * self.page_bytes
+            self.slow_bytes_used = max(0, self.slow_bytes_used - int(self._counts.pop(key).sum()) * self.page_bytes)
         self.slow_resident[row].zero_()
 
+    def _refresh_usage(self) -> None:
+        # pages filled during decode are offloaded inside the step graph
+        # (fc_offload_filled sets slow_resident on the device; a second write
+        # of a page raises FC_ERR_WRITE_TWICE there): the slow-tier bytes in
+        # use are the device flags plus host-ledgered pages not flagged yet
+        torch.cuda.current_stream(self.store.device).synchronize()
+        flags = self.slow_resident.cpu().numpy()
+        extra = 0
+        for (row, head), c in self._counts.items():
+            extra += int((c.astype(bool) & ~flags[row, head.layer, head.head].astype(bool)).sum())
+        self.slow_bytes_used = (int(flags.sum()) + extra) * self.page_bytes
+
     def offload_counts(self, row: int, head: HeadId) -> dict:
-        c = self._counts.get((row, HeadId(*head)))
-        return {} if c is None else {int(p): int(c[p]) for p in np.flatnonzero(c)}
+        """Pages of (row, head) in the slow tier, each written once: the
+        host-ledgered offloads (post-prefill, incremental) and the decode-time
+        offloads recorded on the device (tiering.py:99-157)."""
+        head = HeadId(*head)
+        c = self._counts.get((row, head))
+        dev = self.slow_resident[row, head.layer, head.head].cpu().numpy().astype(bool)
+        if c is not None:
+            dev |= c.astype(bool)
+        return {int(p): 1 for p in np.flatnonzero(dev)}
 
     def slow_pages(self, row: int, head: HeadId) -> set:
         return set(self.offload_counts(row, head))
@@ -230,6 +251,17 @@ class ReloadStager:
         self._hits32.zero_()
         self.staged_pages.add_(self.stage_count[0].clamp(max=self.capacity).long())
         self.store.stage_clear(self.staged_map, self.stage_list, self.stage_count, self.capacity)
+
+    def forget_row(self, row: int) -> None:
+        """A retired row: drop its staged pages before the row can host a new
+        request (the staging map is indexed by (row, layer, head, page); a stale
+        entry would hand the old request's page to the new one at its first
+        rerank).  The current stream first waits for the staging copies, so no
+        copy still reads the old request's host slots when the new request's
+        offload overwrites them."""
+        if self.pending:
+            torch.cuda.current_stream(self.store.device).wait_event(self.ev_staged)
+        self.staged_map[row].fill_(-1)
 
     def rerank_launched(self) -> None:
         """Host bookkeeping after a rerank step was launched (the step graph

@@ -113,6 +113,48 @@ def test_pool_exhaustion_is_atomic():
     assert pool.free_count == 1
 
 
+def test_device_recycle_exhaustion_leaves_table_unchanged():
+    """fc_rerank_recycle with more deficit pages than free blocks: PoolExhausted,
+    and the table, free list and copy list are as before the call — the paired
+    moves of the diff kernel are undone (blocktable.py:313-331 validates before
+    mutating)."""
+    from paper_2511_00868_b200.errors import PoolExhausted
+    from paper_2511_00868_b200.store import KVStore
+    st = KVStore(batch_cap=1, layers=1, kv_heads=2, group=1, head_dim=64, pages_cap=16, n_blocks=16,
+                 sel_cap=16, dtype=torch.float32)
+    st.alloc_pages(0, 0, 4)                     # pages 0..3 of both heads: 8 blocks, 7 free
+    full_top = st.free_count()
+    st.free_top.fill_(2)                        # only 2 of them offered to the recycle
+    st.seq_len.fill_(10 * 16)                   # pages 4..9 exist logically, not resident
+    old = torch.zeros((1, 2, 16), dtype=torch.int32, device="cuda")
+    old[0, :, :4] = torch.arange(4, dtype=torch.int32)
+    n_old = torch.full((1, 2), 4, dtype=torch.int32, device="cuda")
+    new = [0, 4, 5, 6, 7, 8, 9]                 # evicts 1..3, promotes 4..9: 3 pairs + deficit 3
+    st.sel.zero_()
+    st.sel[0, 0, :, :len(new)] = torch.tensor(new, dtype=torch.int32)
+    st.n_sel.fill_(len(new))
+    table0, stack0, top0 = st.table.clone(), st.free_stack.clone(), st.free_count()
+    copies = torch.zeros((64, 4), dtype=torch.int32, device="cuda")
+    nc = torch.zeros(1, dtype=torch.int32, device="cuda")
+    unstable = torch.zeros(2, dtype=torch.uint8, device="cuda")
+    st.rerank_recycle(0, old, n_old, unstable, 1, copies, nc, 1, force_due=True, old_has_tail=False,
+                      extra_tokens=0)
+    with pytest.raises(PoolExhausted):
+        st.check_errors()
+    assert torch.equal(st.table, table0)
+    assert st.free_count() == top0 and torch.equal(st.free_stack[:top0], stack0[:top0])
+    assert int(nc.item()) == 0
+    # with enough blocks the same recycle goes through (control)
+    st.free_top.fill_(full_top)
+    st.rerank_recycle(0, old, n_old, unstable, 1, copies, nc, 1, force_due=True, old_has_tail=False,
+                      extra_tokens=0)
+    st.check_errors()
+    t = st.table[0, 0].cpu().numpy()
+    for h in range(2):
+        assert sorted(np.flatnonzero(t[h]).tolist()) == new
+    assert int(nc.item()) == 2 * 6
+
+
 def test_random_ops_keep_invariants():
     """Fuzz of allocate / evict / recycle / release against the invariants
     (criterion 09 style, test_acceptance.py:261-331), smaller op count."""

@@ -70,7 +70,18 @@ def test_every_request_finishes_and_tokens_add_up():
     assert m.output_tokens == sum(r.output_tokens - 1 for r in reqs)  # prefill emits the first token
     assert m.peak_batch == 2 and eng.max_active == 2
     assert eng.rows == {}
-    assert m.throughput_tokens_per_s > 0 and m.tpot_mean_s == 0.01
+    assert m.throughput_tokens_per_s > 0 and m.tpot_mean_s >= 0.01
+
+
+def test_tpot_is_per_request_and_counts_other_prefills():
+    # simulator.py:590-592: TPOT = (last - first token) / (emitted - 1) per
+    # request, so another request's prefill between two tokens counts
+    reqs = [Request(0, 0.0, 100, 10), Request(1, 0.03, 100, 3)]
+    m, _ = _run(reqs, B=2)
+    a = (0.05 + 0.05 + 9 * 0.01 - 0.05) / 9      # first token 0.05, B's prefill, 9 steps
+    b = 0.01                                      # first token 0.10, 2 steps
+    assert abs(m.tpot_mean_s - (a + b) / 2) < 1e-12
+    assert abs(m.tpot_p95_s - a) < 1e-12 and abs(m.tpot_p50_s - b) < 1e-12
 
 
 def test_admission_waits_for_budget():
