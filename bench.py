@@ -41,19 +41,22 @@ METRIC = "decode-attn tokens/s/GPU at 32k ctx, % HBM roofline, vs CPU ref"
 # (no collective).  A GPU holds at most 8 such requests fully resident (146 GB
 # of KV + summaries), so below 8 GPUs each rank runs the 8-GPU per-GPU share
 # (weak-scaling unit) and says so in the config.
-CFG4 = dict(workload="config4: llama3.1-8b-shaped decode, 32 layers, 32q/8kv heads, d=128, 128k ctx, "
+CFG4 = dict(key="config4", workload="config4: llama3.1-8b-shaped decode, 32 layers, 32q/8kv heads, d=128, 128k ctx, "
                      "64 requests request-parallel over the GPUs, page 16, top-K 128 pages, R=16, u=0.25",
             layers=32, kv_heads=8, group=4, head_dim=128, ctx=131072, batch=8, topk=128,
             period=16, unstable_fraction=0.25, total_requests=64)
 
 
 
-def _traffic():
-    """dram__bytes_read.sum + dram__bytes_write.sum per attn_kernel launch from
-    the committed ncu launch list (profiles/r01_traffic.json), or None."""
+def _traffic(key: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the roofline
+    kernel of workload ``key`` (e.g. "config2/attn_kernel"), from the ncu
+    capture of that same kernel and config summarised in
+    profiles/traffic.json; None when no capture of that exact pair exists."""
     try:
-        with open(os.path.join(HERE, "profiles", "r01_traffic.json")) as fh:
-            return float(json.load(fh)["traffic_bytes_per_launch"])
+        with open(os.path.join(HERE, "profiles", "traffic.json")) as fh:
+            ent = json.load(fh)[key]
+        return float(ent["traffic_bytes_per_launch"])
     except Exception:
         return None
 
@@ -177,36 +180,55 @@ def cpu_baseline(cfg, target_s=15.0):
                        f"processes; extrapolated x B*L*H per step")}
 
 
-def run_reference(args, cfg):
-    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
-    if rank != 0:
-        return
-    from oracle import cpu_ref
+def reference_cpu(cfg, *, steps, warmup, units_per_step=None):
+    """The unmodified reference ``tierkv`` (baseline/_ref, oracle/tierkv_ref.py)
+    over head units of one (request, layer) of ``cfg`` on every host core;
+    falls back to the oracle port when baseline/_ref is absent.  Returns
+    (tokens/s extrapolated x B*L*H, seconds per step of the config, dict)."""
+    from oracle import cpu_ref, tierkv_ref
     cores = cpu_ref.host_cores()
     due = cpu_ref.due_fraction(cfg["unstable_fraction"], cfg["period"])
-    units_per_sample = cores * 4
-    cpu_ref._setup(cfg["ctx"], cfg["kv_heads"], cfg["head_dim"], cfg["group"], cfg["topk"], 12345)
-    import multiprocessing as mp
-    n_due = int(round(due * units_per_sample))
-    jobs = [(i % cfg["kv_heads"], i < n_due) for i in range(units_per_sample)]
-    with mp.get_context("fork").Pool(cores, initializer=cpu_ref._limit_blas) as pool:
-        for _ in range(args.warmup):
-            pool.map(cpu_ref._unit, jobs)
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            pool.map(cpu_ref._unit, jobs)
-        dt = time.perf_counter() - t0
-    spu = dt / (args.steps * units_per_sample)
+    ups = units_per_step or cores * 4
+    if tierkv_ref.available():
+        dt = tierkv_ref.run_steps(ctx=cfg["ctx"], heads=cfg["kv_heads"], d=cfg["head_dim"], g=cfg["group"],
+                                  k=cfg["topk"], due_frac=due, units_per_step=ups, steps=steps,
+                                  warmup=warmup, cores=cores)
+        kind, what = "reference", "the unmodified reference tierkv 0.1.0 (baseline/_ref): update_minmax, " \
+                                  "G x score_pages + select_topk(pin last) when due, G x sparse_decode"
+    else:
+        cpu_ref._setup(cfg["ctx"], cfg["kv_heads"], cfg["head_dim"], cfg["group"], cfg["topk"], 12345)
+        import multiprocessing as mp
+        n_due = int(round(due * ups))
+        jobs = [(i % cfg["kv_heads"], i < n_due) for i in range(ups)]
+        with mp.get_context("fork").Pool(cores, initializer=cpu_ref._limit_blas) as pool:
+            for _ in range(max(1, warmup)):
+                pool.map(cpu_ref._unit, jobs)
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                pool.map(cpu_ref._unit, jobs)
+            dt = time.perf_counter() - t0
+        kind, what = "port", "the oracle restatement of tierkv (baseline/_ref absent)"
+    spu = dt / (steps * ups)
     step_s = spu * cfg["batch"] * cfg["layers"] * cfg["kv_heads"]
     tps = cfg["batch"] / step_s
+    info = {"value": tps, "unit": "tokens/s", "cores": cores, "kind": kind,
+            "sample": (f"{steps} x {ups} head-step units (due fraction u+(1-u)/R={due:.4f}) of one "
+                       f"(request, layer) at {cfg['ctx']} ctx, float64, fork pool of {cores} processes "
+                       f"with one BLAS thread each; {what}; extrapolated x B*L*H per step")}
+    return tps, step_s, info
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    tps, step_s, info = reference_cpu(cfg, steps=args.steps, warmup=args.warmup)
     line = {"metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic N(0,1) KV/queries (bf16-rounded), seed 12345",
             "config": {"workload": cfg["workload"]}, "impl": "reference",
-            "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port",
-                             "sample": f"each step = {units_per_sample} head units of one (request, "
-                                       f"layer), extrapolated x B*L*H; oracle restatement of tierkv"},
+            "cpu_baseline": info,
             "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -402,7 +424,11 @@ def run_ours(args, cfg):
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg)
+        from oracle import cpu_ref
+        _, _, cpu = reference_cpu(cfg, steps=4, warmup=1, units_per_step=cpu_ref.host_cores() * 64)
+        if cpu["kind"] == "reference":  # the oracle port beside it
+            port = cpu_baseline(cfg)
+            cpu["port"] = {"value": port["value"], "cores": port["cores"], "sample": port["sample"]}
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -423,7 +449,7 @@ def run_ours(args, cfg):
         "gpu_launches": launches,
         "step_ms": step_stats,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": _traffic(), "kernel": "fc_sparse_decode (attn_kernel)",
+                     "frac": achieved / peak, "traffic": _traffic(cfg.get("key", "config2") + "/attn_kernel"), "kernel": "fc_sparse_decode (attn_kernel)",
                      "peak_source": peak_src, "avg_launch_us": att_avg_s * 1e6,
                      "isolated_launch_us": att_iso_s * 1e6, "alg_bytes_per_launch": att_alg,
                      "serialized_launch_us": att_serial_s * 1e6,
