@@ -260,6 +260,8 @@ def run_ours(args, cfg):
         eng.mixed_clusters = False
     if os.environ.get("FC_FUSED") == "0":  # profiling knob: scoring and attention as two launches
         eng.fused_score_attend = False
+    if os.environ.get("FC_BALANCED") == "0":  # profiling knob: no balanced-scoring launches
+        eng.balanced_scoring = False
     # prefill: 4 distinct random [H, T, d] sources, rotated over (row, layer)
     seed0 = 12345 + 1000 * rank
     srcs = [(device_normal((H, T, D), seed=seed0 + 2 * i, device=dev),

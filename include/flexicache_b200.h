@@ -243,6 +243,25 @@ int fc_score_attend(const fc_store *s, int layer, const void *q,
  * fc_score_attend_map_fits: 1 when a cluster of `cluster` CTAs of this
  * kernel fits on the device (n_ctas a multiple of it). */
 int fc_score_attend_map_fits(const fc_store *s, int n_ctas, int cluster);
+/* fc_score_attend with the scoring balanced over the whole GPU: one wave of
+ * max(batch * kv_heads, SMs) co-resident CTAs first scores equal shares of
+ * the concatenation of the due heads' candidate pages (as fc_score_select's
+ * balanced kernel: the same per-page scores), then CTA i selects head i when
+ * it is due (after every share of its scores landed; select_topk with the
+ * last page pinned, scoring.py:164-193) and attends head i (sparse_decode,
+ * attention.py:85-111, with the fused update_minmax).  For layers where only
+ * some heads are due the summaries then stream at the GPU's rate rather than
+ * one SM's.  counters: [batch_cap * kv_heads] int32, zero, left zero.
+ * bf16 only; fc_score_attend_balanced_supported returns the grid it uses for
+ * this batch, 0 when it does not fit (FC_E_UNSUPPORTED). */
+int fc_score_attend_balanced_supported(const fc_store *s, int batch);
+int fc_score_attend_balanced(const fc_store *s, int layer, const void *q,
+                             const uint8_t *unstable, int period, int force_due,
+                             int topk, int extra_tokens, int kv_prefetch,
+                             float *scores_out, int32_t *counters,
+                             const void *k_new, const void *v_new, void *out,
+                             float *lse, float scale, int attend_appended,
+                             int batch, void *stream);
 int fc_score_attend_map(const fc_store *s, int layer, const void *q,
                         const uint8_t *unstable, int period, int force_due,
                         int topk, int extra_tokens, int kv_prefetch,

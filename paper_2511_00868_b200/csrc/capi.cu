@@ -70,8 +70,13 @@ int fc_debug_attn_trace(void *device_buf) { return cuda_status(set_attn_trace(de
 int fc_debug_run_trace(void *device_buf) { return cuda_status(set_run_trace(device_buf)); }
 int fc_debug_persist_trace(void *device_buf) { return cuda_status(set_persist_trace(device_buf)); }
 int fc_debug_score_trace(void *device_buf) { return cuda_status(set_score_trace(device_buf)); }
+int fc_debug_sa_trace(void *device_buf) { return cuda_status(set_sa_trace(device_buf)); }
 /* test hook: scoring kernel choice, -1 auto, 0 balanced, 1 head-aligned */
 int fc_debug_score_mode(int mode) { set_score_mode(mode); return FC_OK; }
+int fc_debug_score_ctas_per_sm(int n) { set_score_ctas_per_sm(n); return FC_OK; }
+/* tuning hook: byte cap of the next-layer summary warm-up in fc_score_attend
+ * (0 off, < 0 default 48 MiB) */
+int fc_debug_summary_prefetch(long long bytes) { set_summary_prefetch_cap(bytes); return FC_OK; }
 /* test hook: attention variant, 0 cluster per head (default), 1 balanced
  * all-SM variant for small head counts */
 int fc_debug_attn_mode(int mode) { set_attn_mode(mode); return FC_OK; }
@@ -199,6 +204,42 @@ int fc_score_attend(const fc_store *s, int layer, const void *q, const uint8_t *
     a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.max_splits = 1;
     return cuda_status(launch_score_attend(v, s->dtype, layer, q, unstable, period, force_due, topk, extra_tokens,
                                            scores_out, batch, kv_prefetch ? 1 : 0, a, (cudaStream_t)stream));
+}
+
+int fc_score_attend_balanced_supported(const fc_store *s, int batch) {
+    if (check_store(s) != FC_OK || s->pages_cap > kMaxPagesCap || batch < 1 || batch > s->batch_cap) return 0;
+    return score_attend_balanced_grid(make_view(s), s->dtype, batch);
+}
+
+int fc_score_attend_balanced(const fc_store *s, int layer, const void *q, const uint8_t *unstable, int period,
+                             int force_due, int topk, int extra_tokens, int kv_prefetch, float *scores_out,
+                             int32_t *counters, const void *k_new, const void *v_new, void *out, float *lse,
+                             float scale, int attend_appended, int batch, void *stream) {
+    FC_CHECK(check_store(s));
+    if (layer < 0 || layer >= s->layers) return invalid("layer out of range");
+    if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
+    if (period < 1) return invalid("period must be >= 1");  // rerank_due, scoring.py:198-199
+    if (topk < 1) return invalid("k must be >= 1");          // select_topk, scoring.py:174-175
+    if (topk > s->sel_cap) return FC_E_CAPACITY;
+    if (extra_tokens < 0 || extra_tokens > 1) return invalid("extra_tokens must be 0 or 1");
+    if (!q || !unstable || !scores_out || !counters || !out) return invalid("null buffer");
+    if ((k_new == nullptr) != (v_new == nullptr)) return invalid("k_new and v_new go together");
+    if (k_new && extra_tokens != 1) return invalid("fused append needs extra_tokens = 1");
+    if (!(scale > 0.f) || !std::isfinite(scale)) return invalid("scale must be positive");
+    if (s->pages_cap > kMaxPagesCap) return FC_E_CAPACITY;
+    if (batch == 0) return FC_OK;
+    const StoreView v = make_view(s);
+    if (!score_attend_balanced_grid(v, s->dtype, batch)) {
+        std::snprintf(g_last_error, sizeof(g_last_error), "balanced score+attend does not fit this batch / geometry");
+        return FC_E_UNSUPPORTED;
+    }
+    AttnArgs a = {};
+    a.layer = layer; a.q = q; a.k_new = k_new; a.v_new = v_new; a.out = out; a.lse = lse;
+    a.scale_log2 = scale * 1.4426950408889634f;
+    a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.max_splits = 1;
+    return cuda_status(launch_score_attend_balanced(v, s->dtype, layer, q, unstable, period, force_due, topk,
+                                                    extra_tokens, scores_out, counters, batch, kv_prefetch ? 1 : 0,
+                                                    a, (cudaStream_t)stream));
 }
 
 int fc_score_attend_map_fits(const fc_store *s, int n_ctas, int cluster) {

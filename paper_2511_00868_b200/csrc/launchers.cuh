@@ -25,6 +25,11 @@ struct AttnArgs {
     // cluster of one) or -1 (idle); null = CTA i / S attends head i / S
     const int32_t *cta_map;
     int map_heads;        // batch * H: bound of the map's head indices
+    // fc_score_attend: CTAs of heads not scored this step, once their pages
+    // are attended, warm L2 with the next layer's due summaries (the scored
+    // CTAs of that layer then stream them from L2) when those are at most
+    // this many bytes; 0 = off (set by the launcher)
+    int64_t pf_cap;
 };
 
 // persistent multi-layer attention (attn_run.cu)
@@ -69,6 +74,9 @@ cudaError_t launch_score_attend_map(const StoreView &, int, int, const void *, c
                                     float *, int, const AttnArgs &, int, int, cudaStream_t);
 cudaError_t launch_score_attend(const StoreView &, int, int, const void *, const uint8_t *, int, int, int, int,
                                 float *, int, int, const AttnArgs &, cudaStream_t);
+int score_attend_balanced_grid(const StoreView &, int, int);
+cudaError_t launch_score_attend_balanced(const StoreView &, int, int, const void *, const uint8_t *, int, int, int, int,
+                                         float *, int32_t *, int, int, const AttnArgs &, cudaStream_t);
 cudaError_t launch_select(const float *, int, const int32_t *, int, int, int, int32_t *, int32_t *,
                           cudaStream_t);
 cudaError_t launch_attn(const StoreView &, int, const AttnArgs &, int, cudaStream_t);
@@ -77,7 +85,10 @@ cudaError_t set_attn_trace(void *);
 cudaError_t set_run_trace(void *);
 cudaError_t set_persist_trace(void *);
 cudaError_t set_score_trace(void *);
+cudaError_t set_sa_trace(void *);
 void set_score_mode(int);
+void set_score_ctas_per_sm(int);
+void set_summary_prefetch_cap(int64_t bytes);  // < 0: default
 void set_attn_mode(int);
 void set_run_mode(int);
 cudaError_t launch_trace_capture(const StoreView &, uint32_t *, uint32_t *, int, int, int, int, int, cudaStream_t);

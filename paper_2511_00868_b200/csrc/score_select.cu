@@ -24,6 +24,9 @@ namespace fc {
 
 // Optional per-CTA timeline for profiling (see fc_debug_attn_trace): [grid][4]
 __device__ unsigned long long *g_score_trace = nullptr;
+// fused kernel timeline (fc_debug_sa_trace): [grid][4] entry, selection
+// visible, attention done, exit
+__device__ unsigned long long *g_sa_trace = nullptr;
 FC_DEVINL unsigned long long gtimer_s() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -329,10 +332,13 @@ FC_DEVINL void chunk_to_f<float>(const uint4 &c, float *f) {
 }
 
 // Scores pages [p0, p1) of head hx; w = [sum q⁻ | sum q⁺] in shared memory.
-template <typename T, int D>
+// RPI = pages per lane-slot per iteration: the loads a lane keeps in flight.
+template <typename T, int D, int RPI = kRoundsPerIter>
 __device__ void score_range(const StoreView &s, int hx, int p0, int p1, const float *w,
                             float *scores_row) {
+    constexpr int kRoundsPerIter = RPI;
     using Gm = ScoreGeom<T, D>;
+    constexpr int kPagesPerIter = Gm::kPagesPerSlot * RPI;
     constexpr int LPP = Gm::kLanesPerPage, CPL = Gm::kChunksPerLane, EPC = Gm::kElemsPerChunk;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
@@ -346,7 +352,7 @@ __device__ void score_range(const StoreView &s, int hx, int p0, int p1, const fl
         for (int e = 0; e < EPC; ++e) coef[c][e] = w[(cl + c * LPP) * EPC + e];
     const char *base = reinterpret_cast<const char *>(s.summ) +
                        (int64_t)hx * s.NCAP * Gm::kRecBytes;
-    for (int it0 = p0 + warp * Gm::kPagesPerIter; it0 < p1; it0 += nwarps * Gm::kPagesPerIter) {
+    for (int it0 = p0 + warp * kPagesPerIter; it0 < p1; it0 += nwarps * kPagesPerIter) {
         uint4 raw[kRoundsPerIter][CPL];
 #pragma unroll
         for (int r = 0; r < kRoundsPerIter; ++r) {
@@ -377,7 +383,8 @@ __device__ void score_range(const StoreView &s, int hx, int p0, int p1, const fl
         // plain butterflies over the LPP/R lanes that share a round; lane bits
         // then select which round a lane holds.
         static_assert(LPP >= kRoundsPerIter, "rounds per iteration exceed lanes per page");
-        constexpr int NSTEP = kRoundsPerIter == 16 ? 4 : kRoundsPerIter == 8 ? 3 : kRoundsPerIter == 4 ? 2 : 1;
+        constexpr int NSTEP = kRoundsPerIter == 32 ? 5 : kRoundsPerIter == 16 ? 4 : kRoundsPerIter == 8 ? 3
+                            : kRoundsPerIter == 4 ? 2 : 1;
         int ridx = 0;
 #pragma unroll
         for (int step = 0, dist = LPP / 2, cnt = kRoundsPerIter / 2; step < NSTEP;
@@ -397,6 +404,69 @@ __device__ void score_range(const StoreView &s, int hx, int p0, int p1, const fl
         if ((cl & (LPP / kRoundsPerIter - 1)) == 0) {
             const int p = it0 + ridx * Gm::kPagesPerSlot + sub;
             if (p < p1) scores_row[p] = v[0];
+        }
+    }
+}
+
+// Scores n consecutive page records starting at rec0 (global memory or, for
+// SMEM, a staged copy in shared memory) into out[0, n): score_range's lane
+// layout and reduction, so the scores are bit-identical to it.
+template <typename T, int D, int RPI, bool SMEM>
+__device__ void score_span(const char *rec0, int n, const float *w, float *out) {
+    using Gm = ScoreGeom<T, D>;
+    constexpr int LPP = Gm::kLanesPerPage, CPL = Gm::kChunksPerLane, EPC = Gm::kElemsPerChunk;
+    constexpr int PPI = Gm::kPagesPerSlot * RPI;
+    static_assert(LPP >= RPI, "rounds per iteration exceed lanes per page");
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    const int sub = lane / LPP, cl = lane % LPP;
+    float coef[CPL][EPC];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) coef[c][e] = w[(cl + c * LPP) * EPC + e];
+    for (int it0 = warp * PPI; it0 < n; it0 += nwarps * PPI) {
+        uint4 raw[RPI][CPL];
+#pragma unroll
+        for (int r = 0; r < RPI; ++r) {
+            const int p = it0 + r * Gm::kPagesPerSlot + sub;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                const uint4 *src = reinterpret_cast<const uint4 *>(rec0 + (int64_t)p * Gm::kRecBytes + (cl + c * LPP) * 16);
+                if (p < n) raw[r][c] = SMEM ? *src : __ldg(src);
+                else raw[r][c] = make_uint4(0, 0, 0, 0);
+            }
+        }
+        float v[RPI];
+#pragma unroll
+        for (int r = 0; r < RPI; ++r) {
+            float acc = 0.f;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                float f[EPC];
+                chunk_to_f<T>(raw[r][c], f);
+#pragma unroll
+                for (int e = 0; e < EPC; ++e) acc = fmaf(f[e], coef[c][e], acc);
+            }
+            v[r] = acc;
+        }
+        constexpr int NSTEP = RPI == 32 ? 5 : RPI == 16 ? 4 : RPI == 8 ? 3 : RPI == 4 ? 2 : 1;
+        int ridx = 0;
+#pragma unroll
+        for (int step = 0, dist = LPP / 2, cnt = RPI / 2; step < NSTEP; ++step, dist >>= 1, cnt >>= 1) {
+            const bool upper = (lane & dist) != 0;
+#pragma unroll
+            for (int i = 0; i < cnt; ++i) {
+                const float send = upper ? v[i] : v[i + cnt];
+                const float keep = upper ? v[i + cnt] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, dist);
+            }
+            if (upper) ridx += cnt;
+        }
+#pragma unroll
+        for (int dist = LPP / RPI / 2; dist > 0; dist >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], dist);
+        if ((cl & (LPP / RPI - 1)) == 0) {
+            const int p = it0 + ridx * Gm::kPagesPerSlot + sub;
+            if (p < n) out[p] = v[0];
         }
     }
 }
@@ -606,6 +676,7 @@ constexpr int kHeadScoreWarps = FC_HEAD_WARPS;
 #define FC_SCORE_MODE_DEFAULT -1
 #endif
 static int g_score_mode = FC_SCORE_MODE_DEFAULT;  // -1 auto, 0 balanced, 1 head-aligned (test hook)
+static int g_score_ctas_per_sm = 0;  // balanced kernel: CTAs per SM (0: as many as fit)
 constexpr int kHeadChunkPages = FC_HEAD_CHUNK_PAGES;
 
 template <typename T, int D, int NWS = kHeadScoreWarps>
@@ -722,10 +793,14 @@ __device__ int score_head_stream(const StoreView &s, int layer, const T *__restr
 #pragma unroll
                 for (int cc = 0; cc < CPL; ++cc) {
                     const uint4 raw = *reinterpret_cast<const uint4 *>(chunk + p * Gm::kRecBytes + (cl + cc * LPP) * 16);
+#ifdef FC_SCORE_SKIP_MATH  // profiling variant: the ring without the dot products
+                    acc += __uint_as_float(raw.x & 0x3f000000u);
+#else
                     float f[EPC];
                     chunk_to_f<T>(raw, f);
 #pragma unroll
                     for (int e = 0; e < EPC; ++e) acc = fmaf(f[e], coef[cc][e], acc);
+#endif
                 }
             }
             v[r] = acc;
@@ -847,6 +922,63 @@ score_head_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t
 // warps 0..NWA-1 attend exactly as attn_kernel (attend_head_cta); the ring
 // reuses the scoring ring / keys.  Same results as fc_score_select followed
 // by fc_sparse_decode (the attention reads the selection just written).
+// Next-layer summary warm-up (AttnArgs::pf_cap).  With unstable heads spread
+// over every layer, a plain step's fused launch mixes scored heads (summaries
+// + pages: 2 MB at config 2) and unscored ones (pages: 1 MB); one CTA per
+// head, so the scored CTAs are the layer's critical path while the others sit
+// idle after their pages.  Those idle CTAs here pull the NEXT layer's due
+// summaries into L2 (cp.async.bulk.prefetch.L2), so that layer's scored CTAs
+// stream their summaries at L2 rather than HBM rate.  Nothing a launch writes
+// is in those records except the appended page, which is never scored (the
+// last page is pinned), so the warm-up reads final data.  The next layer of
+// layer L-1 is layer 0 of the next step (step + 1).  `ord` / `n_pf` = this
+// CTA's ordinal among the launch's prefetching CTAs / their number; every
+// prefetching CTA takes an equal share of the due pages.  Thread 0 only.
+static constexpr int64_t kSummaryPrefetchCap = 48ll << 20;  // L2 = 126 MB: leave room for the pages streaming by
+static int64_t g_summary_prefetch_cap = kSummaryPrefetchCap;
+template <typename T, int D>
+__device__ void prefetch_next_summaries(const StoreView &s, int layer, const uint8_t *__restrict__ unstable,
+                                        int period, int topk, int extra_tokens, int batch, int ord, int n_pf,
+                                        int64_t cap) {
+    using Gm = ScoreGeom<T, D>;
+    int nl = layer + 1, step = *s.step;
+    if (nl == s.L) { nl = 0; ++step; }
+    const bool all_due = step % period == 0;
+    int n_due = 0;
+    for (int h = 0; h < s.H; ++h) n_due += (all_due || unstable[nl * s.H + h]) ? 1 : 0;
+    if (n_due == 0) return;
+    // candidate pages per row (every due head of a row has the same count)
+    int64_t total = 0;
+    for (int b = 0; b < batch; ++b) {
+        const int n_tok = s.seq_len[b] + extra_tokens;
+        const int np = n_tok > 0 ? (n_tok + s.PS - 1) / s.PS : 0;
+        if (np > topk) total += (int64_t)(np - 1) * n_due;
+    }
+    if (total == 0 || total * Gm::kRecBytes > cap) return;
+    int64_t lo = total * ord / n_pf;
+    const int64_t hi = total * (ord + 1) / n_pf;
+    int64_t base = 0;
+    for (int b = 0; b < batch && lo < hi; ++b) {
+        const int n_tok = s.seq_len[b] + extra_tokens;
+        const int np = n_tok > 0 ? (n_tok + s.PS - 1) / s.PS : 0;
+        if (np <= topk) continue;
+        const int cand = np - 1;
+        for (int h = 0; h < s.H && lo < hi; ++h) {
+            if (!(all_due || unstable[nl * s.H + h])) continue;
+            if (lo < base + cand) {
+                const int p0 = (int)(lo - base);
+                const int p1 = (int)(hi - base < cand ? hi - base : cand);
+                const char *src = reinterpret_cast<const char *>(s.summ) +
+                                  ((int64_t)s.hix(b, nl, h) * s.NCAP + p0) * Gm::kRecBytes;
+                for (int64_t off = 0, n = (int64_t)(p1 - p0) * Gm::kRecBytes; off < n; off += 65536)
+                    bulk_prefetch_l2(src + off, (uint32_t)(n - off < 65536 ? n - off : 65536));
+                lo = base + p1;
+            }
+            base += cand;
+        }
+    }
+}
+
 template <int NWS, int NWA>
 struct RegSplit {  // registers per thread after the hand-over (multiples of 8)
     static constexpr int kBase = 65536 / (NWS * 32) > 255 ? 255 : 65536 / (NWS * 32);
@@ -873,6 +1005,8 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
     __shared__ __align__(8) uint64_t abars[NWA * NST];
     __shared__ float s_wm[NWA][16], s_wl[NWA][16];
     griddep_launch_dependents();
+    unsigned long long *satr = g_sa_trace;
+    if (satr && threadIdx.x == 0) satr[blockIdx.x * 4] = gtimer_s();
     // S CTAs (a cluster) per head: every rank scores its share of the pages
     // into rank 0's keys (DSMEM), rank 0 selects, every rank attends its
     // share of the selection, rank 0 merges the ranks' states (DSMEM)
@@ -930,7 +1064,25 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
     // the CTA's state for the cluster merge lives past the attention scratch
     float *cstate = reinterpret_cast<float *>(dsm) + (size_t)NWA * s.G * D;
     if constexpr (!CL) {
+        if (satr && threadIdx.x == 0) satr[blockIdx.x * 4 + 1] = gtimer_s();
         attend_head_cta<T, D, NST, NWA>(s, a, bh, dsm, abars, s_wm, s_wl, s_q, 1);
+        if (satr && threadIdx.x == 0) satr[blockIdx.x * 4 + 2] = gtimer_s();
+        if (a.pf_cap > 0 && threadIdx.x == 0) {
+            const int step = *s.step;
+            auto due = [&](int hh) { return force_due || unstable[layer * s.H + hh] || step % period == 0; };
+            if (!due(h)) {
+                int nnd = 0, before = 0;
+                for (int hh = 0; hh < s.H; ++hh) {
+                    const bool nd = !due(hh);
+                    nnd += nd;
+                    before += nd && hh < h;
+                }
+                const int batch = gridDim.x / s.H;
+                prefetch_next_summaries<T, D>(s, layer, unstable, period, topk, extra_tokens, batch,
+                                              b * nnd + before, batch * nnd, a.pf_cap);
+            }
+        }
+        if (satr && threadIdx.x == 0) satr[blockIdx.x * 4 + 3] = gtimer_s();
     } else {
         // (only attending warps get here when NWS > NWA)
         const int n_att = attend_head_cta<T, D, NST, NWA>(s, a, bh, dsm, abars, s_wm, s_wl, s_q, 1, Sh, rank,
@@ -941,6 +1093,274 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
         // rank 0 done reading every rank's shared memory
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
+}
+
+// ---------------------------------------------------------------------------
+// Balanced fused score + select + attend (fc_score_attend_balanced).
+//
+// The head-aligned fused kernel gives each head ONE CTA for its scoring and
+// its attention.  When only some heads of a layer are due (a plain step with
+// the unstable heads spread over the layers: 2 of 8 KV heads at config 2), a
+// scored CTA streams its summaries (1 MB at 32k) and then its pages (1 MB)
+// while an unscored CTA streams only its pages: the layer takes the time of
+// the scored CTA, ~2x the unscored one (45 vs 25 us, scripts/spread_probe.py).
+// Here every CTA of a one-wave grid (max(heads, SMs) CTAs, all co-resident)
+// first scores an equal share of the concatenation of the due heads'
+// candidate pages (score_range, as score_select_kernel), publishing each
+// finished head segment with a release counter; then CTA i < heads attends
+// head i: an unscored head at once, a scored head after its owner CTA (CTA
+// i itself) has waited for every segment of its scores, selected from them
+// and written the selection (the keys alias the attention ring).  The
+// scoring work is spread over every SM, so the due summaries stream at the
+// whole GPU's rate instead of one SM's.  Results: the same per-page scores
+// and selections as fc_score_select's balanced kernel (same score_range),
+// the same attention as fc_sparse_decode (attend_head_cta).
+// Requires every CTA co-resident (the owners wait on the others): the
+// launcher checks the occupancy.  bf16 only (8 warps score and attend).
+#ifndef FC_BAL_ROUNDS
+#define FC_BAL_ROUNDS 32
+#endif
+template <typename T, int D, int NST, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+score_attend_bal_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t *__restrict__ unstable,
+                        int period, int force_due, int topk, int extra_tokens, float *scores, int32_t *counters,
+                        int n_heads, int kv_prefetch, AttnArgs a) {
+    static_assert(NW * 32 == kScoreThreads, "the scoring phase runs on kScoreThreads threads");
+    using Gm = ScoreGeom<T, D>;
+    constexpr size_t kRing = (size_t)NW * NST * AttnGeom<T, D>::kPageBytes;
+    // dynamic: ring [NW][NST][page] (the selecting CTA's keys alias it) | prefix [n_heads + 1]
+    extern __shared__ __align__(128) char dsm[];
+    __shared__ float w[2 * D];
+    __shared__ int s_wsum[NW];
+    __shared__ __align__(8) uint64_t abars[NW * NST];
+    __shared__ float s_wm[NW][16], s_wl[NW][16];
+    __shared__ __align__(8) uint64_t stage_bar;
+    griddep_launch_dependents();
+    unsigned long long *satr = g_sa_trace;
+    if (satr && threadIdx.x == 0) satr[blockIdx.x * 8] = gtimer_s();
+    // without kv_prefetch the previous launch may write this layer's
+    // selection / seq_len: wait before reading anything
+    if (!kv_prefetch) griddep_wait();
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    int *prefix = reinterpret_cast<int *>(dsm + kRing);
+    uint32_t *keys = reinterpret_cast<uint32_t *>(dsm);
+    const int step = *s.step;
+    auto is_due = [&](int h) { return force_due || unstable[layer * s.H + h] || step % period == 0; };
+    auto pages_of = [&](int b) {
+        const int n_tok = s.seq_len[b] + extra_tokens;
+        return n_tok > 0 ? (n_tok + s.PS - 1) / s.PS : 0;
+    };
+    // ---- candidate counts of the due heads (the last page is pinned) and their prefix
+    {
+        int carry = 0;
+        for (int c0 = 0; c0 < n_heads; c0 += blockDim.x) {
+            const int bh = c0 + tid;
+            int cnt = 0;
+            if (bh < n_heads && is_due(bh % s.H)) {
+                const int np = pages_of(bh / s.H);
+                cnt = np > topk ? np - 1 : 0;
+            }
+            int x = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) s_wsum[wid] = x;
+            __syncthreads();
+            int before = carry, tot = 0;
+            for (int ww = 0; ww < NW; ++ww) {
+                if (ww < wid) before += s_wsum[ww];
+                tot += s_wsum[ww];
+            }
+            if (bh < n_heads) prefix[bh] = before + x - cnt;
+            carry += tot;
+            __syncthreads();
+        }
+        if (tid == 0) prefix[n_heads] = carry;
+        __syncthreads();
+    }
+    const int total = prefix[n_heads];
+    // 32 (d = 128): 16 KiB of loads in flight per warp; at most the lanes of a page
+    constexpr int RPI = FC_BAL_ROUNDS < Gm::kLanesPerPage ? FC_BAL_ROUNDS : Gm::kLanesPerPage;
+    int P = (total + gridDim.x - 1) / gridDim.x;
+    P = (P + 31) & ~31;  // equal shares over every CTA (a coarser grain leaves CTAs idle)
+    const int start = min(total, (int)blockIdx.x * P), end = min(total, start + P);
+    // head containing candidate position pos (the last with prefix <= pos)
+    auto head_of = [&](int pos) {
+        int lo = 0, hi = n_heads - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (prefix[mid] <= pos) lo = mid; else hi = mid - 1;
+        }
+        return lo;
+    };
+    auto rec_of = [&](int bh, int page) {
+        return reinterpret_cast<const char *>(s.summ) +
+               ((int64_t)s.hix(bh / s.H, layer, bh % s.H) * s.NCAP + page) * Gm::kRecBytes;
+    };
+    // Stage the head of this CTA's share into shared memory (the ring, idle
+    // until phase 2) with bulk copies issued BEFORE waiting for the previous
+    // launch: the summaries of this layer are final (the previous launch
+    // appends into its own layer, and a due head's last page is never
+    // scored), only q is not.  The rest of the share is read from global.
+    const int staged_end = min(end, start + (int)(kRing / Gm::kRecBytes));
+    if (tid == 0) {
+        mbar_init(&stage_bar, 1);
+        fence_mbar_init();
+        if (start < staged_end) {
+            mbar_arrive_expect_tx(&stage_bar, (uint32_t)(staged_end - start) * Gm::kRecBytes);
+            for (int pos = start; pos < staged_end;) {
+                const int bh = head_of(pos), seg = min(staged_end, prefix[bh + 1]);
+                const char *src = rec_of(bh, pos - prefix[bh]);
+                char *dst = dsm + (size_t)(pos - start) * Gm::kRecBytes;
+                for (int64_t off = 0, nb = (int64_t)(seg - pos) * Gm::kRecBytes; off < nb; off += 65536)
+                    bulk_g2s(dst + off, src + off, (uint32_t)(nb - off < 65536 ? nb - off : 65536), &stage_bar);
+                pos = seg;
+            }
+        }
+    }
+    if (satr && tid == 0) satr[blockIdx.x * 8 + 1] = gtimer_s();
+    if (kv_prefetch) griddep_wait();  // q comes from the previous launch
+    if (satr && tid == 0) satr[blockIdx.x * 8 + 2] = gtimer_s();
+    // ---- phase 1: this CTA's share of the due pages; each finished head segment is published
+    bool landed = false;
+    for (int pos = start; pos < end;) {
+        const int bh = head_of(pos), h_beg = prefix[bh], seg_end = min(end, prefix[bh + 1]);
+        const int b = bh / s.H, h = bh % s.H;
+        __syncthreads();  // w reuse
+        load_group_coeffs<T>(s, q, b, h, w);
+        __syncthreads();
+        float *row = scores + (int64_t)bh * s.NCAP - h_beg;  // indexed by candidate position
+        const int mid = max(pos, min(seg_end, staged_end));  // [pos, mid) staged, [mid, seg_end) from global
+        if (pos < mid) {
+            if (!landed) {
+                mbar_wait(&stage_bar, 0);
+                landed = true;
+                if (satr && tid == 0) satr[blockIdx.x * 8 + 3] = gtimer_s();
+            }
+            score_span<T, D, RPI, true>(dsm + (size_t)(pos - start) * Gm::kRecBytes, mid - pos, w, row + pos);
+        }
+        if (mid < seg_end) score_span<T, D, RPI, false>(rec_of(bh, mid - h_beg), seg_end - mid, w, row + mid);
+        pos = seg_end;
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            atomicAdd(&counters[bh], 1);
+        }
+    }
+    if (satr && threadIdx.x == 0) satr[blockIdx.x * 8 + 4] = gtimer_s();
+    if ((int)blockIdx.x >= n_heads) return;
+    // ---- phase 2: CTA bh owns head bh
+    const int bh = blockIdx.x, b = bh / s.H, h = bh % s.H, hx = s.hix(b, layer, h);
+    const int n_pages = pages_of(b);
+    if (is_due(h) && n_pages > 0) {
+        int32_t *out = s.sel + (int64_t)hx * s.SELCAP;
+        if (n_pages <= topk) {  // budget covers every page
+            for (int i = tid; i < n_pages; i += blockDim.x) out[i] = i;
+            if (tid == 0) s.n_sel[hx] = n_pages;
+        } else {
+            const int h_beg = prefix[bh], h_end = prefix[bh + 1], n_cand = h_end - h_beg;
+            const int expect = (h_end - 1) / P - h_beg / P + 1;  // CTAs that scored a segment of it
+            float *row = scores + (int64_t)bh * s.NCAP;
+            if (tid == 0) {
+                int got;
+                while (true) {
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(got) : "l"(counters + bh) : "memory");
+                    if (got >= expect) break;
+                    __nanosleep(64);
+                }
+                if (satr) satr[blockIdx.x * 8 + 5] = gtimer_s();
+                counters[bh] = 0;  // self-resetting for the next launch
+                row[n_pages - 1] = -INFINITY;  // pinned page: not scored
+            }
+            __syncthreads();
+            for (int i0 = tid; i0 < n_cand; i0 += blockDim.x * 8) {
+                float v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    v[u] = i < n_cand ? __ldcg(row + i) : 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    if (i < n_cand) keys[i] = score_key(v[u]);
+                }
+            }
+            __syncthreads();
+            const int kprime = topk - 1;  // n_pages > topk, so kprime < n_cand
+            if (kprime > 0) block_select<kScoreThreads>(keys, n_cand, kprime, out);
+            if (tid == 0) {
+                out[kprime] = n_pages - 1;
+                s.n_sel[hx] = topk;
+            }
+        }
+        __syncthreads();  // the selection is written; the keys are dead (the ring reuses them)
+    }
+    if (satr && threadIdx.x == 0) satr[blockIdx.x * 8 + 6] = gtimer_s();
+    attend_head_cta<T, D, NST, NW>(s, a, bh, dsm, abars, s_wm, s_wl, nullptr, 1);
+    if (satr && threadIdx.x == 0) satr[blockIdx.x * 8 + 7] = gtimer_s();
+}
+
+template <typename T, int D, int NST, int NW>
+static size_t score_attend_bal_smem(int n_heads) {
+    return (size_t)NW * NST * AttnGeom<T, D>::kPageBytes + (size_t)(n_heads + 1) * sizeof(int);
+}
+
+// CTAs of the balanced fused launch for this batch, 0 if it does not fit
+// (every CTA must be co-resident; the selection keys must fit in the ring)
+template <typename T, int D, int NST, int NW>
+static int score_attend_bal_grid_t(const StoreView &s, int batch) {
+    const int n_heads = batch * s.H;
+    if (n_heads < 1 || (size_t)s.NCAP * 4 > (size_t)NW * NST * AttnGeom<T, D>::kPageBytes) return 0;
+    if (s.NCAP > kScoreThreads * kSelMaxKpt) return 0;
+    auto k = score_attend_bal_kernel<T, D, NST, NW>;
+    const size_t smem = score_attend_bal_smem<T, D, NST, NW>(n_heads);
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int occ = 0, dev = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NW * 32, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = n_heads > sms ? n_heads : sms;
+    return occ >= 1 && grid <= occ * sms ? grid : 0;
+}
+
+int score_attend_balanced_grid(const StoreView &s, int dtype, int batch) {
+    if (dtype != FC_BF16) return 0;
+    return s.D == 128 ? score_attend_bal_grid_t<__nv_bfloat16, 128, 3, 8>(s, batch)
+                      : score_attend_bal_grid_t<__nv_bfloat16, 64, 6, 8>(s, batch);
+}
+
+template <typename T, int D, int NST, int NW>
+static cudaError_t launch_score_attend_bal_t(const StoreView &s, int layer, const void *q, const uint8_t *unstable,
+                                             int period, int force_due, int topk, int extra, float *scores,
+                                             int32_t *counters, int batch, int kv_prefetch, const AttnArgs &a,
+                                             cudaStream_t st) {
+    const int grid = score_attend_bal_grid_t<T, D, NST, NW>(s, batch);
+    if (grid < 1) return cudaErrorInvalidConfiguration;
+    const int n_heads = batch * s.H;
+    return launch_pdl(score_attend_bal_kernel<T, D, NST, NW>, dim3(grid), dim3(NW * 32),
+                      score_attend_bal_smem<T, D, NST, NW>(n_heads), st, s, layer, (const T *)q, unstable, period,
+                      force_due, topk, extra, scores, counters, n_heads, kv_prefetch, a);
+}
+
+cudaError_t launch_score_attend_balanced(const StoreView &s, int dtype, int layer, const void *q,
+                                         const uint8_t *unstable, int period, int force_due, int topk, int extra,
+                                         float *scores, int32_t *counters, int batch, int kv_prefetch,
+                                         const AttnArgs &a, cudaStream_t st) {
+    if (dtype != FC_BF16) return cudaErrorInvalidConfiguration;
+    if (s.D == 128)
+        return launch_score_attend_bal_t<__nv_bfloat16, 128, 3, 8>(
+            s, layer, q, unstable, period, force_due, topk, extra, scores, counters, batch, kv_prefetch, a, st);
+    return launch_score_attend_bal_t<__nv_bfloat16, 64, 6, 8>(s, layer, q, unstable, period, force_due, topk, extra,
+                                                              scores, counters, batch, kv_prefetch, a, st);
 }
 
 // standalone select over caller scores: grid n_heads, block kScoreThreads
@@ -1023,15 +1443,20 @@ static cudaError_t launch_score_t(const StoreView &s, int layer, const void *q,
     const size_t smem = (do_select ? (size_t)s.NCAP * sizeof(uint32_t) : 0) + (size_t)(n_heads + 1) * sizeof(int);
     auto kern = score_select_kernel<T, D>;
     static size_t cached_smem = (size_t)-1;
-    static int grid = 0;
-    if (cached_smem != smem) {  // one full wave at the occupancy this smem allows
+    static int grid = 0, cached_cps = -1;
+    if (cached_smem != smem || cached_cps != g_score_ctas_per_sm) {  // one full wave at the occupancy this smem allows
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        // the SM's largest shared-memory split: the attention launch that
+        // follows (PDL) can then co-reside with this one
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         int occ = 0, dev = 0, sms = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kScoreThreads, smem);
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_score_ctas_per_sm > 0 && g_score_ctas_per_sm < occ) occ = g_score_ctas_per_sm;
         grid = (occ < 1 ? 1 : occ) * sms;
         cached_smem = smem;
+        cached_cps = g_score_ctas_per_sm;
     }
     return launch_pdl(kern, dim3(grid), dim3(kScoreThreads), smem, st, s, layer, (const T *)q, unstable,
                       period, force_due, topk, extra, scores, counters, do_select, n_heads, kv_prefetch);
@@ -1140,8 +1565,10 @@ static cudaError_t launch_score_attend_t(const StoreView &s, int layer, const vo
     if (S > 1)
         return cudaLaunchKernelEx(&cfg, score_attend_kernel<T, D, NST, NWA, NWS, true>, s, layer, (const T *)q,
                                   unstable, period, force_due, topk, extra, scores, kv_prefetch, a, S);
+    AttnArgs a1 = a;
+    a1.pf_cap = g_summary_prefetch_cap;
     return cudaLaunchKernelEx(&cfg, score_attend_kernel<T, D, NST, NWA, NWS, false>, s, layer, (const T *)q, unstable,
-                              period, force_due, topk, extra, scores, kv_prefetch, a, 1);
+                              period, force_due, topk, extra, scores, kv_prefetch, a1, 1);
 }
 
 // mixed clusters (fc_score_attend_map): n_ctas CTAs in clusters of S (a
@@ -1247,6 +1674,12 @@ cudaError_t launch_score_attend_map(const StoreView &s, int dtype, int layer, co
 }
 
 void set_score_mode(int m) { g_score_mode = m; }
+void set_score_ctas_per_sm(int n) { g_score_ctas_per_sm = n; }
+void set_summary_prefetch_cap(int64_t bytes) { g_summary_prefetch_cap = bytes < 0 ? kSummaryPrefetchCap : bytes; }
+
+cudaError_t set_sa_trace(void *p) {
+    return cudaMemcpyToSymbol(g_sa_trace, &p, sizeof(p));
+}
 
 cudaError_t set_score_trace(void *p) {
     return cudaMemcpyToSymbol(g_score_trace, &p, sizeof(p));

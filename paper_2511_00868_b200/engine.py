@@ -86,6 +86,12 @@ class DecodeEngine:
         # at long context: config 4; fc_score_attend_map)
         self.mixed_clusters = True
         self._mixed: dict = {}
+        # plain steps of layers where only some heads are due (the unstable
+        # heads spread over the layers): the due heads' scoring spread over
+        # every SM, then one CTA per head selects and attends
+        # (fc_score_attend_balanced; 37.5 vs 45 us per layer at config 2 with
+        # 2 of 8 KV heads unstable)
+        self.balanced_scoring = True
         # profiling: score every head every step and record
         # the selections on the device (trace.TraceRecorder)
         self.score_all_heads = False
@@ -255,6 +261,14 @@ class DecodeEngine:
         while layer < self.L:
             recycle = recycles(layer)
             scored = scores(layer)
+            if scored and not recycle and self._use_balanced(layer, rerank, force_due):
+                st.score_attend_balanced(layer, self.q[layer], self.unstable, self.R, self.K, self.out[layer],
+                                         self.B, extra_tokens=1, kv_prefetch=layer > 0, k_new=self.k_new[layer],
+                                         v_new=self.v_new[layer], attend_appended=False)
+                if self.after_layer is not None:
+                    self.after_layer(layer)
+                layer += 1
+                continue
             if scored and not recycle and use_fused:
                 # one launch: every head's CTA scores, selects and attends
                 plan = self._mixed_plan(layer) if not (rerank or force_due) else None
@@ -317,6 +331,17 @@ class DecodeEngine:
             self.recorder.capture()
         if self.tiering:  # write-once offload of the page that just filled
             st.offload_filled(self.tier.host, self.unstable, self.tier.slow_resident, self.B)
+
+    def _use_balanced(self, layer: int, rerank: bool, force_due: bool) -> bool:
+        # plain step, some but not all of the layer's heads due
+        if not self.balanced_scoring or rerank or force_due:
+            return False
+        n_due = sum(self.profile.is_unstable(HeadId(layer, h)) for h in range(self.H))
+        # (only where the fused kernel gives every head one CTA: smaller batches
+        # split heads over clusters, and config 4's mixed clusters beat this
+        # there: 6.1k vs 5.1k tokens/s)
+        return (0 < n_due < self.H and self.store.score_attend_supported(self.B) == 1
+                and self.store.score_attend_balanced_supported(self.B) > 0)
 
     def _mixed_plan(self, layer: int):
         # heads due at a plain step = the layer's unstable heads; the map is
@@ -429,7 +454,8 @@ class DecodeEngine:
         while layer < self.L:
             if recycles(layer):
                 n += 2  # recycle + fetch
-            if scores(layer) and not recycles(layer) and use_fused:
+            if scores(layer) and not recycles(layer) and (
+                    use_fused or (not self.score_all_heads and self._use_balanced(layer, rerank, False))):
                 n += 1
                 layer += 1
                 continue

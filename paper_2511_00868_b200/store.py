@@ -225,6 +225,28 @@ class KVStore:
             int(kv_prefetch), self.scores.data_ptr(), _ptr(k_new), _ptr(v_new), out.data_ptr(), _ptr(lse),
             scale, int(attend_appended), batch, self.stream()), "fc_score_attend")
 
+    def score_attend_balanced_supported(self, batch: int) -> int:
+        """Grid of fc_score_attend_balanced for this batch (0: unsupported)."""
+        cache = self.__dict__.setdefault("_bal_grid", {})
+        if batch not in cache:
+            cache[batch] = int(self.lib.fc_score_attend_balanced_supported(self.cptr, batch))
+        return cache[batch]
+
+    def score_attend_balanced(self, layer: int, q: torch.Tensor, unstable: torch.Tensor, period: int, topk: int,
+                              out: torch.Tensor, batch: int, *, force_due: bool = False, extra_tokens: int = 1,
+                              kv_prefetch: bool = False, k_new: torch.Tensor | None = None,
+                              v_new: torch.Tensor | None = None, lse: torch.Tensor | None = None,
+                              scale: float | None = None, attend_appended: bool = False) -> None:
+        """fc_score_attend_balanced: the due heads' scoring spread over every
+        SM, then per head selection and attention (same results as
+        fc_score_select's balanced kernel followed by fc_sparse_decode)."""
+        scale = 1.0 / math.sqrt(self.D) if scale is None else scale
+        _lib.check(self.lib.fc_score_attend_balanced(
+            self.cptr, layer, q.data_ptr(), unstable.data_ptr(), period, int(force_due), topk, extra_tokens,
+            int(kv_prefetch), self.scores.data_ptr(), self.score_counters.data_ptr(), _ptr(k_new), _ptr(v_new),
+            out.data_ptr(), _ptr(lse), scale, int(attend_appended), batch, self.stream()),
+            "fc_score_attend_balanced")
+
     def score_attend_map_fits(self, n_ctas: int, cluster: int) -> bool:
         cache = self.__dict__.setdefault("_map_fits", {})
         if (n_ctas, cluster) not in cache:

@@ -25,11 +25,15 @@ def _round(x, dtype):
 
 
 def run_engine_vs_oracle(*, B, L, H, G, D, T0, steps, K, R, frac, dtype, seed, use_graph,
-                         ragged=False, tiering=False, run_kernel=None, fused=False):
+                         ragged=False, tiering=False, run_kernel=None, fused=False, spread=0):
+    from paper_2511_00868_b200.config import HeadId
     from paper_2511_00868_b200.engine import DecodeEngine
     from paper_2511_00868_b200.stability import HeadProfile
     rng = np.random.default_rng(seed)
     prof = HeadProfile.first_n(L, H, frac)
+    if spread:  # the first `spread` KV heads of every layer unstable (mixed layers)
+        prof = HeadProfile(model_id="spread", n_layers=L, n_heads_per_layer=H, fraction=spread / H,
+                           unstable=tuple(HeadId(l, h) for l in range(L) for h in range(spread)))
     unstable = prof.mask()
     eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D,
                        ctx_cap_tokens=T0 + steps + 64, topk_pages=K, rerank_period=R,
@@ -190,6 +194,75 @@ def test_engine_fused_score_attend_matches_oracle(head_aligned_scoring, dtype, D
                                             ragged=True, fused=True)
     assert eng.launches_per_step(1) == 3  # fused layer 0, attention layer 1, advance
     assert ties <= 2
+
+
+@pytest.mark.parametrize("D,G,spread", [(128, 4, 1), (128, 7, 2), (64, 4, 3)])
+def test_engine_balanced_scoring_matches_oracle(head_aligned_scoring, D, G, spread):
+    """fc_score_attend_balanced (plain steps of layers with some heads due):
+    the due heads' pages scored in equal shares by every CTA of a one-wave
+    grid, then each head's CTA selects (when due) and attends."""
+    worst, ties, eng = run_engine_vs_oracle(B=3, L=2, H=4, G=G, D=D, T0=1500, steps=10, K=8,
+                                            R=4, frac=0.5, dtype=torch.bfloat16, seed=23, use_graph=True,
+                                            ragged=True, fused=True, spread=spread)
+    assert eng._use_balanced(0, False, False) and not eng._use_balanced(0, True, False)
+    assert ties <= 2
+
+
+def test_engine_balanced_scoring_tiered(head_aligned_scoring):
+    run_engine_vs_oracle(B=2, L=2, H=4, G=4, D=128, T0=700, steps=16, K=6, R=4, frac=0.5,
+                         dtype=torch.bfloat16, seed=24, use_graph=True, tiering=True, fused=True, spread=2)
+
+
+def test_balanced_bitwise_equals_two_launch():
+    """At config 2's batch (16 rows x 8 KV heads, 2 due per layer) the
+    balanced fused launch gives the same scores, selections, summaries and
+    outputs, bit for bit, as the balanced scoring kernel followed by
+    fc_sparse_decode (same per-page score arithmetic, same attention)."""
+    import ctypes
+    from paper_2511_00868_b200 import _lib
+    from paper_2511_00868_b200.config import HeadId
+    from paper_2511_00868_b200.engine import DecodeEngine
+    from paper_2511_00868_b200.stability import HeadProfile
+    from paper_2511_00868_b200.synthetic import device_normal
+    B, L, H, G, D, T, K, R = 16, 2, 8, 4, 128, 6000, 32, 16
+    prof = HeadProfile(model_id="spread", n_layers=L, n_heads_per_layer=H, fraction=0.25,
+                       unstable=tuple(HeadId(l, h) for l in range(L) for h in range(2)))
+    eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=T + 64,
+                       topk_pages=K, rerank_period=R, profile=prof)
+    assert eng.store.score_attend_balanced_supported(B) >= B * H
+    for b in range(B):
+        for l in range(L):
+            eng.prefill_layer(b, l, device_normal((H, T - 37 * b, D), seed=3 * b + l),
+                              device_normal((H, T - 37 * b, D), seed=100 + 3 * b + l), alloc=(l == 0))
+    eng.q.copy_(device_normal(tuple(eng.q.shape), seed=5))
+    eng.step()  # initial selection of every head
+    st = eng.store
+    eng.q.copy_(device_normal(tuple(eng.q.shape), seed=6))
+    eng.k_new.copy_(device_normal(tuple(eng.k_new.shape), seed=7))
+    eng.v_new.copy_(device_normal(tuple(eng.v_new.shape), seed=8))
+    snap = [t.clone() for t in (st.sel, st.n_sel, st.summaries, st.kv_pool)]
+    lib = _lib.load()
+    lib.fc_debug_score_mode.argtypes = [ctypes.c_int]
+    lib.fc_debug_score_mode(0)  # the balanced scoring kernel
+    try:
+        for l in range(L):
+            st.score_select(l, eng.q[l], eng.unstable, R, K, B, extra_tokens=1, kv_prefetch=l > 0)
+            st.sparse_decode(l, eng.q[l], eng.out[l], B, max_pages=eng.att_bound, extra_tokens=1,
+                             attend_appended=False, k_new=eng.k_new[l], v_new=eng.v_new[l])
+    finally:
+        lib.fc_debug_score_mode(-1)
+    torch.cuda.synchronize()
+    ref = [t.clone() for t in (st.sel, st.n_sel, st.summaries, eng.out, st.scores)]
+    for t, v in zip((st.sel, st.n_sel, st.summaries, st.kv_pool), snap):
+        t.copy_(v)
+    for l in range(L):
+        st.score_attend_balanced(l, eng.q[l], eng.unstable, R, K, eng.out[l], B, extra_tokens=1,
+                                 kv_prefetch=l > 0, k_new=eng.k_new[l], v_new=eng.v_new[l])
+    torch.cuda.synchronize()
+    st.check_errors()
+    for got, want in zip((st.sel, st.n_sel, st.summaries, eng.out, st.scores), ref):
+        assert torch.equal(got, want)
+    assert int(st.score_counters.abs().sum()) == 0  # left zero for the next launch
 
 
 def test_engine_fused_tiered(head_aligned_scoring):
