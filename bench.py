@@ -69,6 +69,10 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--phases", choices=["aligned", "staggered"], default="aligned",
+                    help="request phases: aligned (all rows admitted together, rerank on the same "
+                         "step) or staggered (row b starts at its own t = 1 + b: each step ~B/R rows "
+                         "rerank, as requests admitted at different times do)")
     ap.add_argument("--batch", type=int, default=CFG2["batch"])
     ap.add_argument("--ctx", type=int, default=CFG2["ctx"])
     ap.add_argument("--layers", type=int, default=CFG2["layers"])
@@ -271,6 +275,9 @@ def run_ours(args, cfg):
             k, v = srcs[(b * L + l) % 4]
             eng.prefill_layer(b, l, k, v, alloc=(l == 0))
     del srcs
+    if args.phases == "staggered":
+        for b in range(B):
+            eng.set_row_step(b, 1 + b % R)
     torch.cuda.synchronize(dev)
     eng.store.check_errors()
     # per-step inputs: NQ distinct sets, copied into the static graph buffers each step
@@ -291,9 +298,10 @@ def run_ours(args, cfg):
     for i in range(args.warmup):
         feed(i)
         eng.step()
-    eng.capture_graphs()  # both step graphs exist before timing
+    eng.capture_graphs(sorted({eng.step_kind(eng.t + i) for i in range(max(args.steps, R))}))
     torch.cuda.synchronize(dev)
     eng.store.check_errors()
+    stats0 = eng.store.scoring_stats()
 
     # ---- timed region: device-resident inputs
     launches = 0
@@ -320,6 +328,10 @@ def run_ours(args, cfg):
     ms = max_over_ranks(ms, world)
     eng.store.check_errors()
     value = world * B * args.steps / (ms / 1e3)
+    stats1 = eng.store.scoring_stats()
+    counters = {k: stats1[k] - stats0[k] for k in stats1}
+    counters["ratio"] = counters["score_evals"] / max(1, counters["score_evals_naive"])
+    counters["source"] = "device counters (FC_STAT_*) over the timed steps: heads scored / L*H per decoding row"
 
     # ---- roofline of the dominant kernel (fc_sparse_decode): its launches for
     # the 32 layers back to back (as inside the step, distinct data per layer,
@@ -447,8 +459,10 @@ def run_ours(args, cfg):
                                       "first round(u*L*H) flat heads (the reference fixture, conftest.py:21-33)"),
                    **({"mixed_clusters": False} if os.environ.get("FC_MIXED") == "0" else {}),
                    **({"fused_score_attend": False} if os.environ.get("FC_FUSED") == "0" else {}),
-                   **({"share": cfg["share"]} if "share" in cfg else {})},
+                   **({"share": cfg["share"]} if "share" in cfg else {}),
+                   "phases": args.phases},
         "gpu_launches": launches,
+        "scoring_counters": counters,
         "step_ms": step_stats,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _traffic(cfg.get("key", "config2") + "/attn_kernel"), "kernel": "fc_sparse_decode (attn_kernel)",

@@ -80,7 +80,32 @@ typedef struct fc_store {
     int32_t *free_top;   /* [1]                                                  */
     int32_t *step;       /* [1] decode step t of the upcoming step (1-based)     */
     uint32_t *error_word;/* [1] sticky FC_ERR_* bits                             */
+    /* per-request decode state (optional; NULL = every row in phase, none held) */
+    int32_t *row_phase;  /* [B_cap] row b's decode step t_b = *step + row_phase[b]:
+                            each request reranks at its own t_b % R == 0
+                            (simulator.py:437-439, per-request r.t)          */
+    uint8_t *row_hold;   /* [B_cap] FC_HOLD_* mode of row b for the next launches:
+                            the reload pause of simulator.py:321-323,542     */
+    uint64_t *stats;     /* [FC_STATS_N] device counters (Metrics,
+                            simulator.py:87-131), or NULL                    */
 } fc_store;
+
+/* row_hold modes (the reloading request pauses; the others decode) */
+#define FC_HOLD_NONE    0   /* decode normally                                   */
+#define FC_HOLD_RERANK  3   /* rerank step of a two-tier row whose promoted pages
+                               arrive on a side stream: score / select / recycle,
+                               but no attention and no advance (t_b stays)       */
+#define FC_HOLD_WAIT    1   /* reload in flight: nothing runs for the row        */
+#define FC_HOLD_RESUME  2   /* reload landed: attend token t_b over the selection
+                               made at the rerank step (stable heads not re-due) */
+
+/* stats counters (each += per step by the kernels that do the work) */
+#define FC_STAT_SCORE_EVALS        0  /* heads scored (Metrics.score_evals)        */
+#define FC_STAT_SCORE_EVALS_NAIVE  1  /* L*H per decoding row (score_evals_naive)  */
+#define FC_STAT_LAYER_SKIPS        2  /* (row, layer) with no due head
+                                         (layer_scoring_skips)                     */
+#define FC_STAT_HELD_ROW_STEPS     3  /* rows held for a reload (pause_steps)      */
+#define FC_STATS_N                 4
 
 /* library identity */
 const char *fc_version(void);
@@ -112,6 +137,14 @@ int fc_alloc_pages(const fc_store *s, int row, int first_page, int n_pages,
  * the simulator's "resident ∪ appended" (simulator.py:463-466,512), so a
  * selection row is always the complete attended set.  Advances *step. */
 int fc_step_advance(const fc_store *s, int batch, void *stream);
+
+/* fc_step_advance that also counts, into s->stats (when set), the step's
+ * layers with no due head per decoding row (Metrics.layer_scoring_skips,
+ * simulator.py:440-446; `unstable` [L][H] flags, rerank period R).  Both
+ * forms honour s->row_phase / s->row_hold: a held row keeps its length and
+ * its own step t_b (simulator.py:321-323 — a paused request does not step). */
+int fc_step_advance_counted(const fc_store *s, int batch, const uint8_t *unstable, int period,
+                            void *stream);
 
 /* ---- (1) KV append + per-page min/max summaries ------------------------ */
 

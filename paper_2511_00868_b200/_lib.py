@@ -14,7 +14,8 @@ import re
 
 from .errors import CudaError, UnsupportedError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libflexicache_b200.so")
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                        os.environ.get("FC_LIB_VARIANT", "libflexicache_b200.so"))  # (A/B builds, profiling)
 HEADER_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                            "include", "flexicache_b200.h")
 
@@ -28,6 +29,9 @@ FC_ERR_SEL_CAP = 16
 FC_ERR_DOUBLE_EVICT = 32
 FC_ERR_WRITE_TWICE = 64
 FC_ERR_TRACE_SHORT = 128
+FC_HOLD_NONE, FC_HOLD_WAIT, FC_HOLD_RESUME, FC_HOLD_RERANK = 0, 1, 2, 3
+FC_STAT_SCORE_EVALS, FC_STAT_SCORE_EVALS_NAIVE, FC_STAT_LAYER_SKIPS, FC_STAT_HELD_ROW_STEPS = 0, 1, 2, 3
+FC_STATS_N = 4
 
 _p = ctypes.c_void_p
 _i = ctypes.c_int
@@ -48,6 +52,7 @@ class FcStore(ctypes.Structure):
         ("kv_pool", _p), ("summaries", _p), ("table", _p), ("seq_len", _p),
         ("sel", _p), ("n_sel", _p), ("free_stack", _p), ("free_top", _p),
         ("step", _p), ("error_word", _p),
+        ("row_phase", _p), ("row_hold", _p), ("stats", _p),
     ]
 
 
@@ -57,6 +62,7 @@ _SIGNATURES = {
     "fc_alloc_pages": (_i, [_p, _i, _i, _i, _p]),
     "fc_free_row": (_i, [_p, _i, _p]),
     "fc_step_advance": (_i, [_p, _i, _p]),
+    "fc_step_advance_counted": (_i, [_p, _i, _p, _i, _p]),
     "fc_kv_prefill": (_i, [_p, _i, _i, _p, _p, _i, _p]),
     "fc_kv_append": (_i, [_p, _i, _p, _p, _i, _p]),
     "fc_kv_gather": (_i, [_p, _i, _i, _i, _i, _p, _p, _p]),

@@ -111,7 +111,7 @@ FC_DEVINL RunLayer run_plan(const StoreView &s, const RunArgs &a, int l, int nh,
         ntok[k] = 0; nsel[k] = 0;
         if (bh < nh) {
             const int b = bh / s.H, h = bh % s.H;
-            ntok[k] = s.seq_len[b] + a.extra_tokens;
+            ntok[k] = s.decodes(b) ? s.seq_len[b] + a.extra_tokens : 0;
             nsel[k] = s.n_sel[s.hix(b, l, h)];
         }
     }

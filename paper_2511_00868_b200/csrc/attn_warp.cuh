@@ -520,9 +520,11 @@ FC_DEVINL HeadInfo head_info(const StoreView &s, int layer, int extra_tokens, in
     HeadInfo hi;
     const int b = bh / s.H, h = bh % s.H;
     hi.hx = s.hix(b, layer, h);
-    hi.n_tok = s.seq_len[b] + extra_tokens;
-    hi.n_pages = hi.n_tok > 0 ? (hi.n_tok + kPageSize - 1) / kPageSize : 0;
+    // (every load issued before the hold test: it must not serialise them)
+    const int len = s.seq_len[b];
     hi.nsel = s.n_sel[hi.hx];
+    hi.n_tok = s.decodes(b) ? len + extra_tokens : 0;  // held rows (reload pause): nothing
+    hi.n_pages = hi.n_tok > 0 ? (hi.n_tok + kPageSize - 1) / kPageSize : 0;
     hi.hi = hi.nsel > 0 ? s.sel[(int64_t)hi.hx * s.SELCAP + hi.nsel - 1] : -1;
     int n_att = attend_appended ? hi.nsel + max(0, hi.n_pages - 1 - hi.hi) : hi.nsel;
     if (hi.n_tok <= 0) n_att = 0;

@@ -102,7 +102,14 @@ int fc_alloc_pages(const fc_store *s, int row, int first_page, int n_pages, void
 int fc_step_advance(const fc_store *s, int batch, void *stream) {
     FC_CHECK(check_store(s));
     if (batch < 0 || batch > s->batch_cap || batch > 1024) return invalid("batch out of range");
-    return cuda_status(launch_step_advance(make_view(s), batch, (cudaStream_t)stream));
+    return cuda_status(launch_step_advance(make_view(s), batch, nullptr, 1, (cudaStream_t)stream));
+}
+
+int fc_step_advance_counted(const fc_store *s, int batch, const uint8_t *unstable, int period, void *stream) {
+    FC_CHECK(check_store(s));
+    if (batch < 0 || batch > s->batch_cap || batch > 1024) return invalid("batch out of range");
+    if (!unstable || period < 1) return invalid("unstable flags and period >= 1 required");
+    return cuda_status(launch_step_advance(make_view(s), batch, unstable, period, (cudaStream_t)stream));
 }
 
 int fc_kv_prefill(const fc_store *s, int row, int layer, const void *k, const void *v, int n_tokens,

@@ -36,15 +36,31 @@ __global__ void alloc_pages_kernel(StoreView s, int row, int first_page, int n_p
 
 // One CTA of up to 1024 threads.  seq_len += 1 for rows [0, batch); rows that
 // now start a page get it for every (layer, head), in (row, layer, head) order.
-__global__ void step_advance_kernel(StoreView s, int batch) {
+// Rows held for a reload (row_hold WAIT / RERANK) keep their length and their
+// own step t_b (row_phase -= 1).  With s.stats: score_evals_naive += L*H per
+// decoding row, layer_scoring_skips += its layers with no due head (needs
+// `unstable`), held-row steps += 1 per held row (Metrics, simulator.py:87-131).
+__global__ void step_advance_kernel(StoreView s, int batch, const uint8_t *unstable, int period) {
     using Scan = cub::BlockScan<int, 1024>;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ int rows_needing[1024];
     __shared__ int s_total;
     __shared__ int s_fail;
+    __shared__ int s_no_unstable;  // layers with no unstable head (skipped at a plain step)
     const int b = threadIdx.x;
     int need = 0, len = 0;
-    if (b < batch && s.seq_len[b] >= 0) {  // seq_len < 0: a free row (serving loop), left alone
+    if (s.stats && unstable) {
+        if (threadIdx.x == 0) s_no_unstable = 0;
+        __syncthreads();
+        for (int l = threadIdx.x; l < s.L; l += blockDim.x) {
+            bool any = false;
+            for (int h = 0; h < s.H; ++h) any |= unstable[l * s.H + h] != 0;
+            if (!any) atomicAdd(&s_no_unstable, 1);
+        }
+    }
+    const bool active = b < batch && s.seq_len[b] >= 0;  // seq_len < 0: a free row (serving loop), left alone
+    const bool held = active && !s.decodes(b);
+    if (active && !held) {
         len = s.seq_len[b] + 1;
         if (len % s.PS == 0) {
             if (len / s.PS < s.NCAP) need = 1;
@@ -84,7 +100,20 @@ __global__ void step_advance_kernel(StoreView s, int batch) {
         }
     }
     __syncthreads();
-    if (b < batch && s.seq_len[b] >= 0) s.seq_len[b] = len;
+    if (active && !held) {
+        s.seq_len[b] = len;
+        if (s.stats) {
+            s.count(FC_STAT_SCORE_EVALS_NAIVE, (unsigned long long)LH);
+            // at the row's boundary every layer has a due head; otherwise the
+            // layers without an unstable head score nothing
+            if (unstable && !s.boundary(*s.step, b, period)) s.count(FC_STAT_LAYER_SKIPS, s_no_unstable);
+        }
+    }
+    if (held) {
+        if (s.row_phase) s.row_phase[b] -= 1;  // t_b stays: the row decodes token t_b later
+        s.count(FC_STAT_HELD_ROW_STEPS, 1);
+    }
+    __syncthreads();  // (every thread read *s.step above)
     if (threadIdx.x == 0) {
         if (!s_fail) *s.free_top = top - s_total * LH;
         *s.step += 1;
@@ -249,8 +278,9 @@ cudaError_t launch_alloc_pages(const StoreView &s, int row, int first, int n, cu
     return cudaGetLastError();
 }
 
-cudaError_t launch_step_advance(const StoreView &s, int batch, cudaStream_t st) {
-    step_advance_kernel<<<1, 1024, 0, st>>>(s, batch);
+cudaError_t launch_step_advance(const StoreView &s, int batch, const uint8_t *unstable, int period,
+                                cudaStream_t st) {
+    step_advance_kernel<<<1, 1024, 0, st>>>(s, batch, unstable, period);
     return cudaGetLastError();
 }
 

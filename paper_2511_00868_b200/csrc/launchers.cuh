@@ -60,7 +60,7 @@ int attn_persist_split(const StoreView &, int, int, int);
 cudaError_t launch_attn_persist(const StoreView &, int, const RunArgs &, int, cudaStream_t);
 
 cudaError_t launch_alloc_pages(const StoreView &, int, int, int, cudaStream_t);
-cudaError_t launch_step_advance(const StoreView &, int, cudaStream_t);
+cudaError_t launch_step_advance(const StoreView &, int, const uint8_t *, int, cudaStream_t);
 cudaError_t launch_free_row(const StoreView &, int, cudaStream_t);
 cudaError_t launch_evict_pages(const StoreView &, const int32_t *, int, cudaStream_t);
 cudaError_t launch_prefill(const StoreView &, int, int, int, const void *, const void *, int, cudaStream_t);

@@ -79,7 +79,7 @@ rerank_diff_kernel(StoreView s, int layer, const int32_t *__restrict__ old_sel,
     int32_t *cnt = ws.cnt(bh);
     // rows in row_skip still hold every page (post-prefill offload in flight):
     // their resident set is not the old selection, so nothing moves
-    const bool due = !unstable[layer * s.H + h] && (force_due || (*s.step % period == 0)) &&
+    const bool due = !unstable[layer * s.H + h] && (force_due || s.boundary(*s.step, b, period)) &&
                      !(row_skip && row_skip[b]);
     if (!due) {
         if (lane == 0) { cnt[0] = 0; cnt[1] = 0; cnt[2] = 0; }
@@ -429,7 +429,7 @@ offload_filled_kernel(StoreView s, char *host_pages, const uint8_t *unstable, ui
         const int b = u / LH, lh = u % LH;
         if (unstable[lh]) continue;
         const int len = s.seq_len[b];
-        if (len <= 0 || len % s.PS != 0) continue;
+        if (len <= 0 || len % s.PS != 0 || !s.decodes(b)) continue;  // (a held row filled nothing)
         const int page = len / s.PS - 1;
         const int64_t off = s.table_off(s.hix(b, lh / s.H, lh % s.H), page);
         const int blk = s.table[off];

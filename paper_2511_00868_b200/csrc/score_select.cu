@@ -525,7 +525,8 @@ score_select_kernel(StoreView s, int layer, const T *__restrict__ q,
                 const int n_pages = n_tok > 0 ? (n_tok + s.PS - 1) / s.PS : 0;
                 if (!do_select) {
                     cnt = n_pages;
-                } else if (force_due || unstable[layer * s.H + h] || step % period == 0) {
+                } else if (s.head_due(step, b, unstable[layer * s.H + h], period, force_due)) {
+                    if (blockIdx.x == 0 && n_pages > 0) s.count(FC_STAT_SCORE_EVALS, 1);
                     if (n_pages > topk) {
                         cnt = n_pages - 1;
                     } else if (blockIdx.x == 0 && n_pages > 0) {  // budget covers every page
@@ -728,10 +729,11 @@ __device__ int score_head_stream(const StoreView &s, int layer, const T *__restr
     if (trace && tid == 0) trace[blockIdx.x * 4] = gtimer_s();
     if (!kv_prefetch) griddep_wait();
     const int b = bh / s.H, h = bh % s.H;
-    const bool due = force_due || unstable[layer * s.H + h] || (*s.step % period == 0);
+    const bool due = s.head_due(*s.step, b, unstable[layer * s.H + h], period, force_due);
     const int n_tok = s.seq_len[b] + extra_tokens;
     const int n_pages = n_tok > 0 ? (n_tok + s.PS - 1) / s.PS : 0;
     const int hx = s.hix(b, layer, h);
+    if (due && n_pages > 0 && rank == 0 && tid == 0) s.count(FC_STAT_SCORE_EVALS, 1);
     if (!due || n_pages == 0) {
         if (kv_prefetch) griddep_wait();
         cluster_wait();
@@ -943,16 +945,17 @@ __device__ void prefetch_next_summaries(const StoreView &s, int layer, const uin
     using Gm = ScoreGeom<T, D>;
     int nl = layer + 1, step = *s.step;
     if (nl == s.L) { nl = 0; ++step; }
-    const bool all_due = step % period == 0;
-    int n_due = 0;
-    for (int h = 0; h < s.H; ++h) n_due += (all_due || unstable[nl * s.H + h]) ? 1 : 0;
-    if (n_due == 0) return;
-    // candidate pages per row (every due head of a row has the same count)
+    // (each row's own boundary: rows rerank at their own t_b)
+    auto due = [&](int b, int h) { return s.head_due(step, b, unstable[nl * s.H + h], period, false); };
+    // candidate pages of the due heads
     int64_t total = 0;
     for (int b = 0; b < batch; ++b) {
         const int n_tok = s.seq_len[b] + extra_tokens;
         const int np = n_tok > 0 ? (n_tok + s.PS - 1) / s.PS : 0;
-        if (np > topk) total += (int64_t)(np - 1) * n_due;
+        if (np <= topk) continue;
+        int n_due = 0;
+        for (int h = 0; h < s.H; ++h) n_due += due(b, h) ? 1 : 0;
+        total += (int64_t)(np - 1) * n_due;
     }
     if (total == 0 || total * Gm::kRecBytes > cap) return;
     int64_t lo = total * ord / n_pf;
@@ -964,7 +967,7 @@ __device__ void prefetch_next_summaries(const StoreView &s, int layer, const uin
         if (np <= topk) continue;
         const int cand = np - 1;
         for (int h = 0; h < s.H && lo < hi; ++h) {
-            if (!(all_due || unstable[nl * s.H + h])) continue;
+            if (!due(b, h)) continue;
             if (lo < base + cand) {
                 const int p0 = (int)(lo - base);
                 const int p1 = (int)(hi - base < cand ? hi - base : cand);
@@ -1069,17 +1072,19 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
         if (satr && threadIdx.x == 0) satr[blockIdx.x * 4 + 2] = gtimer_s();
         if (a.pf_cap > 0 && threadIdx.x == 0) {
             const int step = *s.step;
-            auto due = [&](int hh) { return force_due || unstable[layer * s.H + hh] || step % period == 0; };
-            if (!due(h)) {
-                int nnd = 0, before = 0;
-                for (int hh = 0; hh < s.H; ++hh) {
-                    const bool nd = !due(hh);
-                    nnd += nd;
-                    before += nd && hh < h;
-                }
+            auto due = [&](int bb, int hh) {
+                return s.head_due(step, bb, unstable[layer * s.H + hh], period, force_due);
+            };
+            if (!due(b, h)) {  // the heads not due share the prefetch: this one's ordinal among them
                 const int batch = gridDim.x / s.H;
+                int nnd = 0, before = 0;
+                for (int x = 0; x < batch * s.H; ++x) {
+                    const bool nd = !due(x / s.H, x % s.H);
+                    nnd += nd;
+                    before += nd && x < bh;
+                }
                 prefetch_next_summaries<T, D>(s, layer, unstable, period, topk, extra_tokens, batch,
-                                              b * nnd + before, batch * nnd, a.pf_cap);
+                                              before, nnd, a.pf_cap);
             }
         }
         if (satr && threadIdx.x == 0) satr[blockIdx.x * 4 + 3] = gtimer_s();
@@ -1145,7 +1150,9 @@ score_attend_bal_kernel(StoreView s, int layer, const T *__restrict__ q, const u
     int *prefix = reinterpret_cast<int *>(dsm + kRing);
     uint32_t *keys = reinterpret_cast<uint32_t *>(dsm);
     const int step = *s.step;
-    auto is_due = [&](int h) { return force_due || unstable[layer * s.H + h] || step % period == 0; };
+    auto is_due = [&](int bh) {
+        return s.head_due(step, bh / s.H, unstable[layer * s.H + bh % s.H], period, force_due);
+    };
     auto pages_of = [&](int b) {
         const int n_tok = s.seq_len[b] + extra_tokens;
         return n_tok > 0 ? (n_tok + s.PS - 1) / s.PS : 0;
@@ -1156,7 +1163,7 @@ score_attend_bal_kernel(StoreView s, int layer, const T *__restrict__ q, const u
         for (int c0 = 0; c0 < n_heads; c0 += blockDim.x) {
             const int bh = c0 + tid;
             int cnt = 0;
-            if (bh < n_heads && is_due(bh % s.H)) {
+            if (bh < n_heads && is_due(bh)) {
                 const int np = pages_of(bh / s.H);
                 cnt = np > topk ? np - 1 : 0;
             }
@@ -1254,7 +1261,8 @@ score_attend_bal_kernel(StoreView s, int layer, const T *__restrict__ q, const u
     // ---- phase 2: CTA bh owns head bh
     const int bh = blockIdx.x, b = bh / s.H, h = bh % s.H, hx = s.hix(b, layer, h);
     const int n_pages = pages_of(b);
-    if (is_due(h) && n_pages > 0) {
+    if (is_due(bh) && n_pages > 0) {
+        if (tid == 0) s.count(FC_STAT_SCORE_EVALS, 1);
         int32_t *out = s.sel + (int64_t)hx * s.SELCAP;
         if (n_pages <= topk) {  // budget covers every page
             for (int i = tid; i < n_pages; i += blockDim.x) out[i] = i;

@@ -81,8 +81,14 @@ attn_kernel(StoreView s, AttnArgs a, int S) {
     // previous kernel drains; only q and the new token wait.  A head the
     // preceding scoring launch does not select this step (early_unstable)
     // reads nothing that launch writes: it runs without waiting at all.
-    const bool early = a.early_unstable != nullptr && !a.early_unstable[a.layer * s.H + (blockIdx.x / S) % s.H] &&
-                       (*s.step % a.early_period) != 0;
+    bool early = false;
+    if (a.early_unstable != nullptr) {  // (the head is not due: head_due, spelled out lazily)
+        const int eb = (blockIdx.x / S) / s.H;
+        const int m = s.hold_mode(eb);
+        if (m == FC_HOLD_WAIT) early = true;
+        else if (!a.early_unstable[a.layer * s.H + (blockIdx.x / S) % s.H])
+            early = m == FC_HOLD_RESUME || s.row_step(*s.step, eb) % a.early_period != 0;
+    }
     if (!a.kv_prefetch && !early) griddep_wait();
     char *ring = dsm;
     float *s_q = reinterpret_cast<float *>(dsm + (size_t)NW * NST * Gm::kPageBytes);

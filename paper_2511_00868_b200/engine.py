@@ -30,6 +30,8 @@ import torch
 from .config import HeadId
 from .scoring import layer_scoring_skippable
 from .stability import HeadProfile
+from ._lib import FC_HOLD_NONE as HOLD_NONE, FC_HOLD_RERANK as HOLD_RERANK
+from ._lib import FC_HOLD_RESUME as HOLD_RESUME, FC_HOLD_WAIT as HOLD_WAIT
 from .store import PAGE_SIZE, KVStore
 
 
@@ -53,8 +55,19 @@ class DecodeEngine:
                              sel_cap=topk_pages + self.sel_slack, dtype=dtype, device=self.device)
         self.unstable = profile.mask_tensor(self.device).contiguous()
         self.t = 1                # host mirror of store.step: the upcoming decode step
-        self.selected = False     # initial selection done (first step forces all heads due)
+        self.selected = False     # initial selection done (made at the first step)
         self.seq_host = [0] * batch
+        # per-request decode state (host mirrors of store.row_phase / row_hold):
+        # row b's own step is t_b = t + phase[b] (simulator.py:437-439); rows
+        # admitted together share a phase, rows admitted later rerank on their
+        # own boundary
+        self.phase = [0] * batch
+        self.hold = [0] * batch
+        self._hold_host = torch.zeros(batch, dtype=torch.uint8, pin_memory=True)
+        self._hold_dev_state = [0] * batch  # what the device buffer holds
+        self.decoded_rows: list[int] = []   # rows that emitted a token at the last step
+        self.rerank_rows: list[int] = []    # rows at their rerank boundary at the last step
+        self._initial_rows: set = set()     # admitted rows whose initial selection is due
         self.att_bound = min(pages_cap, topk_pages + self.sel_slack)
         # static step buffers (CUDA-graph inputs/outputs)
         Hq = kv_heads * group
@@ -62,7 +75,7 @@ class DecodeEngine:
         self.k_new = torch.zeros((layers, batch, kv_heads, head_dim), dtype=dtype, device=self.device)
         self.v_new = torch.zeros_like(self.k_new)
         self.out = torch.zeros_like(self.q)
-        self._graphs: dict[tuple, torch.cuda.CUDAGraph] = {}  # (rerank, score_all_heads)
+        self._graphs: dict[tuple, torch.cuda.CUDAGraph] = {}  # (kind, score_all_heads)
         # per-layer hook after the attention launch (e.g. the head-sharded
         # all-gather of outputs, dist.HeadGroup); captured into the step graph
         self.after_layer = after_layer
@@ -132,6 +145,15 @@ class DecodeEngine:
             self.evict_hold_steps = 0  # test hook: keep an eviction pending at least this many steps
             # CTAs of that background copy: the rest of the GPU keeps decoding
             self.offload_ctas = 16
+            # reload pause (simulator.py:321-323,542): a row's
+            # promoted pages are fetched on a side stream after its rerank step;
+            # the row is held (no attention, no advance) until they landed while
+            # the other rows keep decoding.  Off: the fetch runs inside the step.
+            self.reload_pause = False
+            self.fetch_stream = None
+            self._reloads: dict[int, torch.cuda.Event] = {}  # row -> fetch done
+            self._snap_free: list[torch.Tensor] = []
+            self._snap_busy: list[tuple] = []                # (event, copies snapshot)
 
     # -- prefill ----------------------------------------------------------------
 
@@ -169,6 +191,10 @@ class DecodeEngine:
         if self.seq_host[row] >= 0:
             raise ValueError(f"row {row} is busy")
         self.prefill(row, keys, values)
+        # the request's own step counter starts here: its first decode step is
+        # t = 1 (simulator.py:437-439), whatever the engine's global step
+        self.set_row_step(row, 1)
+        self._set_hold(row, HOLD_NONE)
         if self.tiering:
             # post-prefill offload of every full stable-head page, in the
             # background (tiering.py:122-139): decode steps continue meanwhile
@@ -206,6 +232,9 @@ class DecodeEngine:
         if self.tiering and row in self._evict_pending:  # its blocks may still be read by the offload
             torch.cuda.current_stream(self.device).wait_event(self._evict_pending.pop(row)[0])
             self.row_skip[row] = 0
+        if self.tiering and row in self._reloads:  # its blocks may still be written by the fetch
+            torch.cuda.current_stream(self.device).wait_event(self._reloads.pop(row))
+        self._set_hold(row, HOLD_NONE)
         if self.stager is not None:
             self.stager.forget_row(row)
         self.store.free_row(row)
@@ -235,15 +264,141 @@ class DecodeEngine:
         self.store.seq_len[row] = T
         self.seq_host[row] = T
 
-    # -- one decode step -----------------------------------------------------------
+    # -- per-request steps and reload pauses -------------------------------------------
+
+    def row_t(self, row: int, t: int | None = None) -> int:
+        """Row ``row``'s own decode step at global step ``t`` (default: the upcoming one)."""
+        return (self.t if t is None else t) + self.phase[row]
+
+    def set_row_step(self, row: int, t_row: int) -> None:
+        """Make row ``row``'s upcoming decode step ``t_row``: it reranks when its
+        own step is a multiple of R (its rerank phase)."""
+        self.phase[row] = int(t_row) - self.t
+        self.store.row_phase[row] = self.phase[row]
+
+    def _set_hold(self, row: int, mode: int) -> None:
+        self.hold[row] = mode
+
+    def _sync_holds(self) -> None:
+        # the device copy of the hold modes, for the step about to launch (a
+        # small H2D from a ring of pinned buffers, in stream order)
+        if self.hold == self._hold_dev_state:
+            return
+        ring = self.__dict__.setdefault("_hold_ring", [])
+        if len(ring) < 4:
+            buf = (torch.zeros(self.B, dtype=torch.uint8, pin_memory=True), torch.cuda.Event())
+            ring.append(buf)
+        else:
+            buf = ring.pop(0)
+            ring.append(buf)
+            buf[1].synchronize()  # its last copy has been consumed
+        buf[0].copy_(torch.tensor(self.hold, dtype=torch.uint8))
+        self.store.row_hold.copy_(buf[0], non_blocking=True)
+        buf[1].record()
+        self._hold_dev_state = list(self.hold)
+
+    def _active_rows(self):
+        return [b for b in range(self.B) if self.seq_host[b] >= 0]
+
+    def boundary_rows(self, t: int | None = None) -> list:
+        """Rows whose stable heads are due at global step ``t`` (their own step
+        is a multiple of R); at the upcoming step, rows waiting for or resuming
+        after a reload are not (their selection for t_b exists)."""
+        now = t is None or t == self.t
+        t = self.t if t is None else t
+        return [b for b in self._active_rows()
+                if (t + self.phase[b]) % self.R == 0 and not (now and self.hold[b] in (HOLD_WAIT, HOLD_RESUME))]
+
+    def step_kind(self, t: int | None = None) -> str:
+        """'plain' (no row at its boundary), 'rerank' (every decoding row) or
+        'partial' (some rows: requests at different phases)."""
+        now = t is None or t == self.t
+        due = self.boundary_rows(t)
+        if not due:
+            return "plain"
+        rows = [b for b in self._active_rows() if not (now and self.hold[b] == HOLD_WAIT)]
+        return "rerank" if len(due) == len(rows) else "partial"
 
     def is_rerank_step(self, t: int | None = None) -> bool:
-        t = self.t if t is None else t
-        return t % self.R == 0
+        """Some row reranks at global step ``t`` (default: the upcoming one)."""
+        return self.step_kind(t) != "plain"
 
-    def _launch_step(self, rerank: bool, force_due: bool) -> None:
+    def _per_row_needed(self) -> bool:
+        # the kernels read the per-request state only when some active row is
+        # out of phase with the global step or rows can be held
+        return (self.tiering and self.reload_pause) or any(self.phase[b] != 0 for b in self._active_rows())
+
+    def _phases_aligned(self) -> bool:
+        ph = {self.phase[b] % self.R for b in self._active_rows()}
+        return len(ph) <= 1
+
+    def _fetch_mode(self) -> str:
+        """How a two-tier rerank fetches promoted pages: 'async' (side stream,
+        the row held), 'staged' (predicted pages staged ahead, the rest inside
+        the step; rows in phase only) or 'inline' (inside the step)."""
+        if not self.tiering:
+            return "inline"
+        if self.reload_pause:
+            return "async"
+        if self.stager is not None and self._phases_aligned():
+            return "staged"
+        return "inline"
+
+    def _plan_holds(self) -> None:
+        if not (self.tiering and self.reload_pause):
+            for b in range(self.B):
+                self.hold[b] = HOLD_NONE
+            return
+        for b in range(self.B):
+            if self.seq_host[b] < 0:
+                self.hold[b] = HOLD_NONE
+            elif b in self._reloads:
+                if self._reloads[b].query():
+                    del self._reloads[b]
+                    self.hold[b] = HOLD_RESUME
+                else:
+                    self.hold[b] = HOLD_WAIT
+            elif (self.row_t(b) % self.R == 0 and self._stable_layers and not self.eviction_pending(b)):
+                self.hold[b] = HOLD_RERANK
+            else:
+                self.hold[b] = HOLD_NONE
+
+    def _launch_reloads(self) -> None:
+        """After a step graph with reranking rows held: fetch their promoted
+        pages on the fetch stream (from a snapshot of the copy lists, which the
+        next step's recycles overwrite); the rows resume once it finished."""
+        rows = [b for b in range(self.B) if self.hold[b] == HOLD_RERANK]
+        if not rows:
+            return
+        dev = self.device
+        main = torch.cuda.current_stream(dev)
+        if self.fetch_stream is None:
+            self.fetch_stream = torch.cuda.Stream(dev)
+        busy = []
+        for ev, snap in self._snap_busy:
+            (self._snap_free if ev.query() else busy).append(snap)
+        self._snap_busy = busy
+        snap = self._snap_free.pop() if self._snap_free else (torch.empty_like(self.copies),
+                                                              torch.empty_like(self.n_copies))
+        snap[0].copy_(self.copies)
+        snap[1].copy_(self.n_copies)
+        ready = torch.cuda.Event()
+        ready.record(main)
+        with torch.cuda.stream(self.fetch_stream):
+            self.fetch_stream.wait_event(ready)
+            for layer in self._stable_layers:
+                self.tier.reload(layer, snap[0][layer], snap[1][layer:layer + 1])
+            done = torch.cuda.Event()
+            done.record(self.fetch_stream)
+        for b in rows:
+            self._reloads[b] = done
+        self._snap_busy.append((done, snap))
+
+    # -- one decode step -----------------------------------------------------------
+
+    def _launch_step(self, kind: str, force_due: bool, fetch: str = "inline") -> None:
         st = self.store
-        tiered_rerank = self.tiering and rerank and not force_due
+        tiered_rerank = self.tiering and kind != "plain" and not force_due
         use_run = self._use_run()
         use_fused = self.fused_score_attend and st.score_attend_supported(self.B)
 
@@ -251,7 +406,7 @@ class DecodeEngine:
             return tiered_rerank and l in self._stable_layers
 
         def scores(l):
-            return force_due or not self._layer_skippable(l, rerank)
+            return force_due or not self._layer_skippable(l, kind)
 
         if tiered_rerank:  # resident set of stable heads = their current selection
             self.old_sel.copy_(st.sel.transpose(0, 1))
@@ -261,7 +416,7 @@ class DecodeEngine:
         while layer < self.L:
             recycle = recycles(layer)
             scored = scores(layer)
-            if scored and not recycle and self._use_balanced(layer, rerank, force_due):
+            if scored and not recycle and self._use_balanced(layer, kind, force_due):
                 st.score_attend_balanced(layer, self.q[layer], self.unstable, self.R, self.K, self.out[layer],
                                          self.B, extra_tokens=1, kv_prefetch=layer > 0, k_new=self.k_new[layer],
                                          v_new=self.v_new[layer], attend_appended=False)
@@ -271,7 +426,7 @@ class DecodeEngine:
                 continue
             if scored and not recycle and use_fused:
                 # one launch: every head's CTA scores, selects and attends
-                plan = self._mixed_plan(layer) if not (rerank or force_due) else None
+                plan = self._mixed_plan(layer) if kind == "plain" and not force_due else None
                 st.score_attend(layer, self.q[layer], self.unstable, self.R, self.K, self.out[layer], self.B,
                                 force_due=force_due, extra_tokens=1, kv_prefetch=layer > 0,
                                 k_new=self.k_new[layer], v_new=self.v_new[layer], attend_appended=False,
@@ -290,10 +445,11 @@ class DecodeEngine:
                 st.rerank_recycle(layer, self.old_sel[layer], self.n_old[layer], self.unstable, self.R,
                                   self.copies[layer], nc, self.B, old_has_tail=False, extra_tokens=1,
                                   slow_resident=self.tier.slow_resident, row_skip=self.row_skip)
-                if self.stager is not None:
+                if fetch == "staged":
                     self.stager.fetch(layer, self.copies[layer], nc)
-                else:
+                elif fetch == "inline":
                     self.tier.reload(layer, self.copies[layer], nc)
+                # ("async": the rows are held; _launch_reloads fetches after the step)
             if use_run:
                 # persistent attention over the run of layers up to the next one
                 # that needs a selection / table update (or a per-layer hook)
@@ -324,23 +480,29 @@ class DecodeEngine:
             layer += 1
         if tiered_rerank:
             self.fetched_pages.add_(self.n_copies.sum())
-            if self.stager is not None:
+            if fetch == "staged":
                 self.stager.finish_rerank()
-        st.step_advance(self.B)
+        st.step_advance(self.B, self.unstable, self.R)
         if self.recorder is not None:
             self.recorder.capture()
         if self.tiering:  # write-once offload of the page that just filled
             st.offload_filled(self.tier.host, self.unstable, self.tier.slow_resident, self.B)
 
-    def _use_balanced(self, layer: int, rerank: bool, force_due: bool) -> bool:
-        # plain step, some but not all of the layer's heads due
-        if not self.balanced_scoring or rerank or force_due:
+    def _use_balanced(self, layer: int, kind: str, force_due: bool) -> bool:
+        # some but not all of the layer's heads due: a plain step of a layer
+        # with a few unstable heads, or a step where some rows are at their
+        # rerank boundary (requests at different phases)
+        if not self.balanced_scoring or kind == "rerank" or force_due:
             return False
-        n_due = sum(self.profile.is_unstable(HeadId(layer, h)) for h in range(self.H))
+        n_unst = sum(self.profile.is_unstable(HeadId(layer, h)) for h in range(self.H))
+        if kind == "plain" and n_unst == 0:
+            return False
+        if n_unst == self.H:  # every head due at every step: the fused launch
+            return False
         # (only where the fused kernel gives every head one CTA: smaller batches
         # split heads over clusters, and config 4's mixed clusters beat this
         # there: 6.1k vs 5.1k tokens/s)
-        return (0 < n_due < self.H and self.store.score_attend_supported(self.B) == 1
+        return (self.store.score_attend_supported(self.B) == 1
                 and self.store.score_attend_balanced_supported(self.B) > 0)
 
     def _mixed_plan(self, layer: int):
@@ -360,45 +522,72 @@ class DecodeEngine:
             return self.store.run_split(self.B, self.att_bound) >= 2
         return bool(self.run_kernel) and self.store.run_supported(self.B, self.att_bound)
 
-    def _layer_skippable(self, layer: int, rerank: bool) -> bool:
-        # a representative step of the same kind: R (rerank) or 1 (plain, R > 1)
-        t = self.R if rerank else (1 if self.R > 1 else self.R)
+    def _layer_skippable(self, layer: int, kind: str) -> bool:
+        # a representative step of the same kind: R (some row reranks) or 1
+        # (plain, R > 1)
+        t = self.R if kind != "plain" else (1 if self.R > 1 else self.R)
         return layer_scoring_skippable(layer, t, self.profile, self.R)
+
+    def _initial_selection(self) -> None:
+        # every head selects with the first step's query (the selection a
+        # request enters decode with; not a scheduled score evaluation, so the
+        # step's own scoring of its due heads follows as at any step)
+        if self.tiering:  # post-prefill offload of every full stable-head page
+            for b in range(self.B):
+                self.tier.offload_after_prefill(b, self.seq_host[b] // PAGE_SIZE)
+        for layer in range(self.L):
+            self.store.score_select(layer, self.q[layer], self.unstable, self.R, self.K, self.B,
+                                    force_due=True, extra_tokens=1, counted=False)
+        if self.tiering:  # keep only the selection of stable heads in HBM
+            self.store.evict_unselected(self.unstable, self.B)
 
     def step(self, *, use_graph: bool = True) -> torch.Tensor:
         """Run one decode step on the engine's static buffers (q, k_new,
-        v_new -> out).  The first step after prefill makes the initial
-        selection for every head."""
-        rerank = self.is_rerank_step()
+        v_new -> out).  The first step after prefill first makes the initial
+        selection of every head.  Rows at their own rerank boundary rerank;
+        with ``reload_pause`` a two-tier row is held from its rerank until its
+        promoted pages landed (``decoded_rows``: the rows that emitted)."""
         if not self.selected:
-            if self.tiering:  # post-prefill offload of every full stable-head page
-                for b in range(self.B):
-                    self.tier.offload_after_prefill(b, self.seq_host[b] // PAGE_SIZE)
-            self._launch_step(rerank, force_due=True)
-            if self.tiering:  # keep only the selection of stable heads in HBM
-                self.store.evict_unselected(self.unstable, self.B)
+            self._initial_selection()
             self.selected = True
+            use_graph = False  # (eager: sizes the workspaces the graphs capture)
+        if self._initial_rows:
+            self._initial_selections()
+        if self.tiering and self._evict_pending:
+            self._drain_evictions()
+        self.store.per_row = self._per_row_needed()
+        self._plan_holds()
+        self._sync_holds()
+        kind = self.step_kind()
+        fetch = self._fetch_mode()
+        self.rerank_rows = self.boundary_rows()
+        staged = kind != "plain" and fetch == "staged"
+        if staged:
+            self.stager.wait()  # staged promotions have landed
+        if use_graph:
+            key = (kind, self.score_all_heads, fetch, self.store.per_row)
+            g = self._graphs.get(key)
+            if g is None:
+                g = self._capture(kind, fetch)
+            g.replay()
         else:
-            if getattr(self, "_initial_rows", None):
-                self._initial_selections()
-            if self.tiering and self._evict_pending:
-                self._drain_evictions()
-            if rerank and self.tiering and self.stager is not None:
-                self.stager.wait()  # staged promotions have landed
-            if use_graph:
-                g = self._graphs.get((rerank, self.score_all_heads))
-                if g is None:
-                    g = self._capture(rerank)
-                g.replay()
-            else:
-                self._launch_step(rerank, force_due=self.score_all_heads)
-            if rerank and self.tiering and self.stager is not None:
-                self.stager.rerank_launched()
-            if (self.tiering and self.stager is not None and not self.score_all_heads
-                    and any((self.t + ld) % self.R == 0 for ld in self.stager.leads)):
+            self._launch_step(kind, force_due=self.score_all_heads, fetch=fetch)
+        if staged:
+            self.stager.rerank_launched()
+        if fetch == "async" and kind != "plain":
+            self._launch_reloads()
+        if fetch == "staged" and not self.score_all_heads:
+            rows = self._active_rows()
+            t0 = self.row_t(rows[0]) if rows else self.t
+            if any((t0 + ld) % self.R == 0 for ld in self.stager.leads):
                 self.stager.predict(self.q, self.B, self._stable_layers)
+        self.decoded_rows = [b for b in self._active_rows() if self.hold[b] not in (HOLD_WAIT, HOLD_RERANK)]
+        for b in self._active_rows():
+            if self.hold[b] in (HOLD_WAIT, HOLD_RERANK):
+                self.phase[b] -= 1  # (the device did the same in the step advance)
+            else:
+                self.seq_host[b] += 1
         self.t += 1
-        self.seq_host = [s + 1 if s >= 0 else s for s in self.seq_host]
         return self.out
 
     def attach_recorder(self, recorder) -> None:
@@ -408,17 +597,19 @@ class DecodeEngine:
         self.score_all_heads = recorder is not None
         self._graphs.clear()
 
-    def capture_graphs(self) -> None:
-        """Capture both step graphs now (rerank and plain), so no capture or
-        instantiation happens inside a timed region."""
-        for rerank in (False, True):
-            if (rerank, self.score_all_heads) not in self._graphs:
-                self._capture(rerank)
+    def capture_graphs(self, kinds=("plain", "rerank")) -> None:
+        """Capture the step graphs of ``kinds`` now (with the current fetch
+        mode), so no capture or instantiation happens inside a timed region."""
+        fetch = self._fetch_mode()
+        self.store.per_row = self._per_row_needed()
+        for kind in kinds:
+            if (kind, self.score_all_heads, fetch, self.store.per_row) not in self._graphs:
+                self._capture(kind, fetch)
 
-    def _capture(self, rerank: bool) -> torch.cuda.CUDAGraph:
+    def _capture(self, kind: str, fetch: str) -> torch.cuda.CUDAGraph:
         # stream capture records the launches without executing them, so the
         # engine state is untouched; workspaces were sized by the eager first step
-        if not rerank:  # mixed-cluster maps live on the device: build them outside the capture
+        if kind == "plain":  # mixed-cluster maps live on the device: build them outside the capture
             for layer in range(self.L):
                 self._mixed_plan(layer)
         torch.cuda.synchronize(self.device)
@@ -427,10 +618,10 @@ class DecodeEngine:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(s):
             with torch.cuda.graph(g, stream=s):
-                self._launch_step(rerank, force_due=self.score_all_heads)
+                self._launch_step(kind, force_due=self.score_all_heads, fetch=fetch)
         torch.cuda.current_stream(self.device).wait_stream(s)
         torch.cuda.synchronize(self.device)
-        self._graphs[(rerank, self.score_all_heads)] = g
+        self._graphs[(kind, self.score_all_heads, fetch, self.store.per_row)] = g
         return g
 
     def launches_per_step(self, t: int) -> int:
@@ -439,23 +630,25 @@ class DecodeEngine:
         attention launch (append fused) — one fused launch for both, or one
         persistent launch per run of layers, when those are enabled — plus
         the step advance (and the tier copies in two-tier mode)."""
-        rerank = self.is_rerank_step(t)
+        kind = self.step_kind(t)
+        rerank = kind != "plain"
         st = self.store
         use_run = self._use_run()
         use_fused = self.fused_score_attend and st.score_attend_supported(self.B)
+        fetch = self._fetch_mode()
 
         def recycles(l):
             return self.tiering and rerank and l in self._stable_layers
 
         def scores(l):
-            return self.score_all_heads or not self._layer_skippable(l, rerank)
+            return self.score_all_heads or not self._layer_skippable(l, kind)
 
         n, layer = 1, 0  # the step advance
         while layer < self.L:
             if recycles(layer):
-                n += 2  # recycle + fetch
+                n += 2  # recycle + fetch (on the fetch stream with reload pauses)
             if scores(layer) and not recycles(layer) and (
-                    use_fused or (not self.score_all_heads and self._use_balanced(layer, rerank, False))):
+                    use_fused or (not self.score_all_heads and self._use_balanced(layer, kind, False))):
                 n += 1
                 layer += 1
                 continue
@@ -468,7 +661,7 @@ class DecodeEngine:
             layer = end
         if self.tiering:
             n += 1  # offload of the page that just filled
-            if rerank and self.stager is not None:
+            if rerank and fetch == "staged":
                 n += 1  # staging map clear
         return n
 

@@ -18,11 +18,15 @@ leave the row alone until then — and reranks fetch promoted pages (staged
 ahead, tiering.ReloadStager).  With an all-resident engine the
 commit is the request's whole KV (simulator.py:257-258).
 
-Differences from the simulator, by construction:
-* the rerank schedule is the engine's global step counter (every row reranks
-  at t % R == 0), not a per-request t;
-* no reload pauses: promoted pages are fetched inside the rerank step.
-Prompts and decode inputs are synthetic (the reference has no model either).
+Each request steps on its own t (simulator.py:437-439): it enters decode at
+t = 1 whatever the engine's step, so requests admitted at different times
+rerank on different steps (the engine's 'partial' step graphs score only the
+rows at their boundary).  With a two-tier engine the reload pause of
+simulator.py:321-323,542 is real: a row's promoted pages are fetched on a
+side stream after its rerank step and the row is held (emits nothing) until
+they landed, while the other rows keep decoding (``reload_pause``; the
+metrics report the held fraction of row-steps).  Prompts and
+decode inputs are synthetic (the reference has no model either).
 """
 
 from __future__ import annotations
@@ -67,6 +71,8 @@ class ServingMetrics:
     decode_steps: int = 0
     reload_bytes: int = 0
     promoted_fraction: float = 0.0
+    pause_steps: int = 0          # row-steps held for a reload (Metrics.pause_steps)
+    pause_fraction: float = 0.0   # pause_steps / row-steps of active requests
 
     def to_text(self) -> str:
         return "".join(f"{f.name} = {getattr(self, f.name)}\n" for f in fields(self))
@@ -98,8 +104,10 @@ class ServingLoop:
     """
 
     def __init__(self, engine, requests, make_prompt, feed, *, fast_capacity_blocks: int | None = None,
-                 timer=None):
+                 timer=None, reload_pause: bool = True):
         self.eng = engine
+        if getattr(engine, "tiering", False) and hasattr(engine, "reload_pause"):
+            engine.reload_pause = reload_pause
         self.timer = timer if timer is not None else self._time  # timer(fn) -> seconds
         self.pending = sorted(requests, key=lambda r: (r.arrival_s, r.id))
         self.make_prompt = make_prompt
@@ -113,6 +121,7 @@ class ServingLoop:
         self.m = ServingMetrics(n_requests=len(requests))
         self._ttft, self._tpot = [], []
         self._rerank_slots = 0
+        self._row_steps = 0
         self._captured = False
 
     def _commit_blocks(self, req: Request) -> int:
@@ -174,7 +183,7 @@ class ServingLoop:
                 if not self._captured and hasattr(eng, "capture_graphs"):
                     # one-time setup outside the clock (as bench.py captures
                     # before its timed region): the step graphs
-                    eng.capture_graphs()
+                    eng.capture_graphs(("plain", "rerank", "partial"))
                     self._captured = True
                 active[row] = _Active(req, row, commit=need)
                 self._ttft.append(self.now - req.arrival_s)  # prefill emits the first token
@@ -189,19 +198,29 @@ class ServingLoop:
                     self.now = max(self.now, self.pending[0].arrival_s)
                 continue
             self.feed(eng)
-            if eng.tiering and eng.is_rerank_step():
-                # rerank slots of rows that recycle (simulator.py:532): stable
-                # heads x their target, rows past their post-prefill offload
-                n_stable = self.LH - int(eng.unstable.sum().item())
-                for row, a in active.items():
-                    if not eng.eviction_pending(row):
-                        pages = (eng.seq_host[row] + 1 + PAGE_SIZE - 1) // PAGE_SIZE
-                        self._rerank_slots += n_stable * min(eng.K, pages)
+            pre_seq = list(getattr(eng, "seq_host", ()))
             dt = self.timer(eng.step)
             eng.store.check_errors()
             self.now += dt
             steps += 1
+            if eng.tiering:
+                # rerank slots of rows that recycled (simulator.py:532): stable
+                # heads x their target, rows past their post-prefill offload
+                n_stable = self.LH - int(eng.unstable.sum().item())
+                reranked = getattr(eng, "rerank_rows", None)
+                if reranked is None:
+                    reranked = list(active) if eng.is_rerank_step() else []
+                for row in reranked:
+                    if row in active and not eng.eviction_pending(row):
+                        pages = (pre_seq[row] + 1 + PAGE_SIZE - 1) // PAGE_SIZE
+                        self._rerank_slots += n_stable * min(eng.K, pages)
+            decoded = getattr(eng, "decoded_rows", None)
+            decoded = set(active) if decoded is None else set(decoded)
+            self._row_steps += len(active)
+            self.m.pause_steps += len(set(active) - decoded)
             for row in list(active):
+                if row not in decoded:  # held for its reload: no token this step
+                    continue
                 a = active[row]
                 a.emitted += 1
                 a.last_token_s = self.now
@@ -226,6 +245,7 @@ class ServingLoop:
         m = self.m
         m.queued_at_end = len(self.pending) + len(ready)
         m.decode_steps = steps
+        m.pause_fraction = m.pause_steps / self._row_steps if self._row_steps else 0.0
         m.sim_time_s = self.now
         m.throughput_tokens_per_s = m.output_tokens / self.now if self.now > 0 else 0.0
         if eng.tiering:  # promoted pages fetched over the host link (simulator.py:535-541, :600)

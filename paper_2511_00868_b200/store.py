@@ -69,14 +69,34 @@ class KVStore:
         self.free_top = torch.tensor([n_blocks - 1], dtype=torch.int32, device=dev)
         self.step = torch.ones(1, dtype=torch.int32, device=dev)
         self.error_word = torch.zeros(1, dtype=torch.int32, device=dev)
+        # per-request decode state: row b's own step t_b = step + row_phase[b]
+        # (simulator.py:437-439) and its reload-pause mode (FC_HOLD_*)
+        self.row_phase = torch.zeros(batch_cap, dtype=torch.int32, device=dev)
+        self.row_hold = torch.zeros(batch_cap, dtype=torch.uint8, device=dev)
+        # device scoring counters (FC_STAT_*: Metrics, simulator.py:87-131)
+        self.stats = torch.zeros(_lib.FC_STATS_N, dtype=torch.int64, device=dev)
         self._c = _lib.FcStore(
             batch_cap, layers, kv_heads, group, head_dim, PAGE_SIZE, pages_cap, sel_cap,
             _DTYPES[dtype], n_blocks,
             self.kv_pool.data_ptr(), self.summaries.data_ptr(), self.table.data_ptr(),
             self.seq_len.data_ptr(), self.sel.data_ptr(), self.n_sel.data_ptr(),
             self.free_stack.data_ptr(), self.free_top.data_ptr(), self.step.data_ptr(),
-            self.error_word.data_ptr())
-        self.cptr = ctypes.addressof(self._c)
+            self.error_word.data_ptr(), self.row_phase.data_ptr(), self.row_hold.data_ptr(),
+            self.stats.data_ptr())
+        # the descriptor kernels see: with the per-request state only while some
+        # row is out of phase or held (``per_row``); in phase, every kernel
+        # skips those loads (they sat on the attention prologue's dependent
+        # chain: +0.7 us per launch at config 2)
+        self._c_phase = self._c
+        self._c_flat = _lib.FcStore.from_buffer_copy(self._c)
+        self._c_flat.row_phase = None
+        self._c_flat.row_hold = None
+        self.per_row = False
+        # the same store without the counters: selections that are not
+        # scheduled score evaluations (initial selection, reload prediction)
+        self._c_quiet = _lib.FcStore.from_buffer_copy(self._c)
+        self._c_quiet.stats = None
+        self.cptr_quiet = ctypes.addressof(self._c_quiet)
         # scoring workspace: scores [B*H, N_cap] fp32 + per-head counters
         self.scores = torch.full((batch_cap * kv_heads, pages_cap), float("-inf"),
                                  dtype=torch.float32, device=dev)
@@ -86,6 +106,10 @@ class KVStore:
         self._run_ws = torch.zeros(0, dtype=torch.uint8, device=dev)
 
     # -- misc ------------------------------------------------------------------
+
+    @property
+    def cptr(self) -> int:
+        return ctypes.addressof(self._c_phase if self.per_row else self._c_flat)
 
     @property
     def page_bytes(self) -> int:
@@ -145,6 +169,9 @@ class KVStore:
             c.seq_len = self.seq_len[row:row + 1].data_ptr()
             c.sel = self.sel[row].data_ptr()
             c.n_sel = self.n_sel[row].data_ptr()
+            c.row_phase = self.row_phase[row:row + 1].data_ptr()
+            c.row_hold = self.row_hold[row:row + 1].data_ptr()
+            c.stats = None  # (initial selections: not scheduled evaluations)
             views[row] = c
         return ctypes.addressof(views[row])
 
@@ -156,8 +183,24 @@ class KVStore:
             extra_tokens, 0, self.scores.data_ptr(), self.score_counters.data_ptr(), 1, self.stream()),
             "fc_score_select")
 
-    def step_advance(self, batch: int) -> None:
-        _lib.check(self.lib.fc_step_advance(self.cptr, batch, self.stream()), "fc_step_advance")
+    def step_advance(self, batch: int, unstable: torch.Tensor | None = None, period: int = 1) -> None:
+        """fc_step_advance; with ``unstable`` / ``period`` also count the
+        step's skipped layers into ``stats`` (fc_step_advance_counted)."""
+        if unstable is None:
+            _lib.check(self.lib.fc_step_advance(self.cptr, batch, self.stream()), "fc_step_advance")
+        else:
+            _lib.check(self.lib.fc_step_advance_counted(self.cptr, batch, unstable.data_ptr(), period,
+                                                        self.stream()), "fc_step_advance_counted")
+
+    def scoring_stats(self) -> dict:
+        """The device counters (synchronising read): heads scored, the naive
+        count (every head of every decoding row every step), (row, layer)
+        pairs with no due head, row-steps held for a reload."""
+        v = self.stats.tolist()
+        return {"score_evals": v[_lib.FC_STAT_SCORE_EVALS],
+                "score_evals_naive": v[_lib.FC_STAT_SCORE_EVALS_NAIVE],
+                "layer_scoring_skips": v[_lib.FC_STAT_LAYER_SKIPS],
+                "held_row_steps": v[_lib.FC_STAT_HELD_ROW_STEPS]}
 
     def evict_pages(self, pages: torch.Tensor) -> None:
         """pages: int32 [n, 4] (row, layer, head, logical) on the device."""
@@ -193,9 +236,9 @@ class KVStore:
 
     def score_select(self, layer: int, q: torch.Tensor, unstable: torch.Tensor, period: int,
                      topk: int, batch: int, *, force_due: bool = False, extra_tokens: int = 1,
-                     kv_prefetch: bool = False) -> None:
+                     kv_prefetch: bool = False, counted: bool = True) -> None:
         _lib.check(self.lib.fc_score_select(
-            self.cptr, layer, q.data_ptr(), unstable.data_ptr(), period, int(force_due), topk,
+            self.cptr if counted else self.cptr_quiet, layer, q.data_ptr(), unstable.data_ptr(), period, int(force_due), topk,
             extra_tokens, int(kv_prefetch), self.scores.data_ptr(), self.score_counters.data_ptr(),
             batch, self.stream()), "fc_score_select")
 
@@ -404,7 +447,7 @@ class KVStore:
         if key not in views:
             if sel.shape != self.sel.shape or n_sel.shape != self.n_sel.shape:
                 raise ValueError("selection buffers must match the store's sel / n_sel shapes")
-            c = _lib.FcStore.from_buffer_copy(self._c)
+            c = _lib.FcStore.from_buffer_copy(self._c_quiet)
             c.sel, c.n_sel = sel.data_ptr(), n_sel.data_ptr()
             views[key] = (c, (sel, n_sel))
         return ctypes.addressof(views[key][0])
@@ -419,7 +462,7 @@ class KVStore:
         if key not in views:
             if sel.shape != self.sel.shape or n_sel.shape != self.n_sel.shape:
                 raise ValueError("selection buffers must match the store's sel / n_sel shapes")
-            c = _lib.FcStore.from_buffer_copy(self._c)
+            c = _lib.FcStore.from_buffer_copy(self._c_quiet)
             c.layers, c.kv_heads = 1, self.L * self.H
             c.sel, c.n_sel = sel.data_ptr(), n_sel.data_ptr()
             views[key] = (c, (sel, n_sel))

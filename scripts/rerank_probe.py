@@ -63,7 +63,7 @@ feed()
 eng.stager.wait()
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 a.record()
-eng._launch_step(True, force_due=False)
+eng._launch_step("rerank", force_due=False, fetch=eng._fetch_mode())
 b.record()
 torch.cuda.synchronize()
 for name, e0, e1 in pending:

@@ -32,9 +32,12 @@ def test_every_header_symbol_is_exported():
 
 
 def test_struct_layout_matches_header():
-    # 10 int32 geometry fields then 10 pointers
-    assert ctypes.sizeof(_lib.FcStore) == 10 * 4 + 10 * 8
+    # 10 int32 geometry fields then 10 buffer pointers, then the optional
+    # per-request state (row_phase, row_hold, stats)
+    assert ctypes.sizeof(_lib.FcStore) == 10 * 4 + 13 * 8
     assert _lib.FcStore.kv_pool.offset == 40
+    assert _lib.FcStore.row_phase.offset == 40 + 10 * 8
+    assert _lib.FcStore.stats.offset == 40 + 12 * 8
 
 
 def test_argument_errors_map_to_valueerror_without_gpu():

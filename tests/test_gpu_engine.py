@@ -204,7 +204,7 @@ def test_engine_balanced_scoring_matches_oracle(head_aligned_scoring, D, G, spre
     worst, ties, eng = run_engine_vs_oracle(B=3, L=2, H=4, G=G, D=D, T0=1500, steps=10, K=8,
                                             R=4, frac=0.5, dtype=torch.bfloat16, seed=23, use_graph=True,
                                             ragged=True, fused=True, spread=spread)
-    assert eng._use_balanced(0, False, False) and not eng._use_balanced(0, True, False)
+    assert eng._use_balanced(0, "plain", False) and not eng._use_balanced(0, "rerank", False)
     assert ties <= 2
 
 

@@ -93,8 +93,9 @@ def _run_fullsize(B, T):
                     if due:
                         extra = 1 if n_alloc > n_pages else 0
                         assert len(s) == K + extra
-        # selection == select_topk over the GPU scores (layer 1 was scored last on rerank steps)
-        if t % R == 0 or step == 0:
+        # selection == select_topk over the GPU scores (layer 1 was scored last
+        # on rerank steps; the first step's initial selection scored it last)
+        if t % R == 0:
             scores = st.scores.cpu().numpy()
             for bh in [x for x in (0, 5, 9, 15) if x < B * H]:
                 b, h = divmod(bh, H)

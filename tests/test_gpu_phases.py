@@ -1,0 +1,228 @@
+"""Per-request decode steps on the GPU: every row reranks at its OWN step
+t_b % R == 0 (simulator.py:437-439, the per-request ``r.t``), and with a
+two-tier engine and ``reload_pause`` a row's promoted pages are fetched on a
+side stream after its rerank while the row is held — it emits nothing until
+they landed, the other rows keep decoding (simulator.py:321-323,542 ``reload_until``;
+PAPER.md:221-230).  Checked step by step against the float64 oracle:
+
+* summaries bit-exact for every row that decoded;
+* selections: a head is re-selected exactly when the reference would (its
+  row's boundary, or every step when unstable; nothing while the row waits
+  for its reload) and equals ``select_topk`` on the oracle's float64 group
+  scores outside the fp32 tie band; otherwise it is the previous selection
+  plus the pages appended since;
+* attention of every row that decoded over its selection (bf16 2e-2);
+* two-tier: stable heads keep exactly their selection in HBM, and a held row
+  resumes with the same outputs as if the fetch had been inside the step.
+
+Also criterion 11c of the reference (test_acceptance.py:444-461) on the
+device counters: with 16 heads, u = 0.25, R = 16 and 160 decode steps the
+ratio of scored heads to the naive count is exactly 0.296875.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import flexicache_oracle as O  # noqa: E402
+
+PS = 16
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def _band(qs, mins, maxs):
+    D, G = mins.shape[1], qs.shape[0]
+    mag = np.abs(qs).sum(axis=0) @ np.maximum(np.abs(mins), np.abs(maxs)).T
+    return 2.0 * (2 * D + G + 2) * 2.0 ** -24 * float(mag.max())
+
+
+def run_phases(*, B, L, H, G, D, T0, K, R, steps, row_steps, tiering=False, pause=False, seed=0,
+               frac=0.5, batch_fill=False):
+    from paper_2511_00868_b200.engine import HOLD_RERANK, HOLD_RESUME, HOLD_WAIT, DecodeEngine
+    from paper_2511_00868_b200.stability import HeadProfile
+    rng = np.random.default_rng(seed)
+    prof = HeadProfile.first_n(L, H, frac)
+    unstable = prof.mask()
+    eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=T0 + 17 * B + steps + 64,
+                       topk_pages=K, rerank_period=R, profile=prof, tiering=tiering)
+    if tiering:
+        eng.reload_pause = pause
+    dev = eng.device
+    keys, vals = {}, {}
+    for b in range(B):
+        T = T0 + 17 * b
+        k = O.bf16_round(rng.standard_normal((L, H, T, D)))
+        v = O.bf16_round(rng.standard_normal((L, H, T, D)))
+        for l in range(L):
+            for h in range(H):
+                keys[b, l, h], vals[b, l, h] = k[l, h], v[l, h]
+        eng.prefill(b, torch.as_tensor(k).to(dev).bfloat16(), torch.as_tensor(v).to(dev).bfloat16())
+        eng.set_row_step(b, row_steps[b])
+    exp = {}
+    pend = [None] * B         # the inputs of each row's next token (re-fed while it is held)
+    stats = {"heads": 0, "band": 0, "held": 0, "boundaries": 0, "reselected": 0, "scored": 0}
+    emitted = [0] * B
+    for step in range(steps):
+        for b in range(B):
+            if pend[b] is None:
+                pend[b] = tuple(O.bf16_round(rng.standard_normal(s)) for s in ((L, H * G, D), (L, H, D), (L, H, D)))
+            eng.q[:, b].copy_(torch.as_tensor(pend[b][0]))
+            eng.k_new[:, b].copy_(torch.as_tensor(pend[b][1]))
+            eng.v_new[:, b].copy_(torch.as_tensor(pend[b][2]))
+        first = not eng.selected
+        t_row = [eng.row_t(b) for b in range(B)]
+        eng.step(use_graph=step > 0)
+        torch.cuda.synchronize()
+        eng.store.check_errors()
+        st = eng.store
+        sel, n_sel = st.sel.cpu().numpy(), st.n_sel.cpu().numpy()
+        out = eng.out.double().cpu().numpy()
+        summ = st.summaries.double().cpu().numpy()
+        table = st.table.cpu().numpy()
+        seq = st.seq_len.cpu().numpy()
+        decoded = set(eng.decoded_rows)
+        for b in range(B):
+            hold = eng.hold[b]
+            q, kn, vn = pend[b]
+            if b in decoded:
+                assert hold not in (HOLD_WAIT, HOLD_RERANK)
+            else:
+                assert pause and hold in (HOLD_WAIT, HOLD_RERANK), (step, b, hold)
+                stats["held"] += 1
+            stats["boundaries"] += int(t_row[b] % R == 0 and hold != HOLD_WAIT and hold != HOLD_RESUME)
+            n_tok_next = keys[b, 0, 0].shape[0] + 1     # with the token of this step
+            n_pages = O.pages_for_tokens(n_tok_next, PS)
+            assert int(seq[b]) == n_tok_next - (0 if b in decoded else 1), (step, b)
+            for l in range(L):
+                for h in range(H):
+                    kk = np.vstack([keys[b, l, h], kn[l, h][None]])
+                    vv = np.vstack([vals[b, l, h], vn[l, h][None]])
+                    mins, maxs, _ = O.minmax_build(kk, PS)
+                    gsel = tuple(p for p in sel[b, l, h, :n_sel[b, l, h]].tolist() if p < n_pages)
+                    qs = q[l, h * G:(h + 1) * G]
+                    if hold == HOLD_WAIT:
+                        counted = False
+                    elif hold == HOLD_RESUME:
+                        counted = bool(unstable[l, h])
+                    else:
+                        counted = bool(unstable[l, h]) or t_row[b] % R == 0
+                    stats["scored"] += int(counted)  # (the initial selection is not counted)
+                    due = first or counted
+                    if due:
+                        osc = O.group_scores(qs, mins, maxs)
+                        osel = O.select_topk_fast(osc, K, (n_pages - 1,))
+                        stats["heads"] += 1
+                        if gsel != osel:
+                            assert len(gsel) == len(osel), (step, b, l, h)
+                            band = _band(qs, mins, maxs)
+                            kth = np.sort(osc[:-1])[::-1][min(K, n_pages) - 2]
+                            for p in set(gsel) ^ set(osel):
+                                assert abs(osc[p] - kth) <= band, (step, b, l, h, p)
+                            stats["band"] += 1
+                        if (b, l, h) in exp and not unstable[l, h] and gsel != exp[b, l, h]:
+                            stats["reselected"] += 1
+                    else:
+                        # the previous selection plus the pages opened since
+                        prev = exp[b, l, h]
+                        want = tuple(sorted(set(prev) | set(range(prev[-1] + 1, n_pages))))
+                        assert gsel == want, (step, b, l, h, hold)
+                    exp[b, l, h] = gsel
+                    if tiering and not unstable[l, h]:
+                        n_alloc = O.pages_for_tokens(int(seq[b]) + 1, PS)
+                        resident = tuple(np.flatnonzero(table[b, l, h, :n_alloc]).tolist())
+                        assert resident == tuple(sel[b, l, h, :n_sel[b, l, h]].tolist()), (step, b, l, h)
+                    if b in decoded:
+                        assert np.array_equal(summ[b, l, h, :n_pages, 0], mins), (step, b, l, h)
+                        assert np.array_equal(summ[b, l, h, :n_pages, 1], maxs), (step, b, l, h)
+                        want = O.gqa_sparse_decode(qs, kk, vv, PS, O.attended_pages(gsel, n_pages))
+                        got = out[l, b, h * G:(h + 1) * G]
+                        err = np.linalg.norm(got - want) / np.linalg.norm(want)
+                        assert err <= 2e-2, (step, b, l, h, err)
+                        keys[b, l, h], vals[b, l, h] = kk, vv
+            if b in decoded:
+                pend[b] = None
+                emitted[b] += 1
+    return eng, stats, emitted
+
+
+@pytest.mark.parametrize("tiering", [False, True])
+def test_rows_rerank_at_their_own_step(tiering):
+    """Three requests at different phases (their own t = 1, 2, 3 at the first
+    step): each reranks on its own boundary; the steps in between are
+    'partial' steps where only that row's stable heads are scored."""
+    R = 4
+    eng, stats, emitted = run_phases(B=3, L=2, H=4, G=4, D=128, T0=700, K=8, R=R, steps=14,
+                                     row_steps=[1, 2, 3], tiering=tiering, seed=11)
+    assert emitted == [14, 14, 14] and stats["held"] == 0
+    assert stats["reselected"] > 0
+    kinds = {eng.step_kind(t) for t in range(eng.t, eng.t + R)}
+    assert kinds == {"partial", "plain"}  # one row at a time reaches its boundary
+    assert any(k[0] == "partial" for k in eng._graphs)
+
+
+def test_reload_pause_holds_only_the_reranking_row():
+    """Two-tier with reload pauses: a row at its boundary scores, selects and
+    recycles, then is held (no attention, no advance, its own t unchanged)
+    until its promoted pages have landed; the other rows decode meanwhile.
+    After it resumes its outputs match the oracle on the selection made with
+    its rerank-step query."""
+    R = 4
+    eng, stats, emitted = run_phases(B=3, L=2, H=4, G=4, D=128, T0=700, K=8, R=R, steps=20,
+                                     row_steps=[1, 2, 3], tiering=True, pause=True, seed=12)
+    assert stats["boundaries"] >= 3 and stats["held"] >= stats["boundaries"]
+    assert min(emitted) > 0 and sum(emitted) + stats["held"] == 3 * 20
+    assert int(eng.fetched_pages.item()) > 0
+    # retiring a held row waits for its fetch before the blocks return
+    for b in range(3):
+        eng.retire(b)
+    torch.cuda.synchronize()
+    eng.store.check_errors()
+    assert eng.store.free_count() == eng.store.n_blocks - 1
+
+
+def test_reload_pause_device_counts_held_rows():
+    R = 4
+    eng, stats, emitted = run_phases(B=2, L=2, H=2, G=2, D=64, T0=400, K=6, R=R, steps=12,
+                                     row_steps=[1, 3], tiering=True, pause=True, seed=13)
+    c = eng.store.scoring_stats()
+    assert c["held_row_steps"] == stats["held"] > 0
+    assert c["score_evals_naive"] == sum(emitted) * eng.L * eng.H
+    assert c["score_evals"] == stats["scored"]
+
+
+def test_criterion_11c_score_evaluation_ratio_on_device():
+    """test_acceptance.py:444-461 with the scoring done by the kernels and
+    counted on the device: Config(num_layers=4, kv_heads_per_layer=4,
+    unstable_fraction=0.25, rerank_period=16), 3 requests of 2048 prompt
+    tokens, 160 decode steps -> score_evals / score_evals_naive ==
+    0.25 + 0.75/16 == 0.296875 exactly; the 3 all-stable layers are skipped
+    on the 150 plain steps of each request (Metrics.layer_scoring_skips)."""
+    from paper_2511_00868_b200.engine import DecodeEngine
+    from paper_2511_00868_b200.stability import HeadProfile
+    B, L, H, G, D, T, R = 3, 4, 4, 1, 128, 2048, 16
+    eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=T + 200,
+                       topk_pages=32, rerank_period=R, profile=HeadProfile.first_n(L, H, 0.25))
+    g = torch.Generator(device="cuda")
+    g.manual_seed(4)
+    for b in range(B):
+        k = torch.randn((L, H, T, D), generator=g, device="cuda").bfloat16()
+        eng.prefill(b, k, torch.randn_like(k))
+    for _ in range(160):
+        eng.q.normal_(generator=g)
+        eng.k_new.normal_(generator=g)
+        eng.v_new.normal_(generator=g)
+        eng.step()
+    c = eng.store.scoring_stats()
+    eng.store.check_errors()
+    assert c["score_evals"] < c["score_evals_naive"]
+    assert c["score_evals_naive"] == B * 160 * L * H
+    assert c["score_evals"] / c["score_evals_naive"] == 0.296875 == 0.25 + (1 - 0.25) / 16
+    assert c["layer_scoring_skips"] == B * 150 * 3
+    assert c["held_row_steps"] == 0
