@@ -769,8 +769,8 @@ __device__ int score_head_stream(const StoreView &s, int layer, const T *__restr
             bulk_g2s(ring + (size_t)c * HG::kChunkBytes, base + (int64_t)c * HG::kChunkBytes, bytes, &full[c]);
         }
     }
-    if (trace && tid == 0) trace[blockIdx.x * 4 + 1] = gtimer_s();
     if (kv_prefetch) griddep_wait();  // q comes from the previous launch
+    if (trace && tid == 0) trace[blockIdx.x * 4 + 1] = gtimer_s();  // (released)
     load_group_coeffs<T>(s, q, b, h, w);
     __syncthreads();
     const int sub = lane / LPP, cl = lane % LPP;
@@ -935,29 +935,48 @@ score_head_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t
 // last page is pinned), so the warm-up reads final data.  The next layer of
 // layer L-1 is layer 0 of the next step (step + 1).  `ord` / `n_pf` = this
 // CTA's ordinal among the launch's prefetching CTAs / their number; every
-// prefetching CTA takes an equal share of the due pages.  Thread 0 only.
+// prefetching CTA takes an equal share of the due pages.  Called by one warp
+// (all lanes): lanes cover rows, so the per-row state (each row's own step,
+// its reload hold) is read once per row and in parallel.
 static constexpr int64_t kSummaryPrefetchCap = 48ll << 20;  // L2 = 126 MB: leave room for the pages streaming by
 static int64_t g_summary_prefetch_cap = kSummaryPrefetchCap;
+
+// heads of row b due in layer l at global step step0 (bit h), for rows held
+// waiting for a reload none; unstable heads every step, all at the boundary
+FC_DEVINL uint32_t row_due_mask(const StoreView &s, int step0, int b, int l, const uint8_t *__restrict__ unstable,
+                               int period, int force_due) {
+    const uint32_t all = s.H >= 32 ? 0xffffffffu : (1u << s.H) - 1;
+    if (force_due) return all;
+    if (s.hold_mode(b) == FC_HOLD_WAIT) return 0;
+    if (s.boundary(step0, b, period)) return all;
+    uint32_t m = 0;
+    for (int h = 0; h < s.H && h < 32; ++h) m |= unstable[l * s.H + h] ? (1u << h) : 0u;
+    return m;
+}
+
 template <typename T, int D>
 __device__ void prefetch_next_summaries(const StoreView &s, int layer, const uint8_t *__restrict__ unstable,
                                         int period, int topk, int extra_tokens, int batch, int ord, int n_pf,
                                         int64_t cap) {
     using Gm = ScoreGeom<T, D>;
+    const int lane = threadIdx.x & 31;
     int nl = layer + 1, step = *s.step;
     if (nl == s.L) { nl = 0; ++step; }
-    // (each row's own boundary: rows rerank at their own t_b)
-    auto due = [&](int b, int h) { return s.head_due(step, b, unstable[nl * s.H + h], period, false); };
-    // candidate pages of the due heads
+    // candidate pages of the due heads, per row (lanes), then over rows
     int64_t total = 0;
-    for (int b = 0; b < batch; ++b) {
-        const int n_tok = s.seq_len[b] + extra_tokens;
-        const int np = n_tok > 0 ? (n_tok + s.PS - 1) / s.PS : 0;
-        if (np <= topk) continue;
-        int n_due = 0;
-        for (int h = 0; h < s.H; ++h) n_due += due(b, h) ? 1 : 0;
-        total += (int64_t)(np - 1) * n_due;
+    for (int b0 = 0; b0 < batch; b0 += 32) {
+        const int b = b0 + lane;
+        int64_t mine = 0;
+        if (b < batch) {
+            const int n_tok = s.seq_len[b] + extra_tokens;
+            const int np = n_tok > 0 ? (n_tok + s.PS - 1) / s.PS : 0;
+            if (np > topk) mine = (int64_t)(np - 1) * __popc(row_due_mask(s, step, b, nl, unstable, period, 0));
+        }
+        for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+        total += mine;
     }
     if (total == 0 || total * Gm::kRecBytes > cap) return;
+    if (lane != 0) return;
     int64_t lo = total * ord / n_pf;
     const int64_t hi = total * (ord + 1) / n_pf;
     int64_t base = 0;
@@ -966,8 +985,13 @@ __device__ void prefetch_next_summaries(const StoreView &s, int layer, const uin
         const int np = n_tok > 0 ? (n_tok + s.PS - 1) / s.PS : 0;
         if (np <= topk) continue;
         const int cand = np - 1;
+        const uint32_t due = row_due_mask(s, step, b, nl, unstable, period, 0);
+        if (base + (int64_t)cand * __popc(due) <= lo) {  // the whole row is before this share
+            base += (int64_t)cand * __popc(due);
+            continue;
+        }
         for (int h = 0; h < s.H && lo < hi; ++h) {
-            if (!due(b, h)) continue;
+            if (!((due >> h) & 1u)) continue;
             if (lo < base + cand) {
                 const int p0 = (int)(lo - base);
                 const int p1 = (int)(hi - base < cand ? hi - base : cand);
@@ -1070,18 +1094,28 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
         if (satr && threadIdx.x == 0) satr[blockIdx.x * 4 + 1] = gtimer_s();
         attend_head_cta<T, D, NST, NWA>(s, a, bh, dsm, abars, s_wm, s_wl, s_q, 1);
         if (satr && threadIdx.x == 0) satr[blockIdx.x * 4 + 2] = gtimer_s();
-        if (a.pf_cap > 0 && threadIdx.x == 0) {
-            const int step = *s.step;
-            auto due = [&](int bb, int hh) {
-                return s.head_due(step, bb, unstable[layer * s.H + hh], period, force_due);
-            };
-            if (!due(b, h)) {  // the heads not due share the prefetch: this one's ordinal among them
-                const int batch = gridDim.x / s.H;
+        if (a.pf_cap > 0 && threadIdx.x < 32) {
+            // the heads not due share the prefetch: this one's ordinal among
+            // them (lanes over rows: each row's due mask read once)
+            const int step = *s.step, lane = threadIdx.x;
+            const int batch = gridDim.x / s.H;
+            const uint32_t all = s.H >= 32 ? 0xffffffffu : (1u << s.H) - 1;
+            if (!((row_due_mask(s, step, b, layer, unstable, period, force_due) >> h) & 1u)) {
                 int nnd = 0, before = 0;
-                for (int x = 0; x < batch * s.H; ++x) {
-                    const bool nd = !due(x / s.H, x % s.H);
+                for (int b0 = 0; b0 < batch; b0 += 32) {
+                    const int bb = b0 + lane;
+                    int nd = 0, bef = 0;
+                    if (bb < batch) {
+                        const uint32_t notdue = ~row_due_mask(s, step, bb, layer, unstable, period, force_due) & all;
+                        nd = __popc(notdue);
+                        bef = bb < b ? nd : (bb == b ? __popc(notdue & ((1u << h) - 1)) : 0);
+                    }
+                    for (int o = 16; o > 0; o >>= 1) {
+                        nd += __shfl_xor_sync(0xffffffffu, nd, o);
+                        bef += __shfl_xor_sync(0xffffffffu, bef, o);
+                    }
                     nnd += nd;
-                    before += nd && x < bh;
+                    before += bef;
                 }
                 prefetch_next_summaries<T, D>(s, layer, unstable, period, topk, extra_tokens, batch,
                                               before, nnd, a.pf_cap);
@@ -1090,13 +1124,16 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
         if (satr && threadIdx.x == 0) satr[blockIdx.x * 4 + 3] = gtimer_s();
     } else {
         // (only attending warps get here when NWS > NWA)
+        if (satr && threadIdx.x == 0) satr[blockIdx.x * 4 + 1] = gtimer_s();
         const int n_att = attend_head_cta<T, D, NST, NWA>(s, a, bh, dsm, abars, s_wm, s_wl, s_q, 1, Sh, rank,
                                                           Sh > 1 ? cstate : nullptr);
+        if (satr && threadIdx.x == 0) satr[blockIdx.x * 4 + 2] = gtimer_s();
         // every rank's state written
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         if (Sh > 1 && rank == 0 && n_att > 0) merge_head_cluster<T, D>(s, a, bh, cstate, Sh, NWA * 32);
         // rank 0 done reading every rank's shared memory
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (satr && threadIdx.x == 0) satr[blockIdx.x * 4 + 3] = gtimer_s();
     }
 }
 

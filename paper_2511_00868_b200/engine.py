@@ -99,6 +99,13 @@ class DecodeEngine:
         # at long context: config 4; fc_score_attend_map)
         self.mixed_clusters = True
         self._mixed: dict = {}
+        # 'partial' steps (some rows at their boundary): the heads due in a
+        # layer get a cluster of CTAs each, the others one CTA each, with the
+        # map rewritten before each step for the rows due then (a static
+        # device buffer per layer pattern, so one graph serves every step)
+        self.partial_clusters = True
+        self._partial: dict = {}      # unstable-head pattern -> (S, n_ctas, buffer) or None
+        self._partial_maps: dict = {}  # (pattern, due rows) -> device map
         # plain steps of layers where only some heads are due (the unstable
         # heads spread over the layers): the due heads' scoring spread over
         # every SM, then one CTA per head selects and attends
@@ -426,7 +433,13 @@ class DecodeEngine:
                 continue
             if scored and not recycle and use_fused:
                 # one launch: every head's CTA scores, selects and attends
-                plan = self._mixed_plan(layer) if kind == "plain" and not force_due else None
+                plan = None
+                if kind == "plain" and not force_due:
+                    plan = self._mixed_plan(layer)
+                elif kind == "partial" and not force_due:
+                    # (where the balanced launch is not used: 35.4 vs 33.9 us per
+                    # layer at config 2 with one row of 16 due, partial_probe.py)
+                    plan = self._partial_plan(layer)
                 st.score_attend(layer, self.q[layer], self.unstable, self.R, self.K, self.out[layer], self.B,
                                 force_due=force_due, extra_tokens=1, kv_prefetch=layer > 0,
                                 k_new=self.k_new[layer], v_new=self.v_new[layer], attend_appended=False,
@@ -517,6 +530,57 @@ class DecodeEngine:
                                   if scored and n_pages > 0 else None)
         return self._mixed[layer]
 
+    def _layer_pattern(self, layer: int) -> tuple:
+        return tuple(h for h in range(self.H) if self.profile.is_unstable(HeadId(layer, h)))
+
+    def _partial_plan(self, layer: int):
+        """(map buffer, S) for a 'partial' step's fused launch of ``layer``,
+        or None (balanced / uniform launch instead).  Sized for the most rows
+        at their boundary on one step under the current phases."""
+        if not (self.partial_clusters and self.fused_score_attend and self.store.score_attend_supported(self.B)):
+            return None
+        pat = self._layer_pattern(layer)
+        if len(pat) == self.H:
+            return None
+        if pat not in self._partial:
+            rows = self._active_rows()
+            per_res = {}
+            for b in rows:
+                per_res[(self.t + self.phase[b]) % self.R] = per_res.get((self.t + self.phase[b]) % self.R, 0) + 1
+            max_due = max(per_res.values()) if per_res else 1
+            n_s = len(rows) * len(pat) + max_due * (self.H - len(pat))
+            n_pages = (max(self.seq_host) + 1 + PAGE_SIZE - 1) // PAGE_SIZE
+            # (per-CTA rate and selection latency as measured for a scored head
+            # at config 2: ~45 GB/s, ~7 us from streamed to attending,
+            # scripts/partial_probe.py)
+            plan = (self.store.cluster_plan(self.B, n_s, n_pages, self.K, bw_sm_gbs=45.0, select_us=7.0)
+                    if n_pages > 0 else None)
+            if plan is not None:
+                S, n_ctas = plan
+                plan = (S, n_ctas, torch.full((n_ctas,), -1, dtype=torch.int32, device=self.device))
+            self._partial[pat] = plan
+        p = self._partial[pat]
+        return None if p is None else (p[2], p[0])
+
+    def _fill_partial_maps(self) -> None:
+        # the CTA maps of this step's due (row, head) pairs into the static buffers
+        due = tuple(self.boundary_rows())
+        active = self._active_rows()
+        for pat, plan in self._partial.items():
+            if plan is None:
+                continue
+            key = (pat, due)
+            m = self._partial_maps.get(key)
+            if m is None:
+                scored = {(b, h) for b in active for h in pat if self.hold[b] != HOLD_WAIT}
+                scored |= {(b, h) for b in due for h in range(self.H)}
+                S, n_ctas, _ = plan
+                if len(self._partial_maps) > 4096:
+                    self._partial_maps.clear()
+                m = self._partial_maps[key] = self.store.cluster_map_pairs(self.B, scored, S, n_ctas).to(
+                    self.device)
+            plan[2].copy_(m, non_blocking=True)
+
     def _use_run(self) -> bool:
         if self.run_kernel is None:
             return self.store.run_split(self.B, self.att_bound) >= 2
@@ -564,6 +628,11 @@ class DecodeEngine:
         staged = kind != "plain" and fetch == "staged"
         if staged:
             self.stager.wait()  # staged promotions have landed
+        if kind == "partial" and not self.score_all_heads:
+            if not use_graph or (kind, False, fetch, self.store.per_row) not in self._graphs:
+                for layer in range(self.L):  # plans (and their buffers) exist before launch / capture
+                    self._partial_plan(layer)
+            self._fill_partial_maps()
         if use_graph:
             key = (kind, self.score_all_heads, fetch, self.store.per_row)
             g = self._graphs.get(key)
@@ -612,6 +681,9 @@ class DecodeEngine:
         if kind == "plain":  # mixed-cluster maps live on the device: build them outside the capture
             for layer in range(self.L):
                 self._mixed_plan(layer)
+        if kind == "partial":
+            for layer in range(self.L):
+                self._partial_plan(layer)
         torch.cuda.synchronize(self.device)
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))

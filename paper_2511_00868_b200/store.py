@@ -350,6 +350,68 @@ class KVStore:
         m += others
         return torch.tensor(m, dtype=torch.int32, device=self.device), S
 
+    def cluster_plan(self, batch: int, n_scored: int, n_pages: int, topk_pages: int, *,
+                     sms: int | None = None, bw_sm_gbs: float = 90.0, bw_gbs: float = 6000.0,
+                     select_us: float = 0.0):
+        """The cluster size S for a launch in which ``n_scored`` of the
+        batch's (row, head) pairs are scored (any pairs: e.g. every head of
+        the rows at their rerank boundary), by the bandwidth model of
+        ``mixed_cluster_map``: (S, CTAs) or None when the uniform launch models
+        as fast or no one-wave grid fits."""
+        if sms is None:
+            if not hasattr(self, "_sms"):
+                self._sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+            sms = self._sms
+        n_s, n_o = n_scored, batch * self.H - n_scored
+        if n_s <= 0 or n_o <= 0:
+            return None
+        att = min(n_pages, topk_pages + 2) * self.page_bytes
+        summ = n_pages * 2 * self.D * self.kv_pool.element_size()
+
+        def est(scored_cta, other_cta):
+            # a scored head's CTAs stream their share, then wait for the selection
+            total = n_s * (summ + att) + n_o * att
+            t_cta = max(scored_cta / (bw_sm_gbs * 1e3) + select_us, other_cta / (bw_sm_gbs * 1e3))
+            return max(t_cta, total / (bw_gbs * 1e3))  # us
+
+        su = self.score_attend_supported(batch)
+        if su < 1:
+            return None
+        best = None
+        for S in (2, 4, 8, 16):  # (clusters of 3 leave GPC SMs unused: a second wave, partial_probe.py)
+            n_ctas = (n_s + (n_o + S - 1) // S) * S
+            if n_ctas > sms or not self.score_attend_map_fits(n_ctas, S):
+                continue
+            t = (est((summ + att) / S, att), S)
+            if best is None or t < best[0]:
+                best = (t, S, n_ctas)
+        if best is None or best[0][0] >= 0.9 * est((summ + att) / su, att / su):
+            return None
+        return best[1], best[2]
+
+    def cluster_map_pairs(self, batch: int, scored, S: int, n_ctas: int) -> torch.Tensor:
+        """Host map for fc_score_attend_map: each (row, head) in ``scored`` a
+        cluster of S CTAs, every other head one CTA (bit 30), S to a cluster;
+        padded with idle CTAs (-1) to ``n_ctas``."""
+        scored = set(scored)
+        n_all = batch * self.H
+        while scored and len(scored) * S + -(-(n_all - len(scored)) // S) * S > n_ctas:
+            scored.discard(max(scored))  # too many for the grid: the rest attend (and score) alone
+        m, others = [], []
+        for b in range(batch):
+            for h in range(self.H):
+                bh = b * self.H + h
+                if (b, h) in scored:
+                    m += [bh] * S
+                else:
+                    others.append(bh | (1 << 30))
+        others += [-1] * (-len(others) % S)
+        m += others
+        if len(m) > n_ctas:
+            raise ValueError(f"map needs {len(m)} CTAs > {n_ctas}")
+        m += [-1] * (n_ctas - len(m))
+        return torch.tensor(m, dtype=torch.int32)
+
     def score_pages(self, layer: int, q: torch.Tensor, batch: int, *, extra_tokens: int = 0) -> None:
         _lib.check(self.lib.fc_score_pages(self.cptr, layer, q.data_ptr(), extra_tokens,
                                            self.scores.data_ptr(), batch, self.stream()),
