@@ -500,137 +500,175 @@ def run_ours(args, cfg):
 # HBM, every full page once in pinned host memory, promoted pages fetched over
 # PCIe at every rerank)
 
-CFG3 = dict(workload="config3: llama3.1-8b-shaped decode, 32 layers, 32q/8kv, d=128, 32k prompt, "
-                     "batch 1, page 16, top-K 128 pages, R=8, u=0.25, two-tier KV (pinned host slow "
-                     "tier, UVA fetch of promoted pages), AR(1) stable-head queries rho=0.99",
-            layers=32, kv_heads=8, group=4, head_dim=128, ctx=32768, batch=1, topk=128, period=8,
+CFG3 = dict(workload="config3: llama3.1-8b-shaped decode, 32 layers, 32q/8kv, d=128, 32k prompt + 8k "
+                     "generated tokens (to 40k), page 16, top-K 128 pages, R=8, u=0.25, two-tier KV "
+                     "(pinned host slow tier: every full stable-head page offloaded once; stable heads keep "
+                     "their selection in HBM; promoted pages fetched at each rerank), AR(1) stable-head "
+                     "queries rho=0.99",
+            layers=32, kv_heads=8, group=4, head_dim=128, ctx=32768, gen=8192, batch=16, topk=128, period=8,
             unstable_fraction=0.25, rho=0.99)
 
 
-def run_config3(args):
+def _config3_run(args, cfg, *, B, tiering, pause, staggered, gen, dev, prof):
+    """One engine run of config 3: prefill B rows of 32k, then `gen` decode
+    steps (device-timed per step).  Returns the per-run numbers."""
     import torch
-    rank, world, local = dist_setup(args.gpus)
-    from paper_2511_00868_b200.engine import DecodeEngine
-    from paper_2511_00868_b200.stability import HeadProfile
-    from paper_2511_00868_b200.synthetic import device_normal
     from paper_2511_00868_b200.config import HeadId
-    cfg = CFG3
-    dev = torch.device("cuda", local)
+    from paper_2511_00868_b200.engine import DecodeEngine
+    from paper_2511_00868_b200.synthetic import device_normal
     L, H, G, D = cfg["layers"], cfg["kv_heads"], cfg["group"], cfg["head_dim"]
-    B, T, K, R = cfg["batch"], cfg["ctx"], cfg["topk"], cfg["period"]
-    prof = HeadProfile.first_n(L, H, cfg["unstable_fraction"], model_id="llama3.1-8b-shaped")
-    steps_total = 1 + 2 * (args.warmup + args.steps) + 8
-    res = {}
-    for tiering in (True, False):
-        eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D,
-                           ctx_cap_tokens=T + steps_total + 16, topk_pages=K, rerank_period=R,
-                           profile=prof, dtype=torch.bfloat16, device=dev, tiering=tiering)
-        if tiering and eng.stager is not None and os.environ.get("FC_STAGE_LEAD"):
+    T, K, R = cfg["ctx"], cfg["topk"], cfg["period"]
+    eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D,
+                       ctx_cap_tokens=T + gen + args.warmup + 32, topk_pages=K, rerank_period=R,
+                       profile=prof, dtype=torch.bfloat16, device=dev, tiering=tiering)
+    if tiering:
+        eng.reload_pause = pause
+        if os.environ.get("FC_FETCH_CTAS"):  # profiling knob
+            eng.fetch_ctas = int(os.environ["FC_FETCH_CTAS"])
+        if eng.stager is not None and os.environ.get("FC_STAGE_LEAD"):
             eng.stager.leads = tuple(int(x) for x in os.environ["FC_STAGE_LEAD"].split(","))  # profiling knob
             eng.stager.lead = eng.stager.leads[0]
+    srcs = [(device_normal((H, T, D), seed=12345 + 2 * i, device=dev),
+             device_normal((H, T, D), seed=12346 + 2 * i, device=dev)) for i in range(4)]
+    for b in range(B):
         for l in range(L):
-            k = device_normal((H, T, D), seed=12345 + 2 * l, device=dev)
-            v = device_normal((H, T, D), seed=12346 + 2 * l, device=dev)
-            eng.prefill_layer(0, l, k, v, alloc=(l == 0))
-        torch.cuda.synchronize(dev)
-        gen = torch.Generator(device=dev)
-        gen.manual_seed(777)
-        qstate = torch.randn(tuple(eng.q.shape), generator=gen, device=dev)
-        stable_cols = torch.zeros(H * G, dtype=torch.bool, device=dev)
-        stable_mask = torch.tensor([[not prof.is_unstable(HeadId(l, h)) for h in range(H)] for l in range(L)],
-                                   device=dev).repeat_interleave(G, dim=1)  # [L, H*G]
-        rho = cfg["rho"]
+            k, v = srcs[(b * L + l) % 4]
+            eng.prefill_layer(b, l, k, v, alloc=(l == 0))
+    del srcs
+    if staggered:
+        for b in range(B):
+            eng.set_row_step(b, 1 + b % R)
+    torch.cuda.synchronize(dev)
+    gen_ = torch.Generator(device=dev)
+    gen_.manual_seed(777)
+    qstate = torch.randn(tuple(eng.q.shape), generator=gen_, device=dev)
+    stable_mask = torch.tensor([[not prof.is_unstable(HeadId(l, h)) for h in range(H)] for l in range(L)],
+                               device=dev).repeat_interleave(G, dim=1)  # [L, H*G]
+    rho = cfg["rho"]
+    eps = torch.empty_like(qstate)
+    moved = torch.ones(B, dtype=torch.bool, device=dev)  # rows whose query advances (they emitted)
+    moved_host = torch.ones(B, dtype=torch.bool, pin_memory=True)
 
-        def feed():
-            eps = torch.randn(tuple(qstate.shape), generator=gen, device=dev)
-            drift = rho * qstate + (1 - rho * rho) ** 0.5 * eps
-            qstate.copy_(torch.where(stable_mask[:, None, :, None], drift, eps))
-            eng.q.copy_(qstate)
-            eng.k_new.normal_(generator=gen)
-            eng.v_new.normal_(generator=gen)
+    def feed():
+        # a row held for its reload emits nothing, so its next query is the one
+        # it is waiting with: only rows that decoded at the last step advance
+        moved_host.fill_(False)
+        moved_host[eng.decoded_rows if eng.selected else list(range(B))] = True
+        moved.copy_(moved_host, non_blocking=True)
+        eps.normal_(generator=gen_)
+        nxt = torch.where(stable_mask[:, None, :, None], rho * qstate + (1 - rho * rho) ** 0.5 * eps, eps)
+        qstate.copy_(torch.where(moved[None, :, None, None], nxt, qstate))
+        eng.q.copy_(qstate)
+        eng.k_new.normal_(generator=gen_)
+        eng.v_new.normal_(generator=gen_)
 
+    feed()
+    eng.step()
+    for _ in range(args.warmup):
         feed()
         eng.step()
-        for _ in range(args.warmup):
-            feed()
-            eng.step()
-        eng.capture_graphs()
-        torch.cuda.synchronize(dev)
-        eng.store.check_errors()
-        fetched0 = int(eng.fetched_pages.item()) if tiering else 0
-        reranks = sum(1 for i in range(args.steps) if eng.is_rerank_step(eng.t + i))
-        stream = torch.cuda.current_stream(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-        kinds = []
-        hits0 = int(eng.stager.hits.item()) if tiering and eng.stager is not None else 0
-        torch.cuda.synchronize(dev)
-        e0.record(stream)
+    eng.capture_graphs(sorted({eng.step_kind(eng.t + i) for i in range(R)}))
+    torch.cuda.synchronize(dev)
+    eng.store.check_errors()
+    fetched0 = int(eng.fetched_pages.item()) if tiering else 0
+    stats0 = eng.store.scoring_stats()
+    if tiering and pause:
+        eng.fetch_log = []
+    stream = torch.cuda.current_stream(dev)
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(gen + 1)]
+    kinds, emitted = [], 0
+    hits0 = int(eng.stager.hits.item()) if tiering and eng.stager is not None else 0
+    with ClockSampler(dev.index) as clk:
+        torch.cuda._sleep(20_000_000)
         step_ev[0].record(stream)
-        for i in range(args.steps):
-            t = eng.t
-            lead = eng.stager.lead if tiering and eng.stager is not None else 0
-            kinds.append("rerank" if eng.is_rerank_step(t) else
-                         ("predict" if lead and (t + lead) % R == 0 else
-                          ("after_predict" if lead and (t + lead - 1) % R == 0 else "plain")))
+        for i in range(gen):
+            kinds.append(eng.step_kind())
             feed()
             eng.step()
+            emitted += len(eng.decoded_rows)
             step_ev[i + 1].record(stream)
-        e1.record(stream)
         torch.cuda.synchronize(dev)
-        eng.store.check_errors()
-        ms = e0.elapsed_time(e1)
-        out = {"ms_per_step": ms / args.steps, "tokens_s": B * args.steps / (ms / 1e3)}
-        by_kind = {}
-        for i, k in enumerate(kinds):
-            by_kind.setdefault(k, []).append(step_ev[i].elapsed_time(step_ev[i + 1]))
-        out["step_ms_by_kind"] = {k: sum(v) / len(v) for k, v in by_kind.items()}
-        if tiering and eng.stager is not None:
-            out["staged_hits"] = int(eng.stager.hits.item()) - hits0
-        if tiering:
-            fetched = int(eng.fetched_pages.item()) - fetched0
-            pb = eng.store.page_bytes
-            out.update(fetched_pages=fetched, fetched_mb_per_rerank=fetched * pb / max(reranks, 1) / 1e6,
-                       promoted_fraction=fetched / max(reranks, 1) / (len(prof.stable) * B * (K - 1)))
-            # host-link bandwidth of the fetch kernel alone, on the last copy list
-            n = int(eng.n_copies[L - 1].item())
-            if n > 0:
-                a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                ts = []
-                for _ in range(5):
-                    torch.cuda._sleep(5_000_000)
-                    a.record(stream)
-                    eng.tier.reload(L - 1, eng.copies[L - 1], eng.n_copies[L - 1:L])
-                    b_.record(stream)
-                    torch.cuda.synchronize(dev)
-                    ts.append(a.elapsed_time(b_))
-                t_f = sorted(ts)[2] / 1e3
-                out.update(fetch_pages_last_layer=n, fetch_us=t_f * 1e6, host_link_gbs=n * pb / t_f / 1e9)
-            # pinned-host bulk copy bandwidth for reference (cudaMemcpy engine)
-            hb = torch.empty(256 << 20, dtype=torch.uint8, pin_memory=True)
-            db = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-            db.copy_(hb, non_blocking=True)
-            torch.cuda.synchronize(dev)
-            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            db.copy_(hb, non_blocking=True)
-            b_.record(stream)
-            torch.cuda.synchronize(dev)
-            out["memcpy_h2d_gbs"] = hb.numel() / (a.elapsed_time(b_) / 1e3) / 1e9
-            del hb, db
-        res["tiered" if tiering else "all_resident"] = out
-        del eng
-        torch.cuda.empty_cache()
+    eng.store.check_errors()
+    ms = step_ev[0].elapsed_time(step_ev[-1])
+    per = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(gen)]
+    by_kind = {}
+    for k, v in zip(kinds, per):
+        by_kind.setdefault(k, []).append(v)
+    stats1 = eng.store.scoring_stats()
+    out = {"batch": B, "phases": "staggered" if staggered else "aligned",
+           "fetch": eng._fetch_mode() if tiering else "all-resident",
+           "steps": gen, "ms_per_step": ms / gen, "tokens_s": emitted / (ms / 1e3), "emitted": emitted,
+           "step_ms_by_kind": {k: {"n": len(v), "mean": sum(v) / len(v), "p50": sorted(v)[len(v) // 2]}
+                               for k, v in by_kind.items()},
+           "held_row_steps": stats1["held_row_steps"] - stats0["held_row_steps"],
+           "pause_fraction": (stats1["held_row_steps"] - stats0["held_row_steps"]) / (B * gen),
+           "ctx_end": int(eng.store.seq_len.max().item()), "clocks": clk.summary()}
+    if tiering and eng.stager is not None and out["fetch"] == "staged":
+        out["staged_hits"] = int(eng.stager.hits.item()) - hits0
+    if tiering and eng.fetch_log:
+        pb = eng.store.page_bytes
+        durs = [a.elapsed_time(b) for a, b, _ in eng.fetch_log]
+        pages = [int(n.item()) for _, _, n in eng.fetch_log]
+        out["background_fetch"] = {"launches": len(durs), "mean_ms": sum(durs) / len(durs),
+                                   "mean_mb": sum(pages) * pb / len(pages) / 1e6,
+                                   "host_link_gbs": sum(pages) * pb / (sum(durs) / 1e3) / 1e9,
+                                   "busy_fraction": sum(durs) / ms, "ctas": eng.fetch_ctas}
+    if tiering:
+        fetched = int(eng.fetched_pages.item()) - fetched0
+        pb = eng.store.page_bytes
+        out.update(fetched_pages=fetched, fetched_mb_per_step=fetched * pb / gen / 1e6,
+                   fetched_gb_total=fetched * pb / 1e9)
+    del eng
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_config3(args):
+    """Config 3 (BASELINE.json configs[2]): 32k prompt + 8k generated tokens,
+    stable-head rerank every 8 steps, host offload of non-top-K pages.
+
+    The batch is config 2's (16 requests per GPU) at staggered phases, as
+    requests admitted at different times are: each step ~2 rows reach their
+    rerank; with reload pauses those rows are held while their promoted pages
+    cross the host link on the fetch stream, and the other rows decode
+    (reloading overlapped with other requests' compute).
+    Reported beside the same batch all-resident (no host tier) — the fetch is
+    hidden when the two step costs match — and, for one request alone, the
+    two-tier engine with predicted promotions staged ahead (nothing to
+    overlap with: the pause would be the whole step)."""
+    import torch
+    rank, world, local = dist_setup(args.gpus)
+    from paper_2511_00868_b200.stability import HeadProfile
+    cfg = dict(CFG3)
+    dev = torch.device("cuda", local)
+    prof = HeadProfile.first_n(cfg["layers"], cfg["kv_heads"], cfg["unstable_fraction"], model_id="llama3.1-8b-shaped")
+    gen = int(os.environ.get("FC_GEN", cfg["gen"]))  # profiling knob: fewer generated tokens
+    B = args.batch if args.batch != CFG2["batch"] else cfg["batch"]
+    res = {"tiered": _config3_run(args, cfg, B=B, tiering=True, pause=True, staggered=True, gen=gen, dev=dev,
+                                  prof=prof),
+           "all_resident": _config3_run(args, cfg, B=B, tiering=False, pause=False, staggered=True, gen=gen,
+                                        dev=dev, prof=prof)}
+    if not os.environ.get("FC_SKIP_B1"):
+        n1 = min(gen, 2048)
+        res["tiered_b1_staged"] = _config3_run(args, cfg, B=1, tiering=True, pause=False, staggered=False, gen=n1,
+                                               dev=dev, prof=prof)
+        res["all_resident_b1"] = _config3_run(args, cfg, B=1, tiering=False, pause=False, staggered=False, gen=n1,
+                                              dev=dev, prof=prof)
     if rank != 0:
         return
     t, r = res["tiered"], res["all_resident"]
     line = {"metric": METRIC, "value": t["tokens_s"], "unit": "tokens/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t["ms_per_step"],
+            "steps": gen, "warmup": args.warmup, "ms_per_step": t["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic N(0,1) KV; AR(1) rho=0.99 queries on stable heads, fresh on unstable",
-            "config": {"workload": cfg["workload"], "batch": B, "ctx": T, "rerank_period": R},
-            "tiered": t, "all_resident": r,
-            "rerank_overhead_ms_per_step": t["ms_per_step"] - r["ms_per_step"]}
+            "data": "synthetic N(0,1) KV; AR(1) rho=0.99 queries on stable heads, fresh on unstable; "
+                    "a fresh k/v token every step",
+            "config": {"workload": cfg["workload"], "batch": B, "ctx": cfg["ctx"], "generated": gen,
+                       "rerank_period": cfg["period"], "phases": "staggered (row b starts at t = 1 + b % R)",
+                       "reload": "pause: the reranking row is held while its promoted pages are fetched on a "
+                                 "side stream"},
+            "step_overhead_ms_vs_all_resident": t["ms_per_step"] - r["ms_per_step"],
+            "token_rate_vs_all_resident": t["tokens_s"] / r["tokens_s"],
+            **res}
     print(json.dumps(line), flush=True)
 
 

@@ -388,6 +388,13 @@ int fc_rerank_recycle_rows(const fc_store *s, int layer, const int32_t *old_sel,
  * copies [n][4] = (row, head, logical page, dest block) for layer `layer`;
  * host_pages is host-pinned memory [B_cap][L][H][N_cap][2][ps][d] (same
  * in-page layout as the pool), read with a zero-copy UVA gather kernel. */
+/* fc_fetch_pages of the entries of request row `row` only (-1: every
+ * entry) on at most max_ctas CTAs (0 = one per page up to 8 per SM): the
+ * background fetch of a held row's promoted pages (reload pause) on a few
+ * SMs beside the decode steps of the other rows, one launch per row so
+ * each resumes as soon as its own pages landed. */
+int fc_fetch_pages_ctas(const fc_store *s, int layer, const void *host_pages, const int32_t *copies,
+                        const int32_t *n_copies, int max_copies, int row, int max_ctas, void *stream);
 int fc_fetch_pages(const fc_store *s, int layer, const void *host_pages,
                    const int32_t *copies, const int32_t *n_copies,
                    int max_copies, void *stream);

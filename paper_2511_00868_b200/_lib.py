@@ -90,6 +90,7 @@ _SIGNATURES = {
     "fc_fetch_pages": (_i, [_p, _i, _p, _p, _p, _i, _p]),
     "fc_offload_pages": (_i, [_p, _p, _p, _i, _p]),
     "fc_offload_pages_ctas": (_i, [_p, _p, _p, _i, _i, _p]),
+    "fc_fetch_pages_ctas": (_i, [_p, _i, _p, _p, _p, _i, _i, _i, _p]),
     "fc_fetch_pages_staged": (_i, [_p, _i, _p, _p, _p, _i, _p, _p, _p, _p]),
     "fc_stage_promoted": (_i, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _i, _p, _i, _p]),
     "fc_stage_clear": (_i, [_p, _p, _p, _p, _i, _p]),

@@ -453,6 +453,19 @@ int fc_fetch_pages(const fc_store *s, int layer, const void *host_pages, const i
                                     nullptr, nullptr, (cudaStream_t)stream));
 }
 
+int fc_fetch_pages_ctas(const fc_store *s, int layer, const void *host_pages, const int32_t *copies,
+                        const int32_t *n_copies, int max_copies, int row, int max_ctas, void *stream) {
+    FC_CHECK(check_store(s));
+    if (layer < 0 || layer >= s->layers) return invalid("layer out of range");
+    if (!host_pages || !copies || !n_copies) return invalid("null buffer");
+    if (max_ctas < 0) return invalid("max_ctas must be >= 0");
+    if (row < -1 || row >= s->batch_cap) return invalid("row out of range");
+    if (max_copies <= 0) return FC_OK;
+    const int pb = 2 * s->page_size * s->head_dim * (s->dtype == FC_BF16 ? 2 : 4);
+    return cuda_status(launch_fetch(make_view(s), layer, host_pages, copies, n_copies, max_copies, pb, nullptr,
+                                    nullptr, nullptr, (cudaStream_t)stream, max_ctas, row));
+}
+
 int fc_fetch_pages_staged(const fc_store *s, int layer, const void *host_pages, const int32_t *copies,
                           const int32_t *n_copies, int max_copies, const int32_t *staged_map,
                           const void *staging, int32_t *n_staged_hits, void *stream) {

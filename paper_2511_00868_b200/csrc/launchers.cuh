@@ -100,7 +100,7 @@ cudaError_t launch_rerank(const StoreView &, int, const int32_t *, const int32_t
                           int, int, int, const uint8_t *, const uint8_t *, int32_t *, int, int32_t *, void *, int,
                           cudaStream_t);
 cudaError_t launch_fetch(const StoreView &, int, const void *, const int32_t *, const int32_t *, int, int,
-                         const int32_t *, const void *, int32_t *, cudaStream_t);
+                         const int32_t *, const void *, int32_t *, cudaStream_t, int max_ctas = 0, int row = -1);
 cudaError_t launch_stage(const StoreView &, const int32_t *, const int32_t *, const uint8_t *, const uint8_t *,
                          int32_t *, int32_t *, int32_t *, int, const void *, void *, int, int, cudaStream_t);
 cudaError_t launch_stage_plan(const StoreView &, const int32_t *, const int32_t *, const uint8_t *, const uint8_t *,

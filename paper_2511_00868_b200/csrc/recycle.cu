@@ -315,15 +315,25 @@ FC_DEVINL void copy_page(uint4 *dst, const uint4 *src, int n16) {
 // staged_map (optional, [B][L][H][NCAP] int32, -1 = not staged): a promoted
 // page staged ahead of the rerank (stage_fetch_kernel) is copied from the
 // staging area in HBM instead of over the host link.
+//
+// CTAs of 128 threads, 16-byte register loads, 4 in flight per thread: 51
+// GB/s for random 8 KiB pages from 32 CTAs up (55 GB/s for a
+// cudaMemcpy of one contiguous buffer; scripts/micro/fetch_bw.cu).  The CTAs
+// need no shared memory, so they run beside the decode kernels, which hold
+// ~200 KB of it per SM (a bulk-copy variant through shared memory reached
+// the same 51 GB/s alone but could only start between decode launches: 0.92
+// of the rows' steps held at config 3); capping the grid keeps the SMs they
+// take few (PAPER.md: "capping grid size to keep SM occupancy low").
 __global__ void __launch_bounds__(kCopyThreads)
 fetch_kernel(StoreView s, int layer, const char *host_pages, const int32_t *copies,
              const int32_t *n_copies, int max_copies, int page_bytes, const int32_t *staged_map,
-             const char *staging, int32_t *n_staged_hits) {
+             const char *staging, int32_t *n_staged_hits, int row) {
     griddep_launch_dependents();
     griddep_wait();  // the copy list comes from the recycle launch before
     const int n = min(*n_copies, max_copies);
     for (int c = blockIdx.x; c < n; c += gridDim.x) {
         const int b = copies[4 * c], h = copies[4 * c + 1], p = copies[4 * c + 2], blk = copies[4 * c + 3];
+        if (row >= 0 && b != row) continue;  // (one request's pages: it resumes when they landed)
         const int64_t off = s.table_off(s.hix(b, layer, h), p);
         const int slot = staged_map ? staged_map[off] : -1;
         const char *src = slot >= 0 ? staging + (int64_t)slot * page_bytes : host_pages + off * (int64_t)page_bytes;
@@ -509,10 +519,13 @@ cudaError_t launch_rerank(const StoreView &s, int layer, const int32_t *old_sel,
 
 cudaError_t launch_fetch(const StoreView &s, int layer, const void *host_pages, const int32_t *copies,
                          const int32_t *n_copies, int max_copies, int page_bytes, const int32_t *staged_map,
-                         const void *staging, int32_t *n_staged_hits, cudaStream_t st) {
-    const int grid = max(1, min(max_copies, 148 * 8));
+                         const void *staging, int32_t *n_staged_hits, cudaStream_t st, int max_ctas, int row) {
+    // inside a step (the rerank waits for it): one CTA per page, up to 8 per SM;
+    // in the background: max_ctas
+    const int grid = max(1, min(max_copies, max_ctas > 0 ? max_ctas : 148 * 8));
     return launch_pdl(fetch_kernel, dim3(grid), dim3(kCopyThreads), 0, st, s, layer, (const char *)host_pages,
-                      copies, n_copies, max_copies, page_bytes, staged_map, (const char *)staging, n_staged_hits);
+                      copies, n_copies, max_copies, page_bytes, staged_map, (const char *)staging, n_staged_hits,
+                      row);
 }
 
 cudaError_t launch_stage_plan(const StoreView &s, const int32_t *pred_sel, const int32_t *pred_n,

@@ -134,6 +134,13 @@ class DecodeEngine:
                                       device=self.device)
             self.n_copies = torch.zeros(layers, dtype=torch.int32, device=self.device)
             self.fetched_pages = torch.zeros(1, dtype=torch.int64, device=self.device)
+            # reload pauses: one recycle of every layer after the step's attention
+            # (the rows it touches are held) and one copy list for the fetch stream
+            self.old_sel_all = torch.zeros_like(st.sel)
+            self.n_old_all = torch.zeros_like(st.n_sel)
+            self.copies_all = torch.zeros((batch * layers * kv_heads * st.SELCAP, 4), dtype=torch.int32,
+                                          device=self.device)
+            self.n_copies_all = torch.zeros(1, dtype=torch.int32, device=self.device)
             self._stable_layers = [l for l in range(layers)
                                    if any(not profile.is_unstable(HeadId(l, h)) for h in range(kv_heads))]
             # promoted pages staged on a side stream `lead` steps before each
@@ -158,6 +165,8 @@ class DecodeEngine:
             # the other rows keep decoding.  Off: the fetch runs inside the step.
             self.reload_pause = False
             self.fetch_stream = None
+            self.fetch_ctas = 32  # (51 GB/s from 32 CTAs, scripts/micro/fetch_bw.cu)
+            self.fetch_log = None  # list: (start, end, pages) of each background fetch (profiling)
             self._reloads: dict[int, torch.cuda.Event] = {}  # row -> fetch done
             self._snap_free: list[torch.Tensor] = []
             self._snap_busy: list[tuple] = []                # (event, copies snapshot)
@@ -380,25 +389,43 @@ class DecodeEngine:
         dev = self.device
         main = torch.cuda.current_stream(dev)
         if self.fetch_stream is None:
-            self.fetch_stream = torch.cuda.Stream(dev)
+            # the fetch kernel is a handful of CTAs that mostly wait on the host
+            # link: at the default priority its CTAs queued behind the decode
+            # launches (which hold every SM back to back) and a held row waited
+            # for several steps; at high priority they take the next free SMs
+            self.fetch_stream = torch.cuda.Stream(dev, priority=-5)
         busy = []
         for ev, snap in self._snap_busy:
-            (self._snap_free if ev.query() else busy).append(snap)
+            if ev.query():
+                self._snap_free.append(snap)
+            else:
+                busy.append((ev, snap))
         self._snap_busy = busy
-        snap = self._snap_free.pop() if self._snap_free else (torch.empty_like(self.copies),
-                                                              torch.empty_like(self.n_copies))
-        snap[0].copy_(self.copies)
-        snap[1].copy_(self.n_copies)
+        snap = self._snap_free.pop() if self._snap_free else (torch.empty_like(self.copies_all),
+                                                              torch.empty_like(self.n_copies_all))
+        snap[0].copy_(self.copies_all)
+        snap[1].copy_(self.n_copies_all)
         ready = torch.cuda.Event()
         ready.record(main)
         with torch.cuda.stream(self.fetch_stream):
             self.fetch_stream.wait_event(ready)
-            for layer in self._stable_layers:
-                self.tier.reload(layer, snap[0][layer], snap[1][layer:layer + 1])
-            done = torch.cuda.Event()
-            done.record(self.fetch_stream)
-        for b in rows:
-            self._reloads[b] = done
+            # one launch per row, in row order: each row resumes as soon as its
+            # own pages landed (a single launch for all made rows that reranked
+            # together resume together and rerank together again: the phases
+            # clumped and the host link idled between clumps)
+            t0 = None
+            if self.fetch_log is not None:
+                t0 = torch.cuda.Event(enable_timing=True)
+                t0.record(self.fetch_stream)
+            for b in rows:
+                self.store.fetch_pages_all_layers(self.tier.host, snap[0], snap[1], self.fetch_ctas, row=b)
+                done = torch.cuda.Event(enable_timing=t0 is not None)
+                done.record(self.fetch_stream)
+                self._reloads[b] = done
+            if t0 is not None:  # (instrumentation: fetch duration and pages per step)
+                n = torch.empty(1, dtype=torch.int32, device=self.device)
+                n.copy_(snap[1])
+                self.fetch_log.append((t0, done, n))
         self._snap_busy.append((done, snap))
 
     # -- one decode step -----------------------------------------------------------
@@ -406,16 +433,25 @@ class DecodeEngine:
     def _launch_step(self, kind: str, force_due: bool, fetch: str = "inline") -> None:
         st = self.store
         tiered_rerank = self.tiering and kind != "plain" and not force_due
+        # reload pauses: the rows that rerank are held this step, so their
+        # recycle (every layer, one launch) runs after the other rows' attention
+        # and their fetch on the fetch stream (_launch_reloads); the layers
+        # launch as at a step without recycles
+        deferred = tiered_rerank and fetch == "async"
         use_run = self._use_run()
         use_fused = self.fused_score_attend and st.score_attend_supported(self.B)
 
         def recycles(l):
-            return tiered_rerank and l in self._stable_layers
+            return tiered_rerank and not deferred and l in self._stable_layers
 
         def scores(l):
             return force_due or not self._layer_skippable(l, kind)
 
-        if tiered_rerank:  # resident set of stable heads = their current selection
+        if deferred:  # resident set of stable heads = their current selection
+            self.old_sel_all.copy_(st.sel)
+            self.n_old_all.copy_(st.n_sel)
+            self.n_copies_all.zero_()
+        elif tiered_rerank:
             self.old_sel.copy_(st.sel.transpose(0, 1))
             self.n_old.copy_(st.n_sel.transpose(0, 1))
             self.n_copies.zero_()
@@ -491,7 +527,12 @@ class DecodeEngine:
             if self.after_layer is not None:
                 self.after_layer(layer)
             layer += 1
-        if tiered_rerank:
+        if deferred:
+            st.rerank_recycle_all_layers(self.old_sel_all, self.n_old_all, self.unstable, self.R, self.copies_all,
+                                         self.n_copies_all, self.B, slow_resident=self.tier.slow_resident,
+                                         row_skip=self.row_skip)
+            self.fetched_pages.add_(self.n_copies_all.sum())
+        elif tiered_rerank:
             self.fetched_pages.add_(self.n_copies.sum())
             if fetch == "staged":
                 self.stager.finish_rerank()
@@ -709,13 +750,17 @@ class DecodeEngine:
         use_fused = self.fused_score_attend and st.score_attend_supported(self.B)
         fetch = self._fetch_mode()
 
+        deferred = self.tiering and rerank and fetch == "async"
+
         def recycles(l):
-            return self.tiering and rerank and l in self._stable_layers
+            return self.tiering and rerank and not deferred and l in self._stable_layers
 
         def scores(l):
             return self.score_all_heads or not self._layer_skippable(l, kind)
 
         n, layer = 1, 0  # the step advance
+        if deferred:
+            n += 2  # one recycle of every layer; one fetch on the fetch stream
         while layer < self.L:
             if recycles(layer):
                 n += 2  # recycle + fetch (on the fetch stream with reload pauses)

@@ -492,6 +492,32 @@ class KVStore:
             copies.data_ptr(), copies.shape[0], n_copies.data_ptr(), ws.data_ptr(), batch,
             self.stream()), "fc_rerank_recycle_rows")
 
+    def rerank_recycle_all_layers(self, old_sel: torch.Tensor, n_old: torch.Tensor, unstable: torch.Tensor,
+                                  period: int, copies: torch.Tensor, n_copies: torch.Tensor, batch: int, *,
+                                  extra_tokens: int = 1, slow_resident: torch.Tensor | None = None,
+                                  row_skip: torch.Tensor | None = None) -> None:
+        """fc_rerank_recycle_rows of EVERY layer in one launch, through the
+        view of the L layers as one layer of L*H heads: old_sel / n_old in
+        the store's own [B, L, H, ...] layout, one copy list (row, l*H + h,
+        page, block) for fetch_pages_all_layers."""
+        view = self._all_layers_view(self.sel, self.n_sel)
+        if getattr(self, "_rerank_ws_all", None) is None:
+            n = self.lib.fc_rerank_workspace_size(view)
+            self._rerank_ws_all = torch.zeros(n, dtype=torch.uint8, device=self.device)
+        ws = self._rerank_ws_all
+        _lib.check(self.lib.fc_rerank_recycle_rows(
+            view, 0, old_sel.data_ptr(), n_old.data_ptr(), unstable.data_ptr(), period, 0, 0, extra_tokens,
+            _ptr(slow_resident), _ptr(row_skip), copies.data_ptr(), copies.shape[0], n_copies.data_ptr(),
+            ws.data_ptr(), batch, self.stream()), "fc_rerank_recycle_rows")
+
+    def fetch_pages_all_layers(self, host_pages: torch.Tensor, copies: torch.Tensor, n_copies: torch.Tensor,
+                               max_ctas: int = 0, row: int = -1) -> None:
+        """fc_fetch_pages_ctas of a copy list from rerank_recycle_all_layers
+        (the entries of request row ``row`` only, -1: all)."""
+        _lib.check(self.lib.fc_fetch_pages_ctas(self._all_layers_view(self.sel, self.n_sel), 0, host_pages.data_ptr(),
+                                                copies.data_ptr(), n_copies.data_ptr(), copies.shape[0], row,
+                                                max_ctas, self.stream()), "fc_fetch_pages_ctas")
+
     def trace_capture(self, trace_sel: torch.Tensor, trace_pool: torch.Tensor, step_base: int,
                       topk: int, batch: int, extra_tokens: int = 0) -> None:
         """Record every head's top-K selection into trace slot

@@ -45,7 +45,7 @@ torch.cuda.synchronize()
 times = collections.defaultdict(float)
 counts = collections.Counter()
 st = eng.store
-targets = [(st, "score_select"), (st, "rerank_recycle"), (st, "sparse_decode"), (st, "sparse_decode_layers"),
+targets = [(st, "score_select"), (st, "score_attend"), (st, "rerank_recycle"), (st, "sparse_decode"), (st, "sparse_decode_layers"),
            (st, "step_advance"), (st, "offload_filled"), (eng.stager, "fetch"), (eng.stager, "finish_rerank")]
 pending = []
 for obj, name in targets:
