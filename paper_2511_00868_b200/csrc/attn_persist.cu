@@ -314,7 +314,7 @@ static int persist_split_t(const StoreView &s, int batch, int max_pages) {
     }
     const int heads = batch * s.H, sms = persist_sms();
     int best = 0;
-    for (int S = 1; S <= 16 && (int64_t)heads * S <= sms; S *= 2) {
+    for (int S = 1; S <= max_cluster() && (int64_t)heads * S <= sms; S *= 2) {
         if (S * NW * 32 < max_pages) continue;  // a warp holds one entry per lane
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(heads * S);

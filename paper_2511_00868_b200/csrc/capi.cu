@@ -59,6 +59,12 @@ static int check_store(const fc_store *s) {
         if (_r != FC_OK) return _r; \
     } while (0)
 
+namespace fc {
+static int g_max_cluster = 16;
+int max_cluster() { return g_max_cluster; }
+void set_max_cluster(int n) { g_max_cluster = n <= 0 ? 16 : (n > 16 ? 16 : n); }
+}  // namespace fc
+
 extern "C" {
 
 const char *fc_version(void) { return "flexicache-b200 0.1 sm_100a"; }
@@ -73,6 +79,7 @@ int fc_debug_score_trace(void *device_buf) { return cuda_status(set_score_trace(
 int fc_debug_sa_trace(void *device_buf) { return cuda_status(set_sa_trace(device_buf)); }
 /* test hook: scoring kernel choice, -1 auto, 0 balanced, 1 head-aligned */
 int fc_debug_score_mode(int mode) { set_score_mode(mode); return FC_OK; }
+int fc_debug_max_cluster(int n) { set_max_cluster(n); return FC_OK; }
 int fc_debug_score_ctas_per_sm(int n) { set_score_ctas_per_sm(n); return FC_OK; }
 /* tuning hook: byte cap of the next-layer summary warm-up in fc_score_attend
  * (0 off, < 0 default 48 MiB) */

@@ -3,6 +3,10 @@
 #include "store.cuh"
 
 namespace fc {
+// largest cluster (CTAs per head) the automatic splits may choose (16; a
+// test hook pins it so differently sized launches split heads alike)
+int max_cluster();
+void set_max_cluster(int n);
 struct AttnArgs {
     int layer;
     const void *q;

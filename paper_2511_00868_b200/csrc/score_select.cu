@@ -1565,7 +1565,7 @@ static int score_attend_split_t(const StoreView &s, int batch) {
         return 0;
     }
     int best = 0;
-    for (int S = 2; S <= 16 && heads * S <= sms; S *= 2) {
+    for (int S = 2; S <= max_cluster() && heads * S <= sms; S *= 2) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(heads * S);
         cfg.blockDim = dim3(NWS * 32);

@@ -664,7 +664,8 @@ int attn_split(const StoreView &s, int dtype, int batch, int max_pages, int n_ct
         if (bocc >= 1) return -(bocc * num_sms());
     }
     int S = 1;
-    while (2 * S <= FC_ATTN_SMAX && (int64_t)n_heads * 2 * S <= slots && 2 * S * 4 * 2 <= max_pages)
+    while (2 * S <= FC_ATTN_SMAX && 2 * S <= max_cluster() && (int64_t)n_heads * 2 * S <= slots &&
+           2 * S * 4 * 2 <= max_pages)
         S *= 2;
     return S;
 }

@@ -4,8 +4,11 @@ SURVEY.md §8(e): the decode path shards by request with no data-path
 collective — each rank owns its requests' KV pool, summaries, tables and
 selections (``KVStore``) — so the only cross-rank operations are the
 measurement barriers and the max-over-ranks of the timed region.  The
-KV-head-sharded configuration (one all-gather of attention outputs per layer)
-is listed as next work in DESIGN.md §6.
+KV-head-sharded configuration (config 5) splits the KV heads of every layer
+over a head group and all-gathers the attention outputs after each layer
+(``HeadGroup``, one NCCL all-gather over NVLink inside the step graph;
+DESIGN.md §6).  tests/test_gpu_dist.py runs it as 2 ranks on one GPU (gloo)
+against the 1-rank engine, bit for bit.
 """
 
 from __future__ import annotations
