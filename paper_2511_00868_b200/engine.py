@@ -192,6 +192,10 @@ class DecodeEngine:
         self.store.seq_len.fill_(-1)
         self.seq_host = [-1] * self.B
         self.selected = True            # initial selections are made per admitted row
+        # requests join at any step: their phases differ, so the kernels always
+        # read the per-request state (the step graphs captured at the first
+        # admission then serve every later step)
+        self._serving = True
         self._initial_rows = set()
         if self.stager is not None:
             # a batch of rows reranks together: each rerank moves many pages
@@ -342,7 +346,8 @@ class DecodeEngine:
     def _per_row_needed(self) -> bool:
         # the kernels read the per-request state only when some active row is
         # out of phase with the global step or rows can be held
-        return (self.tiering and self.reload_pause) or any(self.phase[b] != 0 for b in self._active_rows())
+        return (getattr(self, "_serving", False) or (self.tiering and self.reload_pause)
+                or any(self.phase[b] != 0 for b in self._active_rows()))
 
     def _phases_aligned(self) -> bool:
         ph = {self.phase[b] % self.R for b in self._active_rows()}
