@@ -295,6 +295,20 @@ int fc_score_attend_balanced(const fc_store *s, int layer, const void *q,
                              const void *k_new, const void *v_new, void *out,
                              float *lse, float scale, int attend_appended,
                              int batch, void *stream);
+/* fc_score_attend_balanced whose CTAs beyond one per head help the scored
+ * heads attend: up to 3 per scored head split its attended pages with the
+ * owner CTA, which merges their states (same results up to the order of the
+ * softmax merge).  helper_ws: fc_score_attend_balanced_workspace_size bytes,
+ * zero before the first call, left zero (self-resetting); NULL = no helpers. */
+size_t fc_score_attend_balanced_workspace_size(const fc_store *s, int batch);
+int fc_score_attend_balanced_ws(const fc_store *s, int layer, const void *q,
+                                const uint8_t *unstable, int period, int force_due,
+                                int topk, int extra_tokens, int kv_prefetch,
+                                float *scores_out, int32_t *counters,
+                                const void *k_new, const void *v_new, void *out,
+                                float *lse, float scale, int attend_appended,
+                                int batch, void *helper_ws, size_t helper_ws_bytes,
+                                void *stream);
 int fc_score_attend_map(const fc_store *s, int layer, const void *q,
                         const uint8_t *unstable, int period, int force_due,
                         int topk, int extra_tokens, int kv_prefetch,

@@ -77,6 +77,9 @@ _SIGNATURES = {
     "fc_score_attend_map_fits": (_i, [_p, _i, _i]),
     "fc_score_attend_balanced_supported": (_i, [_p, _i]),
     "fc_score_attend_balanced": (_i, [_p, _i, _p, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _f, _i, _i, _p]),
+    "fc_score_attend_balanced_workspace_size": (_sz, [_p, _i]),
+    "fc_score_attend_balanced_ws": (_i, [_p, _i, _p, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _f, _i, _i, _p,
+                                         _sz, _p]),
     "fc_score_attend_map": (_i, [_p, _i, _p, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _f, _i, _i, _p, _i, _i,
                                  _p]),
     "fc_sparse_decode_layers_supported": (_i, [_p, _i, _i]),

@@ -696,6 +696,31 @@ FC_DEVINL int attend_head_cta(const StoreView &s, const AttnArgs &a, int bh, cha
     return n_att;
 }
 
+// Merge of a head attended by S CTAs of one launch whose states
+// (attend_head_cta's cstate layout: acc [G][D] | m [16] | l [16]) sit in
+// global memory, rank r's at states + r * (G*D + 32); read through L2.
+template <typename T, int D>
+FC_DEVINL void merge_head_global(const StoreView &s, const AttnArgs &a, int bh, const float *states, int S, int nt) {
+    const int G = s.G, GD = G * D + 32;
+    const int b = bh / s.H, h = bh % s.H;
+    T *out = reinterpret_cast<T *>(a.out) + ((int64_t)b * s.H * G + (int64_t)h * G) * D;
+    float *lse = a.lse ? a.lse + (int64_t)bh * G : nullptr;
+    for (int e = threadIdx.x; e < G * D; e += nt) {
+        const int g = e / D;
+        float M = -INFINITY;
+        for (int r = 0; r < S; ++r) M = fmaxf(M, __ldcg(states + (int64_t)r * GD + G * D + g));
+        float L = 0.f, O = 0.f;
+        for (int r = 0; r < S; ++r) {
+            const float mr = __ldcg(states + (int64_t)r * GD + G * D + g);
+            const float f = mr == -INFINITY ? 0.f : exp2f(mr - M);
+            L += __ldcg(states + (int64_t)r * GD + G * D + 16 + g) * f;
+            O += __ldcg(states + (int64_t)r * GD + e) * f;
+        }
+        out[e] = T(O / L);
+        if (lse && e % D == 0) lse[g] = (M + log2f(L)) * 0.69314718055994531f;
+    }
+}
+
 // Cluster merge of a head attended by S CTAs (attend_head_cta with S > 1):
 // rank 0's first nt threads combine every rank's state through DSMEM and
 // write the output.  Caller: a cluster barrier before and after.

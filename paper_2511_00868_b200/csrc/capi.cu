@@ -225,11 +225,29 @@ int fc_score_attend_balanced_supported(const fc_store *s, int batch) {
     return score_attend_balanced_grid(make_view(s), s->dtype, batch);
 }
 
+size_t fc_score_attend_balanced_workspace_size(const fc_store *s, int batch) {
+    if (check_store(s) != FC_OK || batch < 1 || batch > s->batch_cap) return 0;
+    const size_t nh = (size_t)batch * s->kv_heads;
+    return nh * 2 * sizeof(int32_t) + nh * kBalMaxSplit * ((size_t)s->group * s->head_dim + 32) * sizeof(float);
+}
+
 int fc_score_attend_balanced(const fc_store *s, int layer, const void *q, const uint8_t *unstable, int period,
                              int force_due, int topk, int extra_tokens, int kv_prefetch, float *scores_out,
                              int32_t *counters, const void *k_new, const void *v_new, void *out, float *lse,
                              float scale, int attend_appended, int batch, void *stream) {
+    return fc_score_attend_balanced_ws(s, layer, q, unstable, period, force_due, topk, extra_tokens, kv_prefetch,
+                                       scores_out, counters, k_new, v_new, out, lse, scale, attend_appended, batch,
+                                       nullptr, 0, stream);
+}
+
+int fc_score_attend_balanced_ws(const fc_store *s, int layer, const void *q, const uint8_t *unstable, int period,
+                                int force_due, int topk, int extra_tokens, int kv_prefetch, float *scores_out,
+                                int32_t *counters, const void *k_new, const void *v_new, void *out, float *lse,
+                                float scale, int attend_appended, int batch, void *helper_ws, size_t helper_ws_bytes,
+                                void *stream) {
     FC_CHECK(check_store(s));
+    if (helper_ws && helper_ws_bytes < fc_score_attend_balanced_workspace_size(s, batch))
+        return FC_E_CAPACITY;
     if (layer < 0 || layer >= s->layers) return invalid("layer out of range");
     if (batch < 0 || batch > s->batch_cap) return invalid("batch out of range");
     if (period < 1) return invalid("period must be >= 1");  // rerank_due, scoring.py:198-199
@@ -251,6 +269,11 @@ int fc_score_attend_balanced(const fc_store *s, int layer, const void *q, const 
     a.layer = layer; a.q = q; a.k_new = k_new; a.v_new = v_new; a.out = out; a.lse = lse;
     a.scale_log2 = scale * 1.4426950408889634f;
     a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.max_splits = 1;
+    if (helper_ws) {
+        a.bal_flags = reinterpret_cast<int32_t *>(helper_ws);
+        a.bal_state = reinterpret_cast<float *>(reinterpret_cast<char *>(helper_ws) +
+                                                (size_t)batch * s->kv_heads * 2 * sizeof(int32_t));
+    }
     return cuda_status(launch_score_attend_balanced(v, s->dtype, layer, q, unstable, period, force_due, topk,
                                                     extra_tokens, scores_out, counters, batch, kv_prefetch ? 1 : 0,
                                                     a, (cudaStream_t)stream));

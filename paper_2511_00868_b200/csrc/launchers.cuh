@@ -34,7 +34,13 @@ struct AttnArgs {
     // CTAs of that layer then stream them from L2) when those are at most
     // this many bytes; 0 = off (set by the launcher)
     int64_t pf_cap;
+    // fc_score_attend_balanced: the CTAs beyond one per head help the scored
+    // heads attend (null = off): per head a ready flag and a done counter
+    // [2][B_cap*H], and the partial states [B_cap*H][kBalMaxSplit][G*D + 32]
+    int32_t *bal_flags;
+    float *bal_state;
 };
+constexpr int kBalMaxSplit = 4;  // CTAs attending one scored head (owner + helpers)
 
 // persistent multi-layer attention (attn_run.cu)
 struct RunArgs {

@@ -288,7 +288,7 @@ __device__ void block_select_kpt(const uint32_t *keys, int n, int kprime, int32_
     __syncthreads();
     FC_SEL_STAMP();
 #ifdef FC_SEL_PROFILE
-    if (tid == 0) for (int k = 1; k < np_; ++k) printf("phase %d: %lld\n", k, tp[k] - tp[k - 1]);
+    if (tid == 0) for (int k = 1; k < np_; ++k) printf("phase %d: %lld cta %d t %lld\n", k, tp[k] - tp[k - 1], (int)blockIdx.x, tp[0]);
 #endif
 }
 
@@ -1294,9 +1294,46 @@ score_attend_bal_kernel(StoreView s, int layer, const T *__restrict__ q, const u
         }
     }
     if (satr && threadIdx.x == 0) satr[blockIdx.x * 8 + 4] = gtimer_s();
-    if ((int)blockIdx.x >= n_heads) return;
+    // Helpers: the CTAs beyond one per head split the scored heads' attention
+    // with their owners (kh per head, the head's attended pages cut into kh+1
+    // ranges); a helper waits for the owner's selection, attends its range
+    // and leaves its state in global memory for the owner to merge.  Every
+    // CTA derives the same assignment from the prefix of candidate counts.
+    const int n_extra = (int)gridDim.x - n_heads;
+    int n_sc = 0;
+    if (a.bal_flags != nullptr && n_extra > 0)
+        for (int x = 0; x < n_heads; ++x) n_sc += prefix[x + 1] > prefix[x];
+    const int kh = n_sc > 0 ? min(kBalMaxSplit - 1, n_extra / n_sc) : 0;
+    const int GD = s.G * D + 32;
+    int32_t *ready = a.bal_flags, *done = a.bal_flags ? a.bal_flags + n_heads : nullptr;
+    if ((int)blockIdx.x >= n_heads) {
+        const int e = (int)blockIdx.x - n_heads;
+        if (kh == 0 || e >= n_sc * kh) return;
+        int hb = -1;  // the (e / kh)-th scored head
+        for (int x = 0, k = 0; x < n_heads; ++x)
+            if (prefix[x + 1] > prefix[x] && k++ == e / kh) { hb = x; break; }
+        const int rank = 1 + e % kh;
+        if (tid == 0) {
+            int got;
+            while (true) {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(got) : "l"(ready + hb) : "memory");
+                if (got) break;
+                __nanosleep(64);
+            }
+            if (satr) satr[blockIdx.x * 8 + 5] = gtimer_s();
+        }
+        __syncthreads();
+        attend_head_cta<T, D, NST, NW>(s, a, hb, dsm, abars, s_wm, s_wl, nullptr, 1, kh + 1, rank,
+                                       a.bal_state + ((int64_t)hb * kBalMaxSplit + rank) * GD);
+        __syncthreads();
+        if (satr && tid == 0) satr[blockIdx.x * 8 + 6] = gtimer_s();
+        if (tid == 0)  // (release: the state writes of every thread, ordered by the barrier, first)
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(done + hb) : "memory");
+        return;
+    }
     // ---- phase 2: CTA bh owns head bh
     const int bh = blockIdx.x, b = bh / s.H, h = bh % s.H, hx = s.hix(b, layer, h);
+    const bool helped = kh > 0 && prefix[bh + 1] > prefix[bh];
     const int n_pages = pages_of(b);
     if (is_due(bh) && n_pages > 0) {
         if (tid == 0) s.count(FC_STAT_SCORE_EVALS, 1);
@@ -1335,7 +1372,14 @@ score_attend_bal_kernel(StoreView s, int layer, const T *__restrict__ q, const u
             }
             __syncthreads();
             const int kprime = topk - 1;  // n_pages > topk, so kprime < n_cand
-            if (kprime > 0) block_select<kScoreThreads>(keys, n_cand, kprime, out);
+            if (satr && tid == 0) satr[blockIdx.x * 8 + 1] = gtimer_s();  // (owner: keys in smem)
+            // the selection is emitted into shared memory (the ring past the
+            // keys) and copied out coalesced
+            int32_t *sel_s = reinterpret_cast<int32_t *>(keys + s.NCAP);
+            if (kprime > 0) block_select<kScoreThreads>(keys, n_cand, kprime, sel_s);
+            if (satr && tid == 0) satr[blockIdx.x * 8 + 3] = gtimer_s();  // (owner: selected)
+            __syncthreads();
+            for (int i = tid; i < kprime; i += blockDim.x) out[i] = sel_s[i];
             if (tid == 0) {
                 out[kprime] = n_pages - 1;
                 s.n_sel[hx] = topk;
@@ -1343,8 +1387,29 @@ score_attend_bal_kernel(StoreView s, int layer, const T *__restrict__ q, const u
         }
         __syncthreads();  // the selection is written; the keys are dead (the ring reuses them)
     }
+    if (helped && tid == 0)  // the selection is out (the barrier above orders every thread's writes
+        // before this release, which is cumulative): the helpers may attend
+        asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ready + bh), "r"(1) : "memory");
     if (satr && threadIdx.x == 0) satr[blockIdx.x * 8 + 6] = gtimer_s();
-    attend_head_cta<T, D, NST, NW>(s, a, bh, dsm, abars, s_wm, s_wl, nullptr, 1);
+    if (!helped) {
+        attend_head_cta<T, D, NST, NW>(s, a, bh, dsm, abars, s_wm, s_wl, nullptr, 1);
+    } else {
+        float *st0 = a.bal_state + (int64_t)bh * kBalMaxSplit * GD;
+        const int n_att = attend_head_cta<T, D, NST, NW>(s, a, bh, dsm, abars, s_wm, s_wl, nullptr, 1, kh + 1, 0,
+                                                         st0);
+        if (tid == 0) {
+            int got;
+            while (true) {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(got) : "l"(done + bh) : "memory");
+                if (got >= kh) break;
+                __nanosleep(32);
+            }
+            done[bh] = 0;   // self-resetting for the next launch (which waits for this one)
+            ready[bh] = 0;
+        }
+        __syncthreads();
+        if (n_att > 0) merge_head_global<T, D>(s, a, bh, st0, kh + 1, blockDim.x);
+    }
     if (satr && threadIdx.x == 0) satr[blockIdx.x * 8 + 7] = gtimer_s();
 }
 
@@ -1358,7 +1423,8 @@ static size_t score_attend_bal_smem(int n_heads) {
 template <typename T, int D, int NST, int NW>
 static int score_attend_bal_grid_t(const StoreView &s, int batch) {
     const int n_heads = batch * s.H;
-    if (n_heads < 1 || (size_t)s.NCAP * 4 > (size_t)NW * NST * AttnGeom<T, D>::kPageBytes) return 0;
+    // (the ring holds the owner's keys and its selection during the select)
+    if (n_heads < 1 || (size_t)(s.NCAP + s.SELCAP) * 4 > (size_t)NW * NST * AttnGeom<T, D>::kPageBytes) return 0;
     if (s.NCAP > kScoreThreads * kSelMaxKpt) return 0;
     auto k = score_attend_bal_kernel<T, D, NST, NW>;
     const size_t smem = score_attend_bal_smem<T, D, NST, NW>(n_heads);

@@ -92,6 +92,11 @@ class KVStore:
         self._c_flat.row_phase = None
         self._c_flat.row_hold = None
         self.per_row = False
+        # fc_score_attend_balanced: the CTAs beyond one per head help the
+        # scored heads attend (partial steps: a row at its rerank).  Off: the
+        # owner's selection, not its attention, is the layer's critical path
+        # (33.9 us per partial layer without, 39 us with)
+        self.balanced_helpers = False
         # the same store without the counters: selections that are not
         # scheduled score evaluations (initial selection, reload prediction)
         self._c_quiet = _lib.FcStore.from_buffer_copy(self._c)
@@ -284,11 +289,17 @@ class KVStore:
         SM, then per head selection and attention (same results as
         fc_score_select's balanced kernel followed by fc_sparse_decode)."""
         scale = 1.0 / math.sqrt(self.D) if scale is None else scale
-        _lib.check(self.lib.fc_score_attend_balanced(
+        ws = None
+        if self.balanced_helpers:
+            need = int(self.lib.fc_score_attend_balanced_workspace_size(self.cptr, batch))
+            ws = self.__dict__.get("_bal_ws")
+            if ws is None or ws.numel() < need:
+                ws = self._bal_ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
+        _lib.check(self.lib.fc_score_attend_balanced_ws(
             self.cptr, layer, q.data_ptr(), unstable.data_ptr(), period, int(force_due), topk, extra_tokens,
             int(kv_prefetch), self.scores.data_ptr(), self.score_counters.data_ptr(), _ptr(k_new), _ptr(v_new),
-            out.data_ptr(), _ptr(lse), scale, int(attend_appended), batch, self.stream()),
-            "fc_score_attend_balanced")
+            out.data_ptr(), _ptr(lse), scale, int(attend_appended), batch, _ptr(ws), 0 if ws is None else ws.numel(),
+            self.stream()), "fc_score_attend_balanced_ws")
 
     def score_attend_map_fits(self, n_ctas: int, cluster: int) -> bool:
         cache = self.__dict__.setdefault("_map_fits", {})

@@ -135,9 +135,12 @@ due_row = [b for b in range(B) if (eng.t - 1 + eng.phase[b]) % R == 0]
 role = np.array(["extra"] * grid, dtype=object)
 for c in range(min(grid, B * H)):
     role[c] = "owner" if c // H in due_row else "unscored"
+for c in range(B * H, grid):
+    if a[c, 5] > 0:
+        role[c] = "helper"
 names = ["entry", "issued", "released", "landed", "phase1", "scores_ready", "attn_start", "exit"]
 tr = {}
-for r in ("owner", "unscored", "extra"):
+for r in ("owner", "unscored", "helper", "extra"):
     m = role == r
     if m.any():
         tr[r] = {n: np.percentile((a[m, i] - t0) / 1e3, [0, 50, 100]).round(2).tolist()
@@ -146,3 +149,17 @@ res["due_rows"] = due_row
 res["balanced_trace_last_layer"] = tr
 eng.store.check_errors()
 print(json.dumps(res))
+
+# the due row's score rows after the last step (what the owners selected from)
+if os.environ.get("SCORES"):
+    sc = eng.store.scores.view(B, H, -1).float().cpu().numpy()
+    n_pages = (int(eng.store.seq_len.max().item()) + 1 + 15) // 16
+    for b in due_row[:1]:
+        for h in range(2):
+            row = sc[b, h, :n_pages - 1]
+            lo, hi = row.min(), row.max()
+            bins = np.minimum(((row - lo) * (2048 / (hi - lo))).astype(int), 2047)
+            cnt = np.bincount(bins, minlength=2048)
+            print(json.dumps({"b": b, "h": h, "min": float(lo), "max": float(hi), "p50": float(np.median(row)),
+                              "max_bin": int(cnt.max()), "nonempty_bins": int((cnt > 0).sum()),
+                              "top_k_bin_count": int(cnt[np.searchsorted(np.cumsum(cnt[::-1]), 127)])}))

@@ -263,6 +263,29 @@ def test_balanced_bitwise_equals_two_launch():
     for got, want in zip((st.sel, st.n_sel, st.summaries, eng.out, st.scores), ref):
         assert torch.equal(got, want)
     assert int(st.score_counters.abs().sum()) == 0  # left zero for the next launch
+    # the helper CTAs (the 20 CTAs beyond one per head split the scored heads'
+    # attention with their owners): the same selections and summaries; the
+    # outputs differ only by the order of the softmax merge
+    for t, v in zip((st.sel, st.n_sel, st.summaries, st.kv_pool), snap):
+        t.copy_(v)
+    st.balanced_helpers = True
+    try:
+        for _ in range(2):  # twice: the flags reset themselves
+            for t, v in zip((st.sel, st.n_sel, st.summaries, st.kv_pool), snap):
+                t.copy_(v)
+            for l in range(L):
+                st.score_attend_balanced(l, eng.q[l], eng.unstable, R, K, eng.out[l], B, extra_tokens=1,
+                                         kv_prefetch=l > 0, k_new=eng.k_new[l], v_new=eng.v_new[l])
+            torch.cuda.synchronize()
+            st.check_errors()
+            for got, want in zip((st.sel, st.n_sel, st.summaries, st.scores), (ref[0], ref[1], ref[2], ref[4])):
+                assert torch.equal(got, want)
+            err = (eng.out.float() - ref[3].float()).norm() / ref[3].float().norm()
+            assert float(err) < 5e-3, float(err)
+            flags = st._bal_ws[:2 * B * H * 4].view(torch.int32)
+            assert int(flags.abs().sum()) == 0  # ready / done flags left zero for the next launch
+    finally:
+        st.balanced_helpers = False
 
 
 def test_engine_fused_tiered(head_aligned_scoring):
