@@ -709,10 +709,12 @@ def run_config5(args):
     def gather(layer):
         group.gather(holder["eng"].out[layer], out_full[layer])
 
+    # one head shard (a single GPU): the outputs are already whole, no per-layer
+    # exchange — the layers between scored ones run as persistent launches
     eng = DecodeEngine(batch=B, layers=L, kv_heads=Hl, group=G, head_dim=D,
                        ctx_cap_tokens=T + 2 * (args.warmup + args.steps) + 32, topk_pages=K,
                        rerank_period=R, profile=prof, dtype=torch.bfloat16, device=dev,
-                       after_layer=gather)
+                       after_layer=gather if shards > 1 else None)
     holder["eng"] = eng
     srcs = [(device_normal((Hl, T, D), seed=100 * rank + 2 * i, device=dev),
              device_normal((Hl, T, D), seed=100 * rank + 2 * i + 1, device=dev)) for i in range(2)]
