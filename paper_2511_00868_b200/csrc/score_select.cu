@@ -130,6 +130,7 @@ __device__ void block_select_kpt(const uint32_t *keys, int n, int kprime, int32_
         for (int k = 0; k < KPT; ++k)
             if (tid + k * NT < n) atomicAdd(&hist[lbin(kv[k])], 1);
         __syncthreads();
+        FC_SEL_STAMP();
         int loc[BPT], sum = 0;
 #pragma unroll
         for (int j = 0; j < BPT; ++j) {
@@ -148,6 +149,7 @@ __device__ void block_select_kpt(const uint32_t *keys, int n, int kprime, int32_
             run += loc[j];
         }
         __syncthreads();
+        FC_SEL_STAMP();
         const int B = s_digit;
         if (hist[B] <= 32) {
 #pragma unroll
@@ -177,6 +179,7 @@ __device__ void block_select_kpt(const uint32_t *keys, int n, int kprime, int32_
             }
         }
         __syncthreads();
+        FC_SEL_STAMP();
     }
     uint32_t prefix = 0, mask = 0;
     int remaining = kprime;

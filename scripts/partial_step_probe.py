@@ -154,6 +154,7 @@ print(json.dumps(res))
 if os.environ.get("SCORES"):
     sc = eng.store.scores.view(B, H, -1).float().cpu().numpy()
     n_pages = (int(eng.store.seq_len.max().item()) + 1 + 15) // 16
+    np.save("gpurun_out/due_scores.npy", sc[due_row[0], :, :n_pages - 1])
     for b in due_row[:1]:
         for h in range(2):
             row = sc[b, h, :n_pages - 1]
