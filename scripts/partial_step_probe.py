@@ -29,7 +29,7 @@ for b in range(B):
 del srcs
 if os.environ.get("PHASES", "staggered") == "staggered":
     for b in range(B):
-        eng.set_row_step(b, 1 + b % R)
+        eng.set_row_step(b, 1 + b % int(os.environ.get("PHASE_MOD", R)))
 eng.q.copy_(device_normal(tuple(eng.q.shape), seed=99))
 kg = torch.Generator(device="cuda")
 kg.manual_seed(5)
