@@ -307,6 +307,153 @@ __device__ void block_select(const uint32_t *keys, int n, int kprime, int32_t *o
     else block_select_kpt<NT, kSelMaxKpt>(keys, n, kprime, out, sc);
 }
 
+// Compact form of the same selection for a CTA that runs it alone among
+// CTAs streaming pages (the balanced launch's owner): the keys stay in shared
+// memory and every pass is a rolled loop over them, so the code is a few
+// hundred instructions instead of the unrolled register form's thousands.
+// Same result: the kprime largest keys, ties to the lowest index, emitted in
+// ascending index order (np.lexsort((arange, -scores))).  The crossing bin
+// of the value-linear histogram is ranked exactly when it holds <= 32 keys;
+// otherwise (ties / skew) the unrolled block_select runs.
+template <int NT>
+__device__ void block_select_compact(const uint32_t *keys, int n, int kprime, int32_t *out,
+                                     uint32_t *bits /* [2 * ceil(n/32)] shared */) {
+    __shared__ int hist[kSelBins];
+    __shared__ uint32_t s_kmin, s_kmax, s_T;
+    __shared__ int s_digit, s_above, s_ncand, s_ok, s_rem, s_wsum[NT / 32];
+    __shared__ uint32_t cand_key[32];
+    __shared__ int cand_idx[32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    uint32_t lo = 0xffffffffu, hi = 0u;
+#pragma unroll 1
+    for (int i = tid; i < n; i += NT) { const uint32_t k = keys[i]; lo = min(lo, k); hi = max(hi, k); }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+#pragma unroll 1
+    for (int i = tid; i < kSelBins; i += NT) hist[i] = 0;
+    if (tid == 0) { s_kmin = 0xffffffffu; s_kmax = 0u; s_ncand = 0; s_ok = 0; }
+    __syncthreads();
+    if (lane == 0) { atomicMin(&s_kmin, lo); atomicMax(&s_kmax, hi); }
+    __syncthreads();
+    const float fmin = key_to_float(s_kmin), fmax = key_to_float(s_kmax);
+    const float scale = fmax > fmin ? (float)kSelBins / (fmax - fmin) : 0.f;
+    auto lbin = [&](uint32_t key) {
+        const float b = (key_to_float(key) - fmin) * scale;
+        return b >= (float)(kSelBins - 1) ? kSelBins - 1 : (int)b;
+    };
+#pragma unroll 1
+    for (int i = tid; i < n; i += NT) atomicAdd(&hist[lbin(keys[i])], 1);
+    __syncthreads();
+    // descending bins: thread t owns bins [kSelBins-1-t*BPT .. -BPT+1]
+    constexpr int BPT = kSelBins / NT;
+    int sum = 0;
+#pragma unroll 1
+    for (int j = 0; j < BPT; ++j) sum += hist[kSelBins - 1 - (tid * BPT + j)];
+    int x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
+    if (lane == 31) s_wsum[wid] = x;
+    __syncthreads();
+    int before = x - sum;
+#pragma unroll 1
+    for (int w = 0; w < wid; ++w) before += s_wsum[w];
+    int run = before;
+#pragma unroll 1
+    for (int j = 0; j < BPT; ++j) {
+        const int c = hist[kSelBins - 1 - (tid * BPT + j)];
+        if (run < kprime && run + c >= kprime) { s_digit = kSelBins - 1 - (tid * BPT + j); s_above = run; }
+        run += c;
+    }
+    __syncthreads();
+    const int B = s_digit;
+    if (hist[B] > 32) {  // (ties / skew: the general path)
+        __syncthreads();
+        block_select<NT>(keys, n, kprime, out);
+        return;
+    }
+#pragma unroll 1
+    for (int i = tid; i < n; i += NT)
+        if (lbin(keys[i]) == B) {
+            const int slot = atomicAdd(&s_ncand, 1);
+            cand_key[slot] = keys[i];
+            cand_idx[slot] = i;
+        }
+    __syncthreads();
+    if (tid < 32) {
+        const int c = s_ncand, need = kprime - s_above;
+        const uint32_t myk = lane < c ? cand_key[lane] : 0u;
+        const int myi = lane < c ? cand_idx[lane] : 0x7fffffff;
+        int rank = 0, gt = 0;
+#pragma unroll 1
+        for (int j = 0; j < c; ++j) {
+            const uint32_t kj = __shfl_sync(0xffffffffu, myk, j);
+            const int ij = __shfl_sync(0xffffffffu, myi, j);
+            rank += (kj > myk) || (kj == myk && ij < myi);
+            gt += kj > myk;
+        }
+        if (lane < c && rank == need - 1) { s_T = myk; s_rem = need - gt; }
+    }
+    __syncthreads();
+    const uint32_t T = s_T;
+    const int rem = s_rem;
+    // bit-words of keys > T and == T, 32 indices per word, one warp per word
+    const int nw = (n + 31) / 32;
+    uint32_t *gtb = bits, *eqb = bits + nw;
+#pragma unroll 1
+    for (int w = wid; w < nw; w += NT / 32) {
+        const int i = w * 32 + lane;
+        const uint32_t k = i < n ? keys[i] : 0u;
+        const unsigned g = __ballot_sync(0xffffffffu, i < n && k > T);
+        const unsigned e = __ballot_sync(0xffffffffu, i < n && k == T);
+        if (lane == 0) { gtb[w] = g; eqb[w] = e; }
+    }
+    __syncthreads();
+    // thread t owns words [t*WPT, t*WPT + WPT): the lowest-index equal keys
+    // are taken first, then every selected index is written in order
+    const int WPT = (nw + NT - 1) / NT;
+    int eq_cnt = 0;
+#pragma unroll 1
+    for (int u = 0; u < WPT; ++u) { const int wd = tid * WPT + u; if (wd < nw) eq_cnt += __popc(eqb[wd]); }
+    x = eq_cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
+    __syncthreads();
+    if (lane == 31) s_wsum[wid] = x;
+    __syncthreads();
+    int eq_before = x - eq_cnt;
+#pragma unroll 1
+    for (int w = 0; w < wid; ++w) eq_before += s_wsum[w];
+    int take = max(0, min(eq_cnt, rem - eq_before));
+    int sel_cnt = 0;
+#pragma unroll 1
+    for (int u = 0; u < WPT; ++u) {
+        const int wd = tid * WPT + u;
+        if (wd >= nw) break;
+        uint32_t e = eqb[wd], kept = 0;
+        while (take > 0 && e) { const uint32_t low = e & (~e + 1u); kept |= low; e ^= low; --take; }
+        gtb[wd] |= kept;
+        sel_cnt += __popc(gtb[wd]);
+    }
+    x = sel_cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
+    __syncthreads();
+    if (lane == 31) s_wsum[wid] = x;
+    __syncthreads();
+    int pos = x - sel_cnt;
+#pragma unroll 1
+    for (int w = 0; w < wid; ++w) pos += s_wsum[w];
+#pragma unroll 1
+    for (int u = 0; u < WPT; ++u) {
+        const int wd = tid * WPT + u;
+        if (wd >= nw) break;
+        uint32_t selw = gtb[wd];
+        while (selw) { out[pos++] = wd * 32 + (__ffs(selw) - 1); selw &= selw - 1; }
+    }
+    __syncthreads();
+}
+
+
 // ---------------------------------------------------------------------------
 // scoring of one chunk of pages by one CTA
 
@@ -1379,7 +1526,12 @@ score_attend_bal_kernel(StoreView s, int layer, const T *__restrict__ q, const u
             // the selection is emitted into shared memory (the ring past the
             // keys) and copied out coalesced
             int32_t *sel_s = reinterpret_cast<int32_t *>(keys + s.NCAP);
+            uint32_t *bits = reinterpret_cast<uint32_t *>(sel_s + s.SELCAP);
+#ifndef FC_BAL_UNROLLED_SELECT
+            if (kprime > 0) block_select_compact<kScoreThreads>(keys, n_cand, kprime, sel_s, bits);
+#else
             if (kprime > 0) block_select<kScoreThreads>(keys, n_cand, kprime, sel_s);
+#endif
             if (satr && tid == 0) satr[blockIdx.x * 8 + 3] = gtimer_s();  // (owner: selected)
             __syncthreads();
             for (int i = tid; i < kprime; i += blockDim.x) out[i] = sel_s[i];
@@ -1427,7 +1579,8 @@ template <typename T, int D, int NST, int NW>
 static int score_attend_bal_grid_t(const StoreView &s, int batch) {
     const int n_heads = batch * s.H;
     // (the ring holds the owner's keys and its selection during the select)
-    if (n_heads < 1 || (size_t)(s.NCAP + s.SELCAP) * 4 > (size_t)NW * NST * AttnGeom<T, D>::kPageBytes) return 0;
+    if (n_heads < 1 || (size_t)(s.NCAP + s.SELCAP + 2 * (s.NCAP / 32 + 1)) * 4 >
+                          (size_t)NW * NST * AttnGeom<T, D>::kPageBytes) return 0;
     if (s.NCAP > kScoreThreads * kSelMaxKpt) return 0;
     auto k = score_attend_bal_kernel<T, D, NST, NW>;
     const size_t smem = score_attend_bal_smem<T, D, NST, NW>(n_heads);

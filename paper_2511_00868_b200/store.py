@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import torch
 
@@ -93,10 +94,11 @@ class KVStore:
         self._c_flat.row_hold = None
         self.per_row = False
         # fc_score_attend_balanced: the CTAs beyond one per head help the
-        # scored heads attend (partial steps: a row at its rerank).  Off: the
-        # owner's selection, not its attention, is the layer's critical path
-        # (33.9 us per partial layer without, 39 us with)
-        self.balanced_helpers = False
+        # scored heads attend (partial steps: a row at its rerank).  Off by
+        # default (FC_BAL_HELPERS=1: on): measured slower at config 2 even
+        # with the compact owner select (staggered 11.7k vs 12.0k tokens/s;
+        # DESIGN.md §4)
+        self.balanced_helpers = os.environ.get("FC_BAL_HELPERS", "0") == "1"
         # the same store without the counters: selections that are not
         # scheduled score evaluations (initial selection, reload prediction)
         self._c_quiet = _lib.FcStore.from_buffer_copy(self._c)
