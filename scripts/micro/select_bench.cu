@@ -7,6 +7,18 @@
 namespace fc { int max_cluster() { return 16; } }
 
 template <int NT>
+__global__ void sel_compact_kernel(const float *scores, int n, int kprime, long long *cyc, int32_t *out) {
+    __shared__ uint32_t keys[4096];
+    __shared__ uint32_t bits[2 * 4096 / 32 + 2];
+    for (int i = threadIdx.x; i < n; i += NT) keys[i] = fc::score_key(scores[(int64_t)blockIdx.x * n + i]);
+    __syncthreads();
+    const long long t0 = clock64();
+    fc::block_select_compact<NT>(keys, n, kprime, out + (int64_t)blockIdx.x * kprime, bits);
+    __syncthreads();
+    if (threadIdx.x == 0) cyc[blockIdx.x] = clock64() - t0;
+}
+
+template <int NT>
 __global__ void sel_kernel(const float *scores, int n, int kprime, long long *cyc, int32_t *out) {
     __shared__ uint32_t keys[4096];
     for (int i = threadIdx.x; i < n; i += NT) keys[i] = fc::score_key(scores[(int64_t)blockIdx.x * n + i]);
@@ -36,6 +48,16 @@ int main(int argc, char **argv) {
         sel_kernel<512><<<rows, 512>>>(d, n, 127, cyc, out);
         cudaMemcpy(c.data(), cyc, rows * 8, cudaMemcpyDeviceToHost);
         printf("NT=512:"); for (auto x : c) printf(" %lld", x); printf("\n");
+        std::vector<int32_t> o1((size_t)rows * 127), o2(o1.size());
+        cudaMemcpy(o1.data(), out, o1.size() * 4, cudaMemcpyDeviceToHost);
+        sel_compact_kernel<256><<<rows, 256>>>(d, n, 127, cyc, out);
+        cudaMemcpy(c.data(), cyc, rows * 8, cudaMemcpyDeviceToHost);
+        printf("compact256:"); for (auto x : c) printf(" %lld", x); printf("\n");
+        sel_compact_kernel<512><<<rows, 512>>>(d, n, 127, cyc, out);
+        cudaMemcpy(c.data(), cyc, rows * 8, cudaMemcpyDeviceToHost);
+        printf("compact512:"); for (auto x : c) printf(" %lld", x); printf("\n");
+        cudaMemcpy(o2.data(), out, o2.size() * 4, cudaMemcpyDeviceToHost);
+        printf("same selection: %d\n", (int)(o1 == o2));
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
