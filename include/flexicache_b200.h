@@ -202,6 +202,15 @@ int fc_select_topk(const float *scores, int stride, const int32_t *n_valid,
                    int n_heads, int topk, int pin_last, int32_t *sel_out,
                    int32_t *n_out, void *stream);
 
+/* select_topk (scoring.py:164-193) exactly on float64 scores[n] (the
+ * reference's own precision, no rounding to fp32 keys): the min(k, n)
+ * pages with the highest scores, ties to the lower index, pin_last: page
+ * n-1 always in; sel_out[k] ascending, *n_out the count.  workspace: n
+ * bytes.  n <= 12288. */
+int fc_select_topk_f64(const double *scores, int n, int topk, int pin_last,
+                       uint8_t *workspace, int32_t *sel_out, int32_t *n_out,
+                       void *stream);
+
 /* ---- (3) paged sparse decode attention ---------------------------------- */
 
 /* For every (row, head) of `layer` among rows [0, batch): attend its query

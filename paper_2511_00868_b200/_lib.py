@@ -63,6 +63,7 @@ _SIGNATURES = {
     "fc_free_row": (_i, [_p, _i, _p]),
     "fc_step_advance": (_i, [_p, _i, _p]),
     "fc_step_advance_counted": (_i, [_p, _i, _p, _i, _p]),
+    "fc_select_topk_f64": (_i, [_p, _i, _i, _i, _p, _p, _p, _p]),
     "fc_kv_prefill": (_i, [_p, _i, _i, _p, _p, _i, _p]),
     "fc_kv_append": (_i, [_p, _i, _p, _p, _i, _p]),
     "fc_kv_gather": (_i, [_p, _i, _i, _i, _i, _p, _p, _p]),

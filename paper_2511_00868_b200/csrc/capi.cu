@@ -343,6 +343,17 @@ int fc_select_topk(const float *scores, int stride, const int32_t *n_valid, int 
                                      (cudaStream_t)stream));
 }
 
+int fc_select_topk_f64(const double *scores, int n, int topk, int pin_last, uint8_t *workspace, int32_t *sel_out,
+                       int32_t *n_out, void *stream) {
+    if (topk < 1) return invalid("k must be >= 1");
+    if (n < 0) return invalid("n must be >= 0");
+    if (n > kMaxPagesCap) return FC_E_CAPACITY;
+    if (!scores || !workspace || !sel_out || !n_out) return invalid("null buffer");
+    if (n == 0) return cuda_status(cudaMemsetAsync(n_out, 0, sizeof(int32_t), (cudaStream_t)stream));
+    return cuda_status(launch_select_f64(scores, n, topk, pin_last ? 1 : 0, workspace, sel_out, n_out,
+                                         (cudaStream_t)stream));
+}
+
 size_t fc_sparse_decode_workspace_size(const fc_store *s, int batch, int max_pages, int n_ctas) {
     if (check_store(s) != FC_OK || max_pages < 1 || n_ctas < 0) return 0;
     const StoreView v = make_view(s);

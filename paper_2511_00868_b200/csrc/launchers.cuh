@@ -122,4 +122,5 @@ cudaError_t launch_offload(const StoreView &, void *, const int32_t *, int, int,
 cudaError_t launch_offload_filled(const StoreView &, void *, const uint8_t *, uint8_t *, int, int, cudaStream_t);
 cudaError_t launch_evict_unselected(const StoreView &, const uint8_t *, int, int, cudaStream_t);
 
+cudaError_t launch_select_f64(const double *, int, int, int, uint8_t *, int32_t *, int32_t *, cudaStream_t);
 }  // namespace fc

@@ -1630,6 +1630,58 @@ cudaError_t launch_score_attend_balanced(const StoreView &s, int dtype, int laye
                                                               scores, counters, batch, kv_prefetch, a, st);
 }
 
+// Exact select over float64 scores (the per-call select_topk API on the
+// reference's own float64 scores, scoring.py:164-193): the rank of each page
+// among all — a higher score, or an equal score at a lower index, ranks
+// first (np.lexsort((arange, -scores))) — counted against every other page
+// (n <= 12288: at most 1.5e8 comparisons), then the pages of rank < kprime
+// (and the pinned last page) compacted in ascending index order by one CTA.
+// No rounding of the scores, so no ties that float64 does not have.
+__global__ void __launch_bounds__(256)
+rank_f64_kernel(const double *__restrict__ scores, int n, int kprime, int pin_last, uint8_t *keep) {
+    __shared__ double tile[1024];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nc = pin_last ? n - 1 : n;  // candidates (the last page is pinned)
+    const double si = i < nc ? scores[i] : 0.0;
+    int rank = 0;
+    for (int t0 = 0; t0 < nc; t0 += 1024) {
+        __syncthreads();
+        for (int j = threadIdx.x; j < 1024 && t0 + j < nc; j += blockDim.x) tile[j] = scores[t0 + j];
+        __syncthreads();
+        const int m = min(1024, nc - t0);
+        if (i < nc)
+            for (int j = 0; j < m; ++j) {
+                const double sj = tile[j];
+                rank += (sj > si) || (sj == si && t0 + j < i);
+            }
+    }
+    if (i < n) keep[i] = (i < nc) ? (rank < kprime) : 1;
+}
+
+__global__ void __launch_bounds__(1024) compact_keep_kernel(const uint8_t *keep, int n, int32_t *out, int32_t *n_out) {
+    using Scan = cub::BlockScan<int, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    int carry = 0;
+    for (int c0 = 0; c0 < n; c0 += 1024) {
+        const int i = c0 + threadIdx.x;
+        const int f = i < n ? keep[i] : 0;
+        int pos, tot;
+        Scan(tmp).ExclusiveSum(f, pos, tot);
+        if (f) out[carry + pos] = i;
+        carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *n_out = carry;
+}
+
+cudaError_t launch_select_f64(const double *scores, int n, int topk, int pin_last, uint8_t *keep, int32_t *out,
+                              int32_t *n_out, cudaStream_t st) {
+    const int kprime = pin_last ? topk - 1 : topk;  // (k >= n: every page)
+    rank_f64_kernel<<<(n + 255) / 256, 256, 0, st>>>(scores, n, kprime, pin_last, keep);
+    compact_keep_kernel<<<1, 1024, 0, st>>>(keep, n, out, n_out);
+    return cudaGetLastError();
+}
+
 // standalone select over caller scores: grid n_heads, block kScoreThreads
 __global__ void __launch_bounds__(kScoreThreads)
 select_topk_kernel(const float *scores, int stride, const int32_t *n_valid, int topk,

@@ -283,17 +283,22 @@ def select_topk(scores, k: int, pinned=(), epoch: int = 0) -> TopKSet:
     if n == 0:
         return TopKSet(pages=(), epoch=epoch)
     dev = _device()
-    st = torch.as_tensor(s, dtype=torch.float32).to(dev)
+    # the reference's float64 scores as they are (fc_select_topk_f64: exact
+    # ranks, no fp32 rounding — distinct float64 scores never become ties)
+    st = torch.as_tensor(s, dtype=torch.float64).to(dev)
     pin_last = pins == [n - 1]
     if pins and not pin_last:
-        # pinned pages never compete and always enter: give them the top key
+        # pinned pages never compete and always enter: give them the top score
         st[torch.as_tensor(pins, device=dev)] = float("inf")
-    out = torch.empty((1, k), dtype=torch.int32, device=dev)
+    out = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
     n_out = torch.empty(1, dtype=torch.int32, device=dev)
-    select_topk_device(st.reshape(1, n).contiguous(), torch.tensor([n], dtype=torch.int32, device=dev),
-                       k, pin_last, out, n_out)
+    ws = torch.empty(n, dtype=torch.uint8, device=dev)
+    lib = _lib.load()
+    _lib.check(lib.fc_select_topk_f64(st.data_ptr(), n, k, int(pin_last), ws.data_ptr(), out.data_ptr(),
+                                      n_out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream),
+               "fc_select_topk_f64")
     cnt = int(n_out.item())
-    return TopKSet(pages=tuple(out[0, :cnt].tolist()), epoch=epoch)
+    return TopKSet(pages=tuple(out[:cnt].tolist()), epoch=epoch)
 
 
 def rerank_due(head: HeadId, step: int, profile, period: int) -> bool:

@@ -127,7 +127,7 @@ def test_select_topk_beyond_8192_candidates():
     """The 48-keys-per-thread selection path (8192 < n <= 12288: config 4's
     128k context plus generation): tie-heavy and continuous scores, small and
     large k, exact against the oracle's select_topk."""
-    from paper_2511_00868_b200.scoring import select_topk
+    from paper_2511_00868_b200.scoring import select_topk, select_topk_device
     rng = np.random.default_rng(12)
     for n in (8193, 9001, 10240, 12288):
         for k in (1, 2, 128, 1000):
@@ -135,7 +135,33 @@ def test_select_topk_beyond_8192_candidates():
                 scores = (rng.integers(-3, 4, size=n).astype(float) if ties
                           else rng.standard_normal(n).astype(np.float32).astype(float))
                 got = select_topk(scores, k, pinned=(n - 1,))
-                assert got.pages == O.select_topk_fast(scores, k, (n - 1,)), (n, k, ties)
+                want = O.select_topk_fast(scores, k, (n - 1,))
+                assert got.pages == want, (n, k, ties)
+                # the engine's fp32 device select (the scores are fp32-exact here)
+                st = torch.as_tensor(scores, dtype=torch.float32, device="cuda").reshape(1, n)
+                out = torch.empty((1, k), dtype=torch.int32, device="cuda")
+                n_out = torch.empty(1, dtype=torch.int32, device="cuda")
+                select_topk_device(st, torch.tensor([n], dtype=torch.int32, device="cuda"), k, True, out, n_out)
+                assert tuple(out[0, :int(n_out.item())].tolist()) == want, (n, k, ties)
+
+
+def test_select_topk_float64_scores_that_collide_in_fp32():
+    """The per-call select_topk ranks the reference's float64 scores as they
+    are: scores that differ only below fp32 precision keep their float64 order
+    (a cast to fp32 keys would turn them into index-ordered ties)."""
+    from paper_2511_00868_b200.scoring import select_topk
+    rng = np.random.default_rng(13)
+    for n in (17, 300, 4097, 12288):
+        base = rng.standard_normal(n)
+        # groups of pages whose float64 scores differ by ~1e-12 relative
+        scores = np.round(base, 1) + rng.standard_normal(n) * 1e-12
+        assert len(set(scores.astype(np.float32).tolist())) < len(set(scores.tolist()))
+        for k in (1, 5, 64, n):
+            for pinned in ((), (n - 1,), (0, n // 2)):
+                if len(pinned) > k:
+                    continue
+                got = select_topk(scores, k, pinned=pinned)
+                assert got.pages == O.select_topk(scores, k, pinned), (n, k, pinned)
 
 
 # ---------------------------------------------------------------------------
