@@ -73,6 +73,8 @@ def parse():
                     help="request phases: aligned (all rows admitted together, rerank on the same "
                          "step) or staggered (row b starts at its own t = 1 + b: each step ~B/R rows "
                          "rerank, as requests admitted at different times do)")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the mask / phase variants reported inside the config-2 line")
     ap.add_argument("--batch", type=int, default=CFG2["batch"])
     ap.add_argument("--ctx", type=int, default=CFG2["ctx"])
     ap.add_argument("--layers", type=int, default=CFG2["layers"])
@@ -239,6 +241,75 @@ def run_reference(args, cfg):
 
 # ---------------------------------------------------------------------------
 # our arm
+
+def _variant_run(args, cfg, *, spread: bool, phases: str, steps: int, dev):
+    """Device throughput of config 2 under another unstable-head mask or
+    other request phases (same workload, inputs and timing as the headline):
+    {"value", "ms_per_step", "p50_ms"}."""
+    import torch
+    from paper_2511_00868_b200.config import HeadId
+    from paper_2511_00868_b200.engine import DecodeEngine
+    from paper_2511_00868_b200.stability import HeadProfile
+    from paper_2511_00868_b200.synthetic import device_normal
+    L, H, G, D = cfg["layers"], cfg["kv_heads"], cfg["group"], cfg["head_dim"]
+    B, T, K, R = cfg["batch"], cfg["ctx"], cfg["topk"], cfg["period"]
+    if spread:
+        n = round(cfg["unstable_fraction"] * H)
+        prof = HeadProfile(model_id="llama3.1-8b-shaped", n_layers=L, n_heads_per_layer=H, fraction=n / H,
+                           unstable=tuple(HeadId(l, h) for l in range(L) for h in range(n)))
+    else:
+        prof = HeadProfile.first_n(L, H, cfg["unstable_fraction"], model_id="llama3.1-8b-shaped")
+    total = 2 + args.warmup + steps
+    eng = DecodeEngine(batch=B, layers=L, kv_heads=H, group=G, head_dim=D, ctx_cap_tokens=T + total + 16,
+                       topk_pages=K, rerank_period=R, profile=prof, dtype=torch.bfloat16, device=dev)
+    srcs = [(device_normal((H, T, D), seed=12345 + 2 * i, device=dev),
+             device_normal((H, T, D), seed=12345 + 2 * i + 1, device=dev)) for i in range(4)]
+    for b in range(B):
+        for l in range(L):
+            k, v = srcs[(b * L + l) % 4]
+            eng.prefill_layer(b, l, k, v, alloc=(l == 0))
+    del srcs
+    if phases == "staggered":
+        for b in range(B):
+            eng.set_row_step(b, 1 + b % R)
+    qs = [device_normal(tuple(eng.q.shape), seed=12445 + i, device=dev) for i in range(4)]
+    g = torch.Generator(device=dev)
+    g.manual_seed(77)
+    kv = torch.empty((total,) + tuple(eng.k_new.shape), dtype=eng.k_new.dtype, device=dev)
+    vv = torch.empty_like(kv)
+    kv.normal_(generator=g)
+    vv.normal_(generator=g)
+    it = [0]
+
+    def feed(i):
+        eng.q.copy_(qs[i % 4])
+        eng.k_new.copy_(kv[it[0] % total])
+        eng.v_new.copy_(vv[it[0] % total])
+        it[0] += 1
+
+    feed(0)
+    eng.step()
+    for i in range(args.warmup):
+        feed(i)
+        eng.step()
+    eng.capture_graphs(sorted({eng.step_kind(eng.t + i) for i in range(max(steps, R))}))
+    torch.cuda.synchronize(dev)
+    stream = torch.cuda.current_stream(dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    torch.cuda._sleep(50_000_000)
+    ev[0].record(stream)
+    for i in range(steps):
+        feed(i)
+        eng.step()
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize(dev)
+    eng.store.check_errors()
+    ms = ev[0].elapsed_time(ev[-1])
+    per = sorted(ev[i].elapsed_time(ev[i + 1]) for i in range(steps))
+    del eng, kv, vv, qs
+    torch.cuda.empty_cache()
+    return {"value": B * steps / (ms / 1e3), "ms_per_step": ms / steps, "p50_ms": per[len(per) // 2]}
+
 
 def run_ours(args, cfg):
     import torch
@@ -445,6 +516,19 @@ def run_ours(args, cfg):
                "ms_per_step": ems / args.steps}
         eng.store.check_errors()
 
+    variants = None
+    if world == 1 and not args.no_variants and cfg.get("key", "config2") == "config2" and \
+            not os.environ.get("FC_PROFILE"):
+        # the same workload under the other mask / phases (the headline's mask
+        # is the reference fixture: the unstable heads fill layers 0-7)
+        del eng, qs, ks, vs
+        torch.cuda.empty_cache()
+        variants = {
+            "spread_mask": {"what": "the same u = 0.25 as the first round(u*H) KV heads of every layer",
+                            **_variant_run(args, cfg, spread=True, phases="aligned", steps=args.steps, dev=dev)},
+            "staggered_phases": {"what": "row b starts at its own t = 1 + b % R (one row at its rerank per step)",
+                                 **_variant_run(args, cfg, spread=False, phases="staggered", steps=args.steps,
+                                                dev=dev)}}
     if rank != 0:
         return
     cpu = None
@@ -490,6 +574,7 @@ def run_ours(args, cfg):
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
         "e2e": e2e,
+        **({"variants": variants} if variants else {}),
     }
     print(json.dumps(line), flush=True)
 
