@@ -162,3 +162,48 @@ def test_tiered_peak_commit_held_until_offload_lands():
     assert m.finished == 2
     assert admitted_at[0] == 0 and admitted_at[1] >= eng.lag  # waited for request 0's offload
     assert loop.committed == 0
+
+
+class _PausingEngine(_Engine):
+    """Stand-in whose rows are held one step at each of their own 4th steps
+    (the reload pause): a held row emits nothing that step."""
+
+    def __init__(self, *a):
+        super().__init__(*a)
+        self.t_row = {}
+        self.decoded_rows = []
+
+    def admit(self, row, keys, values):
+        super().admit(row, keys, values)
+        self.t_row[row] = 1
+
+    def retire(self, row):
+        super().retire(row)
+        self.t_row.pop(row, None)
+
+    def step(self):
+        super().step()
+        self.decoded_rows = []
+        for row, t in self.t_row.items():
+            if t % 4 == 0 and not getattr(self, "_held", {}).get(row):
+                self.__dict__.setdefault("_held", {})[row] = True  # held once at its boundary
+                continue
+            self.__dict__.setdefault("_held", {})[row] = False
+            self.decoded_rows.append(row)
+            self.t_row[row] = t + 1
+
+
+def test_held_rows_emit_nothing_and_the_pause_fraction_counts_them():
+    """simulator.py:321-323,542: a reloading request does not step; the
+    others do.  Tokens add up, and Metrics.pause_steps counts the held
+    row-steps."""
+    eng = _PausingEngine(2, 2, 2, 10_000)
+    reqs = [Request(0, 0.0, 100, 9), Request(1, 0.0, 120, 9)]
+    loop = ServingLoop(eng, reqs, make_prompt=lambda r: (r.prompt_tokens, r.prompt_tokens),
+                       feed=lambda e: None, timer=lambda fn: (fn(), 0.01)[1])
+    m = loop.run()
+    assert m.finished == 2
+    assert m.output_tokens == 2 * 8
+    # 8 decoded tokens per request with a hold at t = 4 and t = 8 -> 10 steps each
+    assert m.pause_steps == 4 and m.decode_steps == 10
+    assert abs(m.pause_fraction - 4 / 20) < 1e-12
