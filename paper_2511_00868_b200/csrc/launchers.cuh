@@ -39,6 +39,7 @@ struct AttnArgs {
     // [2][B_cap*H], and the partial states [B_cap*H][kBalMaxSplit][G*D + 32]
     int32_t *bal_flags;
     float *bal_state;
+    int compact_select;   // fc_score_attend: rolled-loop select (block_select_compact)
 };
 constexpr int kBalMaxSplit = 4;  // CTAs attending one scored head (owner + helpers)
 

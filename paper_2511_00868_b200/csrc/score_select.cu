@@ -842,10 +842,12 @@ struct HeadScoreGeom {
 // attention ring / merge scratch)
 template <typename T, int D, int NST, int NWA>
 __host__ __device__ constexpr size_t score_attend_ring_bytes(int ncap) {
-    return (size_t)HeadScoreGeom<T, D>::kStages * HeadScoreGeom<T, D>::kChunkBytes + (size_t)ncap * 4 >
+    // (keys [ncap] then the compact select's bit words [2 * (ncap/32 + 1)])
+    return (size_t)HeadScoreGeom<T, D>::kStages * HeadScoreGeom<T, D>::kChunkBytes + (size_t)ncap * 4 +
+                       (size_t)(ncap / 32 + 1) * 8 >
                    (size_t)NWA * NST * AttnGeom<T, D>::kPageBytes
-               ? (((size_t)HeadScoreGeom<T, D>::kStages * HeadScoreGeom<T, D>::kChunkBytes + (size_t)ncap * 4 + 127) &
-                  ~(size_t)127)
+               ? (((size_t)HeadScoreGeom<T, D>::kStages * HeadScoreGeom<T, D>::kChunkBytes + (size_t)ncap * 4 +
+                   (size_t)(ncap / 32 + 1) * 8 + 127) & ~(size_t)127)
                : (size_t)NWA * NST * AttnGeom<T, D>::kPageBytes;
 }
 
@@ -1018,10 +1020,19 @@ __device__ int score_head_stream(const StoreView &s, int layer, const T *__restr
 // pinned last page (select_topk, scoring.py:164-193).  Every thread of the
 // selecting CTA calls it.
 template <int NT>
-__device__ void score_head_select(const StoreView &s, const uint32_t *keys, int n_cand, int topk, int hx) {
+__device__ void score_head_select(const StoreView &s, const uint32_t *keys, int n_cand, int topk, int hx,
+                                  uint32_t *compact_bits = nullptr) {
     int32_t *out = s.sel + (int64_t)hx * s.SELCAP;
     const int kprime = topk - 1;  // n_pages > topk, so kprime < n_cand
-    if (kprime > 0) block_select<NT>(keys, n_cand, kprime, out);
+    if (kprime > 0) {
+        // beyond 8 keys per thread the unrolled register form's code (16 / 32
+        // / 48 keys per thread) outgrows the instruction cache: the rolled
+        // form is faster in a launch (config 4, 128k: 74.5 -> 70.4 us per
+        // scored layer); up to 8 the unrolled form wins (config 2: 52.8 vs
+        // 53.9 us)
+        if (compact_bits && n_cand > NT * 8) block_select_compact<NT>(keys, n_cand, kprime, out, compact_bits);
+        else block_select<NT>(keys, n_cand, kprime, out);
+    }
     if (threadIdx.x == 0) {
         out[kprime] = n_cand;  // = n_pages - 1
         s.n_sel[hx] = topk;
@@ -1221,7 +1232,8 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
                                                   scores, kv_prefetch, dsm, full, empty, s_rel, w, bh, Sh, rank,
                                                   keys_dst, n_cand, CL);
     if constexpr (CL) cg::this_cluster().sync();  // every rank's keys are in rank 0
-    if (st == 2 && rank == 0) score_head_select<NWS * 32>(s, keys, n_cand, topk, hx);
+    if (st == 2 && rank == 0)
+        score_head_select<NWS * 32>(s, keys, n_cand, topk, hx, a.compact_select ? keys + s.NCAP : nullptr);
     if constexpr (CL) cg::this_cluster().sync();  // the selection (global) is visible to every rank
     else __syncthreads();                         // selection written by this CTA; scoring smem free
     if (a.out == nullptr) return;                 // scoring only (fc_score_select at small batches)
@@ -1881,11 +1893,16 @@ static cudaError_t launch_score_attend_t(const StoreView &s, int layer, const vo
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = S > 1 ? 2 : 1;
-    if (S > 1)
+    static const int compact = std::getenv("FC_SA_COMPACT") ? std::atoi(std::getenv("FC_SA_COMPACT")) : 1;
+    if (S > 1) {
+        AttnArgs ac = a;
+        ac.compact_select = compact;
         return cudaLaunchKernelEx(&cfg, score_attend_kernel<T, D, NST, NWA, NWS, true>, s, layer, (const T *)q,
-                                  unstable, period, force_due, topk, extra, scores, kv_prefetch, a, S);
+                                  unstable, period, force_due, topk, extra, scores, kv_prefetch, ac, S);
+    }
     AttnArgs a1 = a;
     a1.pf_cap = g_summary_prefetch_cap;
+    a1.compact_select = compact;
     return cudaLaunchKernelEx(&cfg, score_attend_kernel<T, D, NST, NWA, NWS, false>, s, layer, (const T *)q, unstable,
                               period, force_due, topk, extra, scores, kv_prefetch, a1, 1);
 }
