@@ -51,30 +51,25 @@ FC_DEVINL bool sorted_contains(const int32_t *a, int n, int x) {
     return lo < n && a[lo] == x;
 }
 
-__global__ void __launch_bounds__(kRecycleWarps * 32)
-rerank_diff_kernel(StoreView s, int layer, const int32_t *__restrict__ old_sel,
-                   const int32_t *__restrict__ n_old_arr, const uint8_t *__restrict__ unstable,
-                   int period, int force_due, int old_has_tail, int extra_tokens,
-                   const uint8_t *__restrict__ slow_resident, const uint8_t *__restrict__ row_skip,
-                   int32_t *copies, int max_copies, int32_t *n_copies, RerankWs ws, int batch) {
-    // per warp: old list | new list | old blocks | evicted | evicted blocks |
-    // promoted, sel_cap + slack entries each
-    // (both selections are staged in shared memory first: the membership
-    // tests are binary searches, which through global memory would chain
-    // ~8 dependent loads per entry)
-    extern __shared__ int32_t dsm_r[];
-    griddep_launch_dependents();
-    griddep_wait();  // the selection comes from the scoring launch before
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// The diff of one head by one warp (every lane calls it).  w_smem: the
+// warp's old list | new list | old blocks | evicted | evicted blocks |
+// promoted, sel_cap + slack entries each (both selections are staged in
+// shared memory first: the membership tests are binary searches, which
+// through global memory would chain ~8 dependent loads per entry).
+FC_DEVINL void rerank_diff_head(const StoreView &s, int layer, const int32_t *__restrict__ old_sel,
+                                const int32_t *__restrict__ n_old_arr, const uint8_t *__restrict__ unstable,
+                                int period, int force_due, int old_has_tail, int extra_tokens,
+                                const uint8_t *__restrict__ slow_resident, const uint8_t *__restrict__ row_skip,
+                                int32_t *copies, int max_copies, int32_t *n_copies, RerankWs ws, int bh,
+                                int32_t *w_smem) {
+    const int lane = threadIdx.x & 31;
     const int cap = s.SELCAP + kRecycleSlack;  // old list incl. pages appended since (old_has_tail)
-    int32_t *s_old = dsm_r + (int64_t)w * 6 * cap;
+    int32_t *s_old = w_smem;
     int32_t *s_new = s_old + cap;
     int32_t *s_oblk = s_new + cap;   // block of old entry i
     int32_t *s_evw = s_oblk + cap;   // evicted pages, ascending
     int32_t *s_evblk = s_evw + cap;  // their blocks
     int32_t *s_prw = s_evblk + cap;  // promoted pages, ascending
-    const int bh = blockIdx.x * kRecycleWarps + w;
-    if (bh >= batch * s.H) return;
     const int b = bh / s.H, h = bh % s.H;
     int32_t *cnt = ws.cnt(bh);
     // rows in row_skip still hold every page (post-prefill offload in flight):
@@ -208,15 +203,29 @@ rerank_diff_kernel(StoreView s, int layer, const int32_t *__restrict__ old_sel,
     if (lane == 0) { cnt[0] = n_ev - m; cnt[1] = n_pr - m; cnt[2] = m; }
 }
 
-// one CTA: pushes of all heads (head order) then pops (head order)
-__global__ void __launch_bounds__(1024)
-rerank_commit_kernel(StoreView s, int layer, int32_t *copies, int max_copies, int32_t *n_copies,
-                     RerankWs ws, int batch) {
+__global__ void __launch_bounds__(kRecycleWarps * 32)
+rerank_diff_kernel(StoreView s, int layer, const int32_t *__restrict__ old_sel,
+                   const int32_t *__restrict__ n_old_arr, const uint8_t *__restrict__ unstable,
+                   int period, int force_due, int old_has_tail, int extra_tokens,
+                   const uint8_t *__restrict__ slow_resident, const uint8_t *__restrict__ row_skip,
+                   int32_t *copies, int max_copies, int32_t *n_copies, RerankWs ws, int batch) {
+    extern __shared__ int32_t dsm_r[];
+    griddep_launch_dependents();
+    griddep_wait();  // the selection comes from the scoring launch before
+    const int w = threadIdx.x >> 5;
+    const int bh = blockIdx.x * kRecycleWarps + w;
+    if (bh >= batch * s.H) return;
+    rerank_diff_head(s, layer, old_sel, n_old_arr, unstable, period, force_due, old_has_tail, extra_tokens,
+                     slow_resident, row_skip, copies, max_copies, n_copies, ws, bh,
+                     dsm_r + (int64_t)w * 6 * (s.SELCAP + kRecycleSlack));
+}
+
+// pushes of all heads (head order) then pops (head order); 1024 threads
+FC_DEVINL void rerank_commit_body(const StoreView &s, int layer, int32_t *copies, int max_copies,
+                                  int32_t *n_copies, RerankWs ws, int batch) {
     using Scan = cub::BlockScan<int, 1024>;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ int s_fail;
-    griddep_launch_dependents();
-    griddep_wait();
     const int nh = batch * s.H;
     const int top0 = *s.free_top;
     // pass 0: can the pool cover every deficit (after the surplus pushes)?
@@ -288,6 +297,35 @@ rerank_commit_kernel(StoreView s, int layer, int32_t *copies, int max_copies, in
     }
     __syncthreads();
     if (threadIdx.x == 0) *s.free_top = top1 - acarry;
+}
+
+__global__ void __launch_bounds__(1024)
+rerank_commit_kernel(StoreView s, int layer, int32_t *copies, int max_copies, int32_t *n_copies,
+                     RerankWs ws, int batch) {
+    griddep_launch_dependents();
+    griddep_wait();
+    rerank_commit_body(s, layer, copies, max_copies, n_copies, ws, batch);
+}
+
+// Few heads (<= 32, e.g. one request): the diffs (warp w: head w) and the
+// commit in ONE CTA — one launch and one dependency hand-off per layer
+// instead of two.  Same results as the two kernels.
+__global__ void __launch_bounds__(1024)
+rerank_small_kernel(StoreView s, int layer, const int32_t *__restrict__ old_sel,
+                    const int32_t *__restrict__ n_old_arr, const uint8_t *__restrict__ unstable,
+                    int period, int force_due, int old_has_tail, int extra_tokens,
+                    const uint8_t *__restrict__ slow_resident, const uint8_t *__restrict__ row_skip,
+                    int32_t *copies, int max_copies, int32_t *n_copies, RerankWs ws, int batch) {
+    extern __shared__ int32_t dsm_r[];
+    griddep_launch_dependents();
+    griddep_wait();  // the selection comes from the scoring launch before
+    const int w = threadIdx.x >> 5;
+    if (w < batch * s.H)
+        rerank_diff_head(s, layer, old_sel, n_old_arr, unstable, period, force_due, old_has_tail, extra_tokens,
+                         slow_resident, row_skip, copies, max_copies, n_copies, ws, w,
+                         dsm_r + (int64_t)w * 6 * (s.SELCAP + kRecycleSlack));
+    __syncthreads();  // every head's diff (global workspace, table) before the commit
+    rerank_commit_body(s, layer, copies, max_copies, n_copies, ws, batch);
 }
 
 // ---------------------------------------------------------------------------
@@ -502,6 +540,19 @@ cudaError_t launch_rerank(const StoreView &s, int layer, const int32_t *old_sel,
                           cudaStream_t st) {
     RerankWs ws{reinterpret_cast<int32_t *>(workspace)};
     const int heads = batch * s.H;
+    const size_t smem1 = (size_t)heads * 6 * (s.SELCAP + kRecycleSlack) * sizeof(int32_t);
+    if (heads <= 32 && smem1 <= 200 * 1024) {
+        static size_t configured1 = 0;
+        if (smem1 > 48 * 1024 && configured1 < smem1) {
+            cudaError_t e = cudaFuncSetAttribute(rerank_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem1);
+            if (e != cudaSuccess) return e;
+            configured1 = smem1;
+        }
+        return launch_pdl(rerank_small_kernel, dim3(1), dim3(1024), smem1, st, s, layer, old_sel, n_old, unstable,
+                          period, force_due, old_has_tail, extra_tokens, slow_resident, row_skip, copies, max_copies,
+                          n_copies, ws, batch);
+    }
     const size_t smem = (size_t)kRecycleWarps * 6 * (s.SELCAP + kRecycleSlack) * sizeof(int32_t);
     static size_t configured = 0;
     if (smem > 48 * 1024 && configured < smem) {
