@@ -764,11 +764,16 @@ class DecodeEngine:
             return self.score_all_heads or not self._layer_skippable(l, kind)
 
         n, layer = 1, 0  # the step advance
+
+        def recycle_kernels(heads):  # diff + commit, or one CTA for <= 32 heads (recycle.cu)
+            return 1 if heads <= 32 and heads * 6 * (st.SELCAP + 64) * 4 <= 200 * 1024 else 2
+
         if deferred:
-            n += 2  # one recycle of every layer; one fetch on the fetch stream
+            # one recycle of every layer; one fetch per held row on the fetch stream
+            n += recycle_kernels(self.B * self.L * self.H) + 1
         while layer < self.L:
             if recycles(layer):
-                n += 2  # recycle + fetch (on the fetch stream with reload pauses)
+                n += recycle_kernels(self.B * self.H) + 1  # recycle + fetch
             if scores(layer) and not recycles(layer) and (
                     use_fused or (not self.score_all_heads and self._use_balanced(layer, kind, False))):
                 n += 1
