@@ -395,9 +395,8 @@ class DecodeEngine:
         main = torch.cuda.current_stream(dev)
         if self.fetch_stream is None:
             # the fetch kernel is a handful of CTAs that mostly wait on the host
-            # link: at the default priority its CTAs queued behind the decode
-            # launches (which hold every SM back to back) and a held row waited
-            # for several steps; at high priority they take the next free SMs
+            # link; at high priority they take the next free SMs rather than
+            # queueing behind the back-to-back decode launches
             self.fetch_stream = torch.cuda.Stream(dev, priority=-5)
         busy = []
         for ev, snap in self._snap_busy:
