@@ -1321,6 +1321,9 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
 // the same attention as fc_sparse_decode (attend_head_cta).
 // Requires every CTA co-resident (the owners wait on the others): the
 // launcher checks the occupancy.  bf16 only (8 warps score and attend).
+#ifndef FC_BAL_BULK_SCORES
+#define FC_BAL_BULK_SCORES 1
+#endif
 #ifndef FC_BAL_ROUNDS
 #define FC_BAL_ROUNDS 32
 #endif
@@ -1339,6 +1342,7 @@ score_attend_bal_kernel(StoreView s, int layer, const T *__restrict__ q, const u
     __shared__ __align__(8) uint64_t abars[NW * NST];
     __shared__ float s_wm[NW][16], s_wl[NW][16];
     __shared__ __align__(8) uint64_t stage_bar;
+    __shared__ __align__(8) uint64_t keys_bar;
     griddep_launch_dependents();
     unsigned long long *satr = g_sa_trace;
     if (satr && threadIdx.x == 0) satr[blockIdx.x * 8] = gtimer_s();
@@ -1518,6 +1522,25 @@ score_attend_bal_kernel(StoreView s, int layer, const T *__restrict__ q, const u
                 counters[bh] = 0;  // self-resetting for the next launch
                 row[n_pages - 1] = -INFINITY;  // pinned page: not scored
             }
+#if FC_BAL_BULK_SCORES
+            // the score row in ONE bulk copy into shared memory (one request
+            // under the launch's full HBM load instead of 2047 loads), then
+            // converted to keys
+            float *raw = reinterpret_cast<float *>(keys + ((2 * s.NCAP + 3) & ~3));  // 16-byte aligned, past the keys
+            const uintptr_t src0 = reinterpret_cast<uintptr_t>(row) & ~uintptr_t(15);
+            const int off = (int)((reinterpret_cast<uintptr_t>(row) - src0) / 4);
+            if (tid == 0) {
+                mbar_init(&keys_bar, 1);
+                fence_mbar_init();
+                asm volatile("fence.proxy.async.global;" ::: "memory");  // the scores are generic-proxy writes
+                const uint32_t nb = (uint32_t)(((off + n_cand) * 4 + 15) & ~15);
+                mbar_arrive_expect_tx(&keys_bar, nb);
+                bulk_g2s(raw, reinterpret_cast<const void *>(src0), nb, &keys_bar);
+            }
+            __syncthreads();
+            mbar_wait(&keys_bar, 0);
+            for (int i = tid; i < n_cand; i += blockDim.x) keys[i] = score_key(raw[off + i]);
+#else
             __syncthreads();
             for (int i0 = tid; i0 < n_cand; i0 += blockDim.x * 8) {
                 float v[8];
@@ -1532,6 +1555,7 @@ score_attend_bal_kernel(StoreView s, int layer, const T *__restrict__ q, const u
                     if (i < n_cand) keys[i] = score_key(v[u]);
                 }
             }
+#endif
             __syncthreads();
             const int kprime = topk - 1;  // n_pages > topk, so kprime < n_cand
             if (satr && tid == 0) satr[blockIdx.x * 8 + 1] = gtimer_s();  // (owner: keys in smem)
@@ -1591,8 +1615,9 @@ template <typename T, int D, int NST, int NW>
 static int score_attend_bal_grid_t(const StoreView &s, int batch) {
     const int n_heads = batch * s.H;
     // (the ring holds the owner's keys and its selection during the select)
-    if (n_heads < 1 || (size_t)(s.NCAP + s.SELCAP + 2 * (s.NCAP / 32 + 1)) * 4 >
-                          (size_t)NW * NST * AttnGeom<T, D>::kPageBytes) return 0;
+    // (the ring holds the owner's keys, the select's scratch and the score row's bulk copy)
+    const size_t need = (size_t)max(3 * s.NCAP + 12, s.NCAP + s.SELCAP + 2 * (s.NCAP / 32 + 1)) * 4;
+    if (n_heads < 1 || need > (size_t)NW * NST * AttnGeom<T, D>::kPageBytes) return 0;
     if (s.NCAP > kScoreThreads * kSelMaxKpt) return 0;
     auto k = score_attend_bal_kernel<T, D, NST, NW>;
     const size_t smem = score_attend_bal_smem<T, D, NST, NW>(n_heads);
