@@ -224,6 +224,22 @@ def reference_cpu(cfg, *, steps, warmup, units_per_step=None):
     return tps, step_s, info
 
 
+def _config(cfg, world, args):
+    """The bench line's `config` (both arms print the same one)."""
+    return {"workload": cfg["workload"], "batch_per_gpu": cfg["batch"], "ctx": cfg["ctx"], "layers": cfg["layers"],
+            "kv_heads": cfg["kv_heads"], "q_heads": cfg["kv_heads"] * cfg["group"], "head_dim": cfg["head_dim"],
+            "page": 16, "topk_pages": cfg["topk"], "rerank_period": cfg["period"],
+            "unstable_fraction": cfg["unstable_fraction"], "parallelism": f"request-parallel x{world}",
+            "l2": "inputs larger than L2 (5+ GiB touched per step vs 126 MB L2)",
+            "unstable_heads": ("spread: the first round(u*H) KV heads of every layer"
+                               if os.environ.get("FC_PROFILE") == "spread" else
+                               "first round(u*L*H) flat heads (the reference fixture, conftest.py:21-33)"),
+            **({"mixed_clusters": False} if os.environ.get("FC_MIXED") == "0" else {}),
+            **({"fused_score_attend": False} if os.environ.get("FC_FUSED") == "0" else {}),
+            **({"share": cfg["share"]} if "share" in cfg else {}),
+            "phases": args.phases}
+
+
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -233,7 +249,7 @@ def run_reference(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic N(0,1) KV/queries (bf16-rounded), seed 12345",
-            "config": {"workload": cfg["workload"]}, "impl": "reference",
+            "config": _config(cfg, max(1, int(os.environ.get("WORLD_SIZE", "1"))), args), "impl": "reference",
             "cpu_baseline": info,
             "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -544,18 +560,7 @@ def run_ours(args, cfg):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic: N(0,1) bf16 KV (4 random [H,T,d] sources rotated over request x layer), "
                 "N(0,1) q inputs per step (4 sets cycled), a distinct N(0,1) k/v token appended every step",
-        "config": {"workload": cfg["workload"], "batch_per_gpu": B, "ctx": T, "layers": L,
-                   "kv_heads": H, "q_heads": H * G, "head_dim": D, "page": 16, "topk_pages": K,
-                   "rerank_period": R, "unstable_fraction": cfg["unstable_fraction"],
-                   "parallelism": f"request-parallel x{world}",
-                   "l2": "inputs larger than L2 (5+ GiB touched per step vs 126 MB L2)",
-                   "unstable_heads": ("spread: the first round(u*H) KV heads of every layer"
-                                      if os.environ.get("FC_PROFILE") == "spread" else
-                                      "first round(u*L*H) flat heads (the reference fixture, conftest.py:21-33)"),
-                   **({"mixed_clusters": False} if os.environ.get("FC_MIXED") == "0" else {}),
-                   **({"fused_score_attend": False} if os.environ.get("FC_FUSED") == "0" else {}),
-                   **({"share": cfg["share"]} if "share" in cfg else {}),
-                   "phases": args.phases},
+        "config": _config(cfg, world, args),
         "gpu_launches": launches,
         "scoring_counters": counters,
         "step_ms": step_stats,
