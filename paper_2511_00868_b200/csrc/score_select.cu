@@ -71,7 +71,17 @@ struct SelScratch {
     int s_rem, s_ncand, s_done;
     uint32_t cand_key[32];
     int cand_idx[32];
+    int s_wsum[NT / 32];
 };
+
+// One selection scratch per kernel, shared by both selection forms (the
+// compact one must not add its own static shared memory: the fused kernels'
+// occupancy is set by their shared-memory footprint).
+template <int NT>
+__device__ __forceinline__ SelScratch<NT> &sel_scratch() {
+    __shared__ SelScratch<NT> sc;
+    return sc;
+}
 
 template <int NT, int KPT>
 __device__ void block_select_kpt(const uint32_t *keys, int n, int kprime, int32_t *out, SelScratch<NT> &sc) {
@@ -301,7 +311,7 @@ constexpr int kSelMaxKpt = 48;
 template <int NT>
 __device__ void block_select(const uint32_t *keys, int n, int kprime, int32_t *out) {
     static_assert(kSelMaxKpt == kSelMaxKptAll, "one scratch size");
-    __shared__ SelScratch<NT> sc;
+    SelScratch<NT> &sc = sel_scratch<NT>();
     if (n <= NT * 8) block_select_kpt<NT, 8>(keys, n, kprime, out, sc);
     else if (n <= NT * 32) block_select_kpt<NT, 32>(keys, n, kprime, out, sc);
     else block_select_kpt<NT, kSelMaxKpt>(keys, n, kprime, out, sc);
@@ -314,15 +324,16 @@ __device__ void block_select(const uint32_t *keys, int n, int kprime, int32_t *o
 // Same result: the kprime largest keys, ties to the lowest index, emitted in
 // ascending index order (np.lexsort((arange, -scores))).  The crossing bin
 // of the value-linear histogram is ranked exactly when it holds <= 32 keys;
-// otherwise (ties / skew) the unrolled block_select runs.
+// otherwise (ties / skew) it returns false and the caller runs the unrolled
+// block_select (one call site per kernel: a second inlined copy of the
+// unrolled form doubles the kernel's code).
 template <int NT>
-__device__ void block_select_compact(const uint32_t *keys, int n, int kprime, int32_t *out,
-                                     uint32_t *bits /* [2 * ceil(n/32)] shared */) {
-    __shared__ int hist[kSelBins];
-    __shared__ uint32_t s_kmin, s_kmax, s_T;
-    __shared__ int s_digit, s_above, s_ncand, s_ok, s_rem, s_wsum[NT / 32];
-    __shared__ uint32_t cand_key[32];
-    __shared__ int cand_idx[32];
+__device__ bool block_select_compact(const uint32_t *keys, int n, int kprime, int32_t *out) {
+    SelScratch<NT> &sc = sel_scratch<NT>();
+    int *hist = sc.hist, *s_wsum = sc.s_wsum, *cand_idx = sc.cand_idx;
+    uint32_t *cand_key = sc.cand_key;
+    uint32_t &s_kmin = sc.s_kmin, &s_kmax = sc.s_kmax, &s_T = sc.s_T;
+    int &s_digit = sc.s_digit, &s_above = sc.s_above, &s_ncand = sc.s_ncand, &s_rem = sc.s_rem;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     uint32_t lo = 0xffffffffu, hi = 0u;
 #pragma unroll 1
@@ -331,7 +342,7 @@ __device__ void block_select_compact(const uint32_t *keys, int n, int kprime, in
     hi = __reduce_max_sync(0xffffffffu, hi);
 #pragma unroll 1
     for (int i = tid; i < kSelBins; i += NT) hist[i] = 0;
-    if (tid == 0) { s_kmin = 0xffffffffu; s_kmax = 0u; s_ncand = 0; s_ok = 0; }
+    if (tid == 0) { s_kmin = 0xffffffffu; s_kmax = 0u; s_ncand = 0; }
     __syncthreads();
     if (lane == 0) { atomicMin(&s_kmin, lo); atomicMax(&s_kmax, hi); }
     __syncthreads();
@@ -366,10 +377,9 @@ __device__ void block_select_compact(const uint32_t *keys, int n, int kprime, in
     }
     __syncthreads();
     const int B = s_digit;
-    if (hist[B] > 32) {  // (ties / skew: the general path)
+    if (hist[B] > 32) {  // (ties / skew: the caller runs the general path)
         __syncthreads();
-        block_select<NT>(keys, n, kprime, out);
-        return;
+        return false;
     }
 #pragma unroll 1
     for (int i = tid; i < n; i += NT)
@@ -397,8 +407,8 @@ __device__ void block_select_compact(const uint32_t *keys, int n, int kprime, in
     const uint32_t T = s_T;
     const int rem = s_rem;
     // bit-words of keys > T and == T, 32 indices per word, one warp per word
-    const int nw = (n + 31) / 32;
-    uint32_t *gtb = bits, *eqb = bits + nw;
+    const int nw = (n + 31) / 32;  // <= NT * kSelMaxKpt / 32 (n_cand's bound)
+    uint32_t *gtb = sc.gt_bits, *eqb = sc.eq_bits;
 #pragma unroll 1
     for (int w = wid; w < nw; w += NT / 32) {
         const int i = w * 32 + lane;
@@ -451,6 +461,7 @@ __device__ void block_select_compact(const uint32_t *keys, int n, int kprime, in
         while (selw) { out[pos++] = wd * 32 + (__ffs(selw) - 1); selw &= selw - 1; }
     }
     __syncthreads();
+    return true;
 }
 
 
@@ -842,12 +853,10 @@ struct HeadScoreGeom {
 // attention ring / merge scratch)
 template <typename T, int D, int NST, int NWA>
 __host__ __device__ constexpr size_t score_attend_ring_bytes(int ncap) {
-    // (keys [ncap] then the compact select's bit words [2 * (ncap/32 + 1)])
-    return (size_t)HeadScoreGeom<T, D>::kStages * HeadScoreGeom<T, D>::kChunkBytes + (size_t)ncap * 4 +
-                       (size_t)(ncap / 32 + 1) * 8 >
+    return (size_t)HeadScoreGeom<T, D>::kStages * HeadScoreGeom<T, D>::kChunkBytes + (size_t)ncap * 4 >
                    (size_t)NWA * NST * AttnGeom<T, D>::kPageBytes
-               ? (((size_t)HeadScoreGeom<T, D>::kStages * HeadScoreGeom<T, D>::kChunkBytes + (size_t)ncap * 4 +
-                   (size_t)(ncap / 32 + 1) * 8 + 127) & ~(size_t)127)
+               ? (((size_t)HeadScoreGeom<T, D>::kStages * HeadScoreGeom<T, D>::kChunkBytes + (size_t)ncap * 4 + 127) &
+                  ~(size_t)127)
                : (size_t)NWA * NST * AttnGeom<T, D>::kPageBytes;
 }
 
@@ -1021,7 +1030,7 @@ __device__ int score_head_stream(const StoreView &s, int layer, const T *__restr
 // selecting CTA calls it.
 template <int NT>
 __device__ void score_head_select(const StoreView &s, const uint32_t *keys, int n_cand, int topk, int hx,
-                                  uint32_t *compact_bits = nullptr) {
+                                  bool compact = false) {
     int32_t *out = s.sel + (int64_t)hx * s.SELCAP;
     const int kprime = topk - 1;  // n_pages > topk, so kprime < n_cand
     if (kprime > 0) {
@@ -1030,8 +1039,8 @@ __device__ void score_head_select(const StoreView &s, const uint32_t *keys, int 
         // form is faster in a launch (config 4, 128k: 74.5 -> 70.4 us per
         // scored layer); up to 8 the unrolled form wins (config 2: 52.8 vs
         // 53.9 us)
-        if (compact_bits && n_cand > NT * 8) block_select_compact<NT>(keys, n_cand, kprime, out, compact_bits);
-        else block_select<NT>(keys, n_cand, kprime, out);
+        if (!(compact && n_cand > NT * 8 && block_select_compact<NT>(keys, n_cand, kprime, out)))
+            block_select<NT>(keys, n_cand, kprime, out);
     }
     if (threadIdx.x == 0) {
         out[kprime] = n_cand;  // = n_pages - 1
@@ -1233,7 +1242,7 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
                                                   keys_dst, n_cand, CL);
     if constexpr (CL) cg::this_cluster().sync();  // every rank's keys are in rank 0
     if (st == 2 && rank == 0)
-        score_head_select<NWS * 32>(s, keys, n_cand, topk, hx, a.compact_select ? keys + s.NCAP : nullptr);
+        score_head_select<NWS * 32>(s, keys, n_cand, topk, hx, a.compact_select != 0);
     if constexpr (CL) cg::this_cluster().sync();  // the selection (global) is visible to every rank
     else __syncthreads();                         // selection written by this CTA; scoring smem free
     if (a.out == nullptr) return;                 // scoring only (fc_score_select at small batches)
@@ -1562,9 +1571,9 @@ score_attend_bal_kernel(StoreView s, int layer, const T *__restrict__ q, const u
             // the selection is emitted into shared memory (the ring past the
             // keys) and copied out coalesced
             int32_t *sel_s = reinterpret_cast<int32_t *>(keys + s.NCAP);
-            uint32_t *bits = reinterpret_cast<uint32_t *>(sel_s + s.SELCAP);
 #ifndef FC_BAL_UNROLLED_SELECT
-            if (kprime > 0) block_select_compact<kScoreThreads>(keys, n_cand, kprime, sel_s, bits);
+            if (kprime > 0 && !block_select_compact<kScoreThreads>(keys, n_cand, kprime, sel_s))
+                block_select<kScoreThreads>(keys, n_cand, kprime, sel_s);
 #else
             if (kprime > 0) block_select<kScoreThreads>(keys, n_cand, kprime, sel_s);
 #endif
@@ -1616,7 +1625,7 @@ static int score_attend_bal_grid_t(const StoreView &s, int batch) {
     const int n_heads = batch * s.H;
     // (the ring holds the owner's keys and its selection during the select)
     // (the ring holds the owner's keys, the select's scratch and the score row's bulk copy)
-    const size_t need = (size_t)max(3 * s.NCAP + 12, s.NCAP + s.SELCAP + 2 * (s.NCAP / 32 + 1)) * 4;
+    const size_t need = (size_t)max(3 * s.NCAP + 12, s.NCAP + s.SELCAP) * 4;
     if (n_heads < 1 || need > (size_t)NW * NST * AttnGeom<T, D>::kPageBytes) return 0;
     if (s.NCAP > kScoreThreads * kSelMaxKpt) return 0;
     auto k = score_attend_bal_kernel<T, D, NST, NW>;
