@@ -138,6 +138,7 @@ def load():
 
 def check(rc: int, what: str) -> None:
     """Map a C-ABI status to the reference's exception types."""
+    capture_probe(what)
     if rc == FC_OK:
         return
     msg = load().fc_last_error().decode(errors="replace")
@@ -148,3 +149,21 @@ def check(rc: int, what: str) -> None:
     if rc == FC_E_CAPACITY:
         raise ValueError(f"{what}: capacity/workspace too small")
     raise CudaError(f"{what}: {msg}")
+
+
+_cudart = None
+
+
+def capture_probe(what: str) -> None:
+    """Debug aid (FC_CAPTURE_CHECK=1): raise naming ``what`` if the current
+    stream's graph capture has been invalidated by an earlier operation."""
+    if not os.environ.get("FC_CAPTURE_CHECK"):
+        return
+    global _cudart
+    import torch
+    if _cudart is None:
+        _cudart = ctypes.CDLL("libcudart.so.12")
+    status = ctypes.c_int(0)
+    _cudart.cudaStreamIsCapturing(ctypes.c_void_p(torch.cuda.current_stream().cuda_stream), ctypes.byref(status))
+    if status.value == 2:  # cudaStreamCaptureStatusInvalidated
+        raise RuntimeError(f"graph capture invalidated at or before: {what}")

@@ -23,6 +23,7 @@ plain steps) so the <= 2·L+1 launches cost no host time.
 
 from __future__ import annotations
 
+import gc
 import math
 
 import torch
@@ -33,6 +34,7 @@ from .stability import HeadProfile
 from ._lib import FC_HOLD_NONE as HOLD_NONE, FC_HOLD_RERANK as HOLD_RERANK
 from ._lib import FC_HOLD_RESUME as HOLD_RESUME, FC_HOLD_WAIT as HOLD_WAIT
 from .store import PAGE_SIZE, KVStore
+from . import _lib
 
 
 class DecodeEngine:
@@ -460,7 +462,9 @@ class DecodeEngine:
             self.n_old.copy_(st.n_sel.transpose(0, 1))
             self.n_copies.zero_()
         layer = 0
+        _lib.capture_probe(f"{kind} step prologue")
         while layer < self.L:
+            _lib.capture_probe(f"{kind} step, before layer {layer}")
             recycle = recycles(layer)
             scored = scores(layer)
             if scored and not recycle and self._use_balanced(layer, kind, force_due):
@@ -733,9 +737,20 @@ class DecodeEngine:
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(s):
-            with torch.cuda.graph(g, stream=s):
-                self._launch_step(kind, force_due=self.score_all_heads, fetch=fetch)
+        # No garbage collection inside the capture: an unreachable engine of
+        # an earlier request / test still holding its step graphs would have
+        # them destroyed mid-capture (cudaGraphExecDestroy is not permitted
+        # while a stream captures), which invalidates this capture.
+        gc.collect()
+        gc_was_enabled = gc.isenabled()
+        gc.disable()
+        try:
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    self._launch_step(kind, force_due=self.score_all_heads, fetch=fetch)
+        finally:
+            if gc_was_enabled:
+                gc.enable()
         torch.cuda.current_stream(self.device).wait_stream(s)
         torch.cuda.synchronize(self.device)
         self._graphs[(kind, self.score_all_heads, fetch, self.store.per_row)] = g
