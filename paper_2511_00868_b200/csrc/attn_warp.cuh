@@ -663,6 +663,7 @@ FC_DEVINL int attend_head_cta(const StoreView &s, const AttnArgs &a, int bh, cha
     }
     st.finalize();
     named_bar_sync(bar_id, NT);  // every warp done with its ring: merge scratch
+    if (tid < NW * NST) mbar_inval(&bars[tid]);  // (the next call initialises them again)
     float *scratch = reinterpret_cast<float *>(ring);  // [NW][G][D]
     for (int g = lane; g < 16; g += 32) { s_wm[w][g] = -INFINITY; s_wl[w][g] = 0.f; }
     __syncwarp();

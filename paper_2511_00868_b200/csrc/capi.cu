@@ -5,6 +5,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "launchers.cuh"
@@ -220,6 +221,21 @@ int fc_score_attend(const fc_store *s, int layer, const void *q, const uint8_t *
                                            scores_out, batch, kv_prefetch ? 1 : 0, a, (cudaStream_t)stream));
 }
 
+// balanced launch workspace: per head ready / claim / done / spare words,
+// then the launch epoch and exit count, 16-byte aligned; then the chunk states
+static size_t bal_flags_bytes(size_t nh) { return ((nh * 4 + 4) * sizeof(int32_t) + 15) & ~size_t(15); }
+
+// chunks per scored head in the balanced launch (FC_BAL_CHUNKS, 2..kBalMaxSplit)
+static int bal_chunks() {
+    static int nc = 0;
+    if (nc == 0) {
+        const char *e = std::getenv("FC_BAL_CHUNKS");
+        nc = e ? std::atoi(e) : kBalMaxSplit;
+        nc = nc < 2 ? 2 : (nc > kBalMaxSplit ? kBalMaxSplit : nc);
+    }
+    return nc;
+}
+
 int fc_score_attend_balanced_supported(const fc_store *s, int batch) {
     if (check_store(s) != FC_OK || s->pages_cap > kMaxPagesCap || batch < 1 || batch > s->batch_cap) return 0;
     return score_attend_balanced_grid(make_view(s), s->dtype, batch);
@@ -228,7 +244,7 @@ int fc_score_attend_balanced_supported(const fc_store *s, int batch) {
 size_t fc_score_attend_balanced_workspace_size(const fc_store *s, int batch) {
     if (check_store(s) != FC_OK || batch < 1 || batch > s->batch_cap) return 0;
     const size_t nh = (size_t)batch * s->kv_heads;
-    return nh * 2 * sizeof(int32_t) + nh * kBalMaxSplit * ((size_t)s->group * s->head_dim + 32) * sizeof(float);
+    return bal_flags_bytes(nh) + nh * kBalMaxSplit * ((size_t)s->group * s->head_dim + 32) * sizeof(float);
 }
 
 int fc_score_attend_balanced(const fc_store *s, int layer, const void *q, const uint8_t *unstable, int period,
@@ -269,10 +285,13 @@ int fc_score_attend_balanced_ws(const fc_store *s, int layer, const void *q, con
     a.layer = layer; a.q = q; a.k_new = k_new; a.v_new = v_new; a.out = out; a.lse = lse;
     a.scale_log2 = scale * 1.4426950408889634f;
     a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.max_splits = 1;
-    if (helper_ws) {
+    if (helper_ws) {  // chunked attention of the scored heads (zero-initialised workspace)
         a.bal_flags = reinterpret_cast<int32_t *>(helper_ws);
         a.bal_state = reinterpret_cast<float *>(reinterpret_cast<char *>(helper_ws) +
-                                                (size_t)batch * s->kv_heads * 2 * sizeof(int32_t));
+                                                bal_flags_bytes((size_t)batch * s->kv_heads));
+        a.max_splits = bal_chunks();
+        static const bool nowait = std::getenv("FC_BAL_NOWAIT") != nullptr;  // (profiling knob)
+        a.bal_wait = nowait ? 0 : 1;
     }
     return cuda_status(launch_score_attend_balanced(v, s->dtype, layer, q, unstable, period, force_due, topk,
                                                     extra_tokens, scores_out, counters, batch, kv_prefetch ? 1 : 0,

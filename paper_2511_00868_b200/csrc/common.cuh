@@ -68,6 +68,12 @@ FC_DEVINL void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
 
+// An mbarrier is invalidated before its shared memory is initialised again
+// (a CTA that streams several heads re-initialises its ring's barriers).
+FC_DEVINL void mbar_inval(uint64_t *bar) {
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 FC_DEVINL void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }

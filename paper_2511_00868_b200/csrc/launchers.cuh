@@ -34,14 +34,16 @@ struct AttnArgs {
     // CTAs of that layer then stream them from L2) when those are at most
     // this many bytes; 0 = off (set by the launcher)
     int64_t pf_cap;
-    // fc_score_attend_balanced: the CTAs beyond one per head help the scored
-    // heads attend (null = off): per head a ready flag and a done counter
-    // [2][B_cap*H], and the partial states [B_cap*H][kBalMaxSplit][G*D + 32]
+    // fc_score_attend_balanced: the scored heads' attention cut into
+    // max_splits chunks claimed by any CTA with no work left (null = off):
+    // per head ready / claim / done / spare words [4][batch*H], the launch
+    // epoch and exit count, and the chunk states [batch*H][kBalMaxSplit][G*D + 32]
     int32_t *bal_flags;
     float *bal_state;
+    int bal_wait;         // balanced launch: CTAs with no work wait for selections still pending
     int compact_select;   // fc_score_attend: rolled-loop select (block_select_compact)
 };
-constexpr int kBalMaxSplit = 4;  // CTAs attending one scored head (owner + helpers)
+constexpr int kBalMaxSplit = 4;  // chunks of one scored head's attention (balanced launch)
 
 // persistent multi-layer attention (attn_run.cu)
 struct RunArgs {

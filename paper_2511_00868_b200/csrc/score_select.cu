@@ -1309,6 +1309,13 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
 }
 
 // ---------------------------------------------------------------------------
+// A load that is re-issued on every call (other CTAs of the launch update the word).
+FC_DEVINL int ld_relaxed_gpu(const int32_t *p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // Balanced fused score + select + attend (fc_score_attend_balanced).
 //
 // The head-aligned fused kernel gives each head ONE CTA for its scoring and
@@ -1469,46 +1476,104 @@ score_attend_bal_kernel(StoreView s, int layer, const T *__restrict__ q, const u
         }
     }
     if (satr && threadIdx.x == 0) satr[blockIdx.x * 8 + 4] = gtimer_s();
-    // Helpers: the CTAs beyond one per head split the scored heads' attention
-    // with their owners (kh per head, the head's attended pages cut into kh+1
-    // ranges); a helper waits for the owner's selection, attends its range
-    // and leaves its state in global memory for the owner to merge.  Every
-    // CTA derives the same assignment from the prefix of candidate counts.
-    const int n_extra = (int)gridDim.x - n_heads;
-    int n_sc = 0;
-    if (a.bal_flags != nullptr && n_extra > 0)
-        for (int x = 0; x < n_heads; ++x) n_sc += prefix[x + 1] > prefix[x];
-    const int kh = n_sc > 0 ? min(kBalMaxSplit - 1, n_extra / n_sc) : 0;
+    // Chunked attention of the scored heads (a.bal_flags != nullptr): the
+    // attended pages of a head with candidates are cut into NC chunks
+    // (attend_head_cta's rank r of NC).  Its owner claims chunks of it once
+    // its selection is out; every CTA with no work of its own left (the CTAs
+    // beyond one per head after scoring, unscored owners after their head,
+    // owners after their chunks) claims chunks of any scored head whose
+    // selection is out.  Chunk states go to global memory; the CTA finishing
+    // a head's last chunk merges them.  Per-head words: ready (= epoch + 1
+    // once the selection is out; the owner zeroes claim / done before), claim
+    // (next chunk; over-claims are harmless), done.  The epoch is constant
+    // within a launch and advanced by the last CTA to exit, so a word left by
+    // an earlier launch never reads as ready (the next launch reads it after
+    // griddepcontrol.wait, i.e. after this launch completed).
+    const bool steal = a.bal_flags != nullptr;
+    const int NC = steal ? a.max_splits : 1;
     const int GD = s.G * D + 32;
-    int32_t *ready = a.bal_flags, *done = a.bal_flags ? a.bal_flags + n_heads : nullptr;
-    if ((int)blockIdx.x >= n_heads) {
-        const int e = (int)blockIdx.x - n_heads;
-        if (kh == 0 || e >= n_sc * kh) return;
-        int hb = -1;  // the (e / kh)-th scored head
-        for (int x = 0, k = 0; x < n_heads; ++x)
-            if (prefix[x + 1] > prefix[x] && k++ == e / kh) { hb = x; break; }
-        const int rank = 1 + e % kh;
+    int32_t *ready = steal ? a.bal_flags : nullptr;
+    int32_t *claim = steal ? a.bal_flags + n_heads : nullptr;
+    int32_t *done = steal ? a.bal_flags + 2 * n_heads : nullptr;
+    int32_t *glob = steal ? a.bal_flags + 4 * n_heads : nullptr;  // [0] epoch, [1] CTAs exited
+    __shared__ int s_epoch, s_pick, s_pend, s_chunk, s_merge;
+    if (steal) {
+        if (tid == 0) s_epoch = ld_relaxed_gpu(glob);
+        __syncthreads();
+    }
+    const int epoch1 = steal ? s_epoch + 1 : 0;
+    // attend chunk c of scored head hb; the CTA finishing its last chunk merges
+    auto run_chunk = [&](int hb, int c) {
+        float *st0 = a.bal_state + (int64_t)hb * kBalMaxSplit * GD;
+        const int n_att = attend_head_cta<T, D, NST, NW>(s, a, hb, dsm, abars, s_wm, s_wl, nullptr, 1, NC, c,
+                                                         st0 + (int64_t)c * GD);
+        __syncthreads();  // every thread's state written
         if (tid == 0) {
-            int got;
-            while (true) {
-                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(got) : "l"(ready + hb) : "memory");
-                if (got) break;
-                __nanosleep(64);
-            }
-            if (satr) satr[blockIdx.x * 8 + 5] = gtimer_s();
+            int old;
+            asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(done + hb) : "memory");
+            s_merge = old == NC - 1;
         }
         __syncthreads();
-        attend_head_cta<T, D, NST, NW>(s, a, hb, dsm, abars, s_wm, s_wl, nullptr, 1, kh + 1, rank,
-                                       a.bal_state + ((int64_t)hb * kBalMaxSplit + rank) * GD);
+        if (s_merge && n_att > 0) merge_head_global<T, D>(s, a, hb, st0, NC, blockDim.x);
+        __syncthreads();  // s_merge read by every thread before it is rewritten
+    };
+    // claim chunks of any scored head until none is left or pending
+    auto help = [&]() {
+        const int off = (int)(((int64_t)blockIdx.x * n_heads) / gridDim.x);
+        while (true) {
+            if (tid == 0) { s_pick = INT_MAX; s_pend = 0; }
+            __syncthreads();
+            for (int x = tid; x < n_heads; x += blockDim.x) {
+                if (prefix[x + 1] <= prefix[x]) continue;
+                if (ld_relaxed_gpu(ready + x) != epoch1) s_pend = 1;
+                else if (ld_relaxed_gpu(claim + x) < NC) atomicMin(&s_pick, (x - off + n_heads) % n_heads);
+            }
+            __syncthreads();
+            const int pick = s_pick, pend = s_pend;
+            __syncthreads();  // read by every thread before tid 0 rewrites them
+            if (satr && tid == 0 && (int)blockIdx.x >= n_heads) {  // (profiling: the help loop's state)
+                satr[blockIdx.x * 8 + 5] += 1;
+                satr[blockIdx.x * 8 + 6] = pick;
+                satr[blockIdx.x * 8 + 1] = pend;
+            }
+            if (pick == INT_MAX) {
+                if (!pend || !a.bal_wait) break;
+                if (tid == 0) __nanosleep(200);
+                continue;
+            }
+            const int hb = (pick + off) % n_heads;
+            if (tid == 0) {
+                int r;
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(ready + hb) : "memory");
+                s_chunk = atomicAdd(claim + hb, 1);
+            }
+            __syncthreads();
+            const int c = s_chunk;
+            if (c < NC) run_chunk(hb, c);
+        }
+    };
+    // every CTA passes here once on its way out
+    auto leave = [&]() {
         __syncthreads();
-        if (satr && tid == 0) satr[blockIdx.x * 8 + 6] = gtimer_s();
-        if (tid == 0)  // (release: the state writes of every thread, ordered by the barrier, first)
-            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(done + hb) : "memory");
+        if (tid == 0) {
+            const int old = atomicAdd(glob + 1, 1);
+            if (old == (int)gridDim.x - 1) {  // last CTA of the launch: advance the epoch
+                glob[1] = 0;
+                __threadfence();
+                glob[0] = epoch1;
+            }
+        }
+    };
+    if ((int)blockIdx.x >= n_heads) {
+        if (steal) {
+            help();
+            leave();
+        }
         return;
     }
     // ---- phase 2: CTA bh owns head bh
     const int bh = blockIdx.x, b = bh / s.H, h = bh % s.H, hx = s.hix(b, layer, h);
-    const bool helped = kh > 0 && prefix[bh + 1] > prefix[bh];
+    const bool chunked = steal && prefix[bh + 1] > prefix[bh];
     const int n_pages = pages_of(b);
     if (is_due(bh) && n_pages > 0) {
         if (tid == 0) s.count(FC_STAT_SCORE_EVALS, 1);
@@ -1587,28 +1652,29 @@ score_attend_bal_kernel(StoreView s, int layer, const T *__restrict__ q, const u
         }
         __syncthreads();  // the selection is written; the keys are dead (the ring reuses them)
     }
-    if (helped && tid == 0)  // the selection is out (the barrier above orders every thread's writes
-        // before this release, which is cumulative): the helpers may attend
-        asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ready + bh), "r"(1) : "memory");
+    if (chunked && tid == 0) {
+        // the selection is out (the barrier above orders every thread's writes
+        // before this release, which is cumulative): chunks may be claimed
+        claim[bh] = 0;
+        done[bh] = 0;
+        asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ready + bh), "r"(epoch1) : "memory");
+    }
     if (satr && threadIdx.x == 0) satr[blockIdx.x * 8 + 6] = gtimer_s();
-    if (!helped) {
+    if (!chunked) {
         attend_head_cta<T, D, NST, NW>(s, a, bh, dsm, abars, s_wm, s_wl, nullptr, 1);
     } else {
-        float *st0 = a.bal_state + (int64_t)bh * kBalMaxSplit * GD;
-        const int n_att = attend_head_cta<T, D, NST, NW>(s, a, bh, dsm, abars, s_wm, s_wl, nullptr, 1, kh + 1, 0,
-                                                         st0);
-        if (tid == 0) {
-            int got;
-            while (true) {
-                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(got) : "l"(done + bh) : "memory");
-                if (got >= kh) break;
-                __nanosleep(32);
-            }
-            done[bh] = 0;   // self-resetting for the next launch (which waits for this one)
-            ready[bh] = 0;
+        while (true) {  // this head's chunks first
+            if (tid == 0) s_chunk = atomicAdd(claim + bh, 1);
+            __syncthreads();
+            const int c = s_chunk;
+            __syncthreads();
+            if (c >= NC) break;
+            run_chunk(bh, c);
         }
-        __syncthreads();
-        if (n_att > 0) merge_head_global<T, D>(s, a, bh, st0, kh + 1, blockDim.x);
+    }
+    if (steal) {
+        help();
+        leave();
     }
     if (satr && threadIdx.x == 0) satr[blockIdx.x * 8 + 7] = gtimer_s();
 }

@@ -45,8 +45,16 @@ def layers():
                                  kv_prefetch=l > 0, k_new=eng.k_new[l], v_new=eng.v_new[l])
 
 
+st.balanced_helpers = os.environ.get("BAL_WS") == "1"
 layers()
 torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(10):
+    layers()
+e1.record()
+torch.cuda.synchronize()
+print("us per layer", round(e0.elapsed_time(e1) * 1e3 / (10 * L), 2))
 sa = torch.zeros(grid * 8, dtype=torch.int64, device=dev)
 lib.fc_debug_sa_trace(sa.data_ptr())
 torch.cuda._sleep(10_000_000)

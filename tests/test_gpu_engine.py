@@ -263,14 +263,15 @@ def test_balanced_bitwise_equals_two_launch():
     for got, want in zip((st.sel, st.n_sel, st.summaries, eng.out, st.scores), ref):
         assert torch.equal(got, want)
     assert int(st.score_counters.abs().sum()) == 0  # left zero for the next launch
-    # the helper CTAs (the 20 CTAs beyond one per head split the scored heads'
-    # attention with their owners): the same selections and summaries; the
-    # outputs differ only by the order of the softmax merge
+    # chunked attention of the scored heads (their pages cut into chunks that
+    # the owner and any CTA with no work left claim; the last to finish a head
+    # merges): the same selections and summaries; the outputs differ only by
+    # the order of the softmax merge
     for t, v in zip((st.sel, st.n_sel, st.summaries, st.kv_pool), snap):
         t.copy_(v)
     st.balanced_helpers = True
     try:
-        for _ in range(2):  # twice: the flags reset themselves
+        for it in range(3):  # repeatedly: the launch epoch keeps earlier launches' words stale
             for t, v in zip((st.sel, st.n_sel, st.summaries, st.kv_pool), snap):
                 t.copy_(v)
             for l in range(L):
@@ -282,8 +283,8 @@ def test_balanced_bitwise_equals_two_launch():
                 assert torch.equal(got, want)
             err = (eng.out.float() - ref[3].float()).norm() / ref[3].float().norm()
             assert float(err) < 5e-3, float(err)
-            flags = st._bal_ws[:2 * B * H * 4].view(torch.int32)
-            assert int(flags.abs().sum()) == 0  # ready / done flags left zero for the next launch
+            glob = st._bal_ws[4 * B * H * 4:(4 * B * H + 2) * 4].view(torch.int32).tolist()
+            assert glob == [(it + 1) * L, 0]  # one epoch per launch, exit count back to zero
     finally:
         st.balanced_helpers = False
 
