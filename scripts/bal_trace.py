@@ -17,7 +17,7 @@ from paper_2511_00868_b200.engine import DecodeEngine  # noqa: E402
 from paper_2511_00868_b200.stability import HeadProfile  # noqa: E402
 from paper_2511_00868_b200.synthetic import device_normal  # noqa: E402
 
-B, L, H, G, D, T, K, R = 16, 4, 8, 4, 128, 32768, 128, 16
+B, L, H, G, D, T, K, R = 16, int(os.environ.get("TL", 4)), 8, 4, 128, 32768, 128, 16
 NU = int(os.environ.get("NU", 2))
 dev = torch.device("cuda", 0)
 prof = HeadProfile(model_id="x", n_layers=L, n_heads_per_layer=H, fraction=NU / H,
