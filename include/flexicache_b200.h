@@ -304,11 +304,13 @@ int fc_score_attend_balanced(const fc_store *s, int layer, const void *q,
                              const void *k_new, const void *v_new, void *out,
                              float *lse, float scale, int attend_appended,
                              int batch, void *stream);
-/* fc_score_attend_balanced whose CTAs beyond one per head help the scored
- * heads attend: up to 3 per scored head split its attended pages with the
- * owner CTA, which merges their states (same results up to the order of the
- * softmax merge).  helper_ws: fc_score_attend_balanced_workspace_size bytes,
- * zero before the first call, left zero (self-resetting); NULL = no helpers. */
+/* fc_score_attend_balanced with the scored heads' attention cut into chunks
+ * (FC_BAL_CHUNKS, 2..4, default 4) that the owner CTA and every CTA with no
+ * work left claim; the CTA finishing a head's last chunk merges the chunk
+ * states (same results up to the order of the softmax merge).  helper_ws:
+ * fc_score_attend_balanced_workspace_size bytes, zero before the first call
+ * and then kept for every later call of the same batch size (per-head words
+ * and a launch epoch the kernel advances itself); NULL = no chunking. */
 size_t fc_score_attend_balanced_workspace_size(const fc_store *s, int batch);
 int fc_score_attend_balanced_ws(const fc_store *s, int layer, const void *q,
                                 const uint8_t *unstable, int period, int force_due,
