@@ -569,7 +569,9 @@ FC_DEVINL void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" :
 template <typename T, int D, int NST, int NW>
 FC_DEVINL int attend_head_cta(const StoreView &s, const AttnArgs &a, int bh, char *ring, uint64_t *bars,
                               float (*s_wm)[16], float (*s_wl)[16], float *s_q, int bar_id, int S = 1,
-                              int rank = 0, float *cstate = nullptr) {
+                              int rank = 0, float *cstate = nullptr, int nst = NST) {
+    // nst <= NST: ring stages in use (fewer pages in flight lowers this
+    // CTA's share of a saturated HBM in favour of the launch's other CTAs)
     using Gm = AttnGeom<T, D>;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     constexpr int NT = NW * 32;
@@ -600,7 +602,7 @@ FC_DEVINL int attend_head_cta(const StoreView &s, const AttnArgs &a, int bh, cha
 #pragma unroll
     for (int i = 0; i < NST; ++i) {
         const int blk = __shfl_sync(0xffffffffu, cur_blk, i);
-        if (lane == 0 && i < n_e) {
+        if (lane == 0 && i < n_e && i < nst) {
             if (blk > 0) {
                 mbar_arrive_expect_tx(&mybars[i], Gm::kPageBytes);
                 bulk_g2s(myring + (size_t)i * Gm::kPageBytes, pool + (int64_t)blk * Gm::kPageBytes, Gm::kPageBytes,
@@ -627,6 +629,8 @@ FC_DEVINL int attend_head_cta(const StoreView &s, const AttnArgs &a, int bh, cha
         tp.load(s, reinterpret_cast<const T *>(a.k_new) + nk, reinterpret_cast<const T *>(a.v_new) + nk, hd.hx,
                 hd.n_pages - 1, tok_slot, lane);
     }
+    int stg = 0;
+    uint32_t ph = 0;
     for (int i = 0; i < n_e; ++i) {
         if (i > 0 && (i & 31) == 0) {
             cur_blk = nxt_blk;
@@ -635,12 +639,11 @@ FC_DEVINL int attend_head_cta(const StoreView &s, const AttnArgs &a, int bh, cha
             nxt_blk = (j < j0 + n_e) ? resolve_block(s, hd, entry_page(s, hd, j)) : 0;
         }
         const int blk = __shfl_sync(0xffffffffu, cur_blk, i & 31);
-        const int ni = i + NST;
+        const int ni = i + nst;
         const int nb_cur = __shfl_sync(0xffffffffu, cur_blk, ni & 31);
         const int nb_nxt = __shfl_sync(0xffffffffu, nxt_blk, ni & 31);
         const int nblk = (ni >> 5) == chunk ? nb_cur : nb_nxt;
-        const int stg = i % NST;
-        mbar_wait(&mybars[stg], (i / NST) & 1);
+        mbar_wait(&mybars[stg], ph);
         if (blk > 0) {
             char *stage = myring + (size_t)stg * Gm::kPageBytes;
             const bool last = (j0 + i == n_att - 1);
@@ -659,6 +662,10 @@ FC_DEVINL int attend_head_cta(const StoreView &s, const AttnArgs &a, int bh, cha
             } else {
                 mbar_arrive_expect_tx(&mybars[stg], 0);
             }
+        }
+        if (++stg == nst) {
+            stg = 0;
+            ph ^= 1u;
         }
     }
     st.finalize();

@@ -285,6 +285,12 @@ int fc_score_attend_balanced_ws(const fc_store *s, int layer, const void *q, con
     a.layer = layer; a.q = q; a.k_new = k_new; a.v_new = v_new; a.out = out; a.lse = lse;
     a.scale_log2 = scale * 1.4426950408889634f;
     a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.max_splits = 1;
+    {
+        // ring stages of the heads that are not scored: one fewer than the
+        // scored heads' (-1); FC_BAL_NST overrides (0: all stages; tuning knob)
+        static const int nst = std::getenv("FC_BAL_NST") ? std::atoi(std::getenv("FC_BAL_NST")) : -1;
+        a.bal_nst = nst;
+    }
     if (helper_ws) {  // chunked attention of the scored heads (zero-initialised workspace)
         a.bal_flags = reinterpret_cast<int32_t *>(helper_ws);
         a.bal_state = reinterpret_cast<float *>(reinterpret_cast<char *>(helper_ws) +

@@ -40,6 +40,7 @@ struct AttnArgs {
     // epoch and exit count, and the chunk states [batch*H][kBalMaxSplit][G*D + 32]
     int32_t *bal_flags;
     float *bal_state;
+    int bal_nst;          // balanced launch: ring stages of the heads that are not scored (-1: NST - 1, 0: all)
     int bal_wait;         // balanced launch: CTAs with no work wait for selections still pending
     int compact_select;   // fc_score_attend: rolled-loop select (block_select_compact)
 };

@@ -1661,7 +1661,15 @@ score_attend_bal_kernel(StoreView s, int layer, const T *__restrict__ q, const u
     }
     if (satr && threadIdx.x == 0) satr[blockIdx.x * 8 + 6] = gtimer_s();
     if (!chunked) {
-        attend_head_cta<T, D, NST, NW>(s, a, bh, dsm, abars, s_wm, s_wl, nullptr, 1);
+        // a head that is not scored streams through fewer stages (a.bal_nst;
+        // default one fewer): with fewer of its pages in flight it takes a
+        // smaller share of the saturated HBM, and the scored heads, which
+        // start their attention ~8 us later, a larger one (config 2: spread
+        // mask 12.80k -> 12.94k, staggered phases 12.23k -> 12.51k tokens/s;
+        // one stage: slower)
+        const int want = a.bal_nst < 0 ? NST - 1 : a.bal_nst;
+        const int nst = (want > 0 && want < NST && !is_due(bh)) ? want : NST;
+        attend_head_cta<T, D, NST, NW>(s, a, bh, dsm, abars, s_wm, s_wl, nullptr, 1, 1, 0, nullptr, nst);
     } else {
         while (true) {  // this head's chunks first
             if (tid == 0) s_chunk = atomicAdd(claim + bh, 1);
