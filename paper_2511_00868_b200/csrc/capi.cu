@@ -186,6 +186,13 @@ int fc_score_select(const fc_store *s, int layer, const void *q, const uint8_t *
                                     (cudaStream_t)stream));
 }
 
+// ring stages of the heads a scoring launch does not score: one fewer than
+// the scored heads' (-1); FC_BAL_NST overrides (0: all stages; tuning knob)
+static int unscored_nst() {
+    static const int nst = std::getenv("FC_BAL_NST") ? std::atoi(std::getenv("FC_BAL_NST")) : -1;
+    return nst;
+}
+
 int fc_score_attend_supported(const fc_store *s, int batch) {
     if (check_store(s) != FC_OK || batch < 1 || batch > s->batch_cap || s->pages_cap > kMaxPagesCap) return 0;
     return score_attend_supported(make_view(s), s->dtype, batch);
@@ -216,7 +223,7 @@ int fc_score_attend(const fc_store *s, int layer, const void *q, const uint8_t *
     AttnArgs a = {};
     a.layer = layer; a.q = q; a.k_new = k_new; a.v_new = v_new; a.out = out; a.lse = lse;
     a.scale_log2 = scale * 1.4426950408889634f;
-    a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.max_splits = 1;
+    a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.max_splits = 1; a.bal_nst = unscored_nst();
     return cuda_status(launch_score_attend(v, s->dtype, layer, q, unstable, period, force_due, topk, extra_tokens,
                                            scores_out, batch, kv_prefetch ? 1 : 0, a, (cudaStream_t)stream));
 }
@@ -285,12 +292,7 @@ int fc_score_attend_balanced_ws(const fc_store *s, int layer, const void *q, con
     a.layer = layer; a.q = q; a.k_new = k_new; a.v_new = v_new; a.out = out; a.lse = lse;
     a.scale_log2 = scale * 1.4426950408889634f;
     a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.max_splits = 1;
-    {
-        // ring stages of the heads that are not scored: one fewer than the
-        // scored heads' (-1); FC_BAL_NST overrides (0: all stages; tuning knob)
-        static const int nst = std::getenv("FC_BAL_NST") ? std::atoi(std::getenv("FC_BAL_NST")) : -1;
-        a.bal_nst = nst;
-    }
+    a.bal_nst = unscored_nst();
     if (helper_ws) {  // chunked attention of the scored heads (zero-initialised workspace)
         a.bal_flags = reinterpret_cast<int32_t *>(helper_ws);
         a.bal_state = reinterpret_cast<float *>(reinterpret_cast<char *>(helper_ws) +
@@ -337,7 +339,7 @@ int fc_score_attend_map(const fc_store *s, int layer, const void *q, const uint8
     AttnArgs a = {};
     a.layer = layer; a.q = q; a.k_new = k_new; a.v_new = v_new; a.out = out; a.lse = lse;
     a.scale_log2 = scale * 1.4426950408889634f;
-    a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.max_splits = 1;
+    a.extra_tokens = extra_tokens; a.attend_appended = attend_appended; a.max_splits = 1; a.bal_nst = unscored_nst();
     a.cta_map = cta_map; a.map_heads = batch * s->kv_heads;
     return cuda_status(launch_score_attend_map(v, s->dtype, layer, q, unstable, period, force_due, topk,
                                                extra_tokens, scores_out, kv_prefetch ? 1 : 0, a, n_ctas, cluster,

@@ -1084,6 +1084,17 @@ score_head_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8_t
                           dsm, full, empty, s_rel, w);
 }
 
+// Ring stages of a head in a scoring launch: a head that is not scored
+// (score_head_stream status != 2) streams through one stage fewer (a.bal_nst
+// < 0, the default; 0: all stages), so the heads that score and select first
+// take a larger share of the saturated HBM for their attention.
+template <int NST>
+FC_DEVINL int unscored_stages(const AttnArgs &a, int st) {
+    if (st == 2 || a.bal_nst == 0) return NST;
+    const int want = a.bal_nst < 0 ? NST - 1 : a.bal_nst;
+    return want > 0 && want < NST ? want : NST;
+}
+
 // Fused scoring + attention of one head per CTA (layers whose heads are
 // scored this step): the selection never leaves the CTA's view before its
 // pages stream — no grid-wide wait between scoring and attention, no second
@@ -1263,7 +1274,8 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
     float *cstate = reinterpret_cast<float *>(dsm) + (size_t)NWA * s.G * D;
     if constexpr (!CL) {
         if (satr && threadIdx.x == 0) satr[blockIdx.x * 4 + 1] = gtimer_s();
-        attend_head_cta<T, D, NST, NWA>(s, a, bh, dsm, abars, s_wm, s_wl, s_q, 1);
+        attend_head_cta<T, D, NST, NWA>(s, a, bh, dsm, abars, s_wm, s_wl, s_q, 1, 1, 0, nullptr,
+                                        unscored_stages<NST>(a, st));
         if (satr && threadIdx.x == 0) satr[blockIdx.x * 4 + 2] = gtimer_s();
         if (a.pf_cap > 0 && threadIdx.x < 32) {
             // the heads not due share the prefetch: this one's ordinal among
@@ -1297,7 +1309,7 @@ score_attend_kernel(StoreView s, int layer, const T *__restrict__ q, const uint8
         // (only attending warps get here when NWS > NWA)
         if (satr && threadIdx.x == 0) satr[blockIdx.x * 4 + 1] = gtimer_s();
         const int n_att = attend_head_cta<T, D, NST, NWA>(s, a, bh, dsm, abars, s_wm, s_wl, s_q, 1, Sh, rank,
-                                                          Sh > 1 ? cstate : nullptr);
+                                                          Sh > 1 ? cstate : nullptr, unscored_stages<NST>(a, st));
         if (satr && threadIdx.x == 0) satr[blockIdx.x * 4 + 2] = gtimer_s();
         // every rank's state written
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
