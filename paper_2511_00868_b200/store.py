@@ -93,11 +93,10 @@ class KVStore:
         self._c_flat.row_phase = None
         self._c_flat.row_hold = None
         self.per_row = False
-        # fc_score_attend_balanced: the CTAs beyond one per head help the
-        # scored heads attend (partial steps: a row at its rerank).  Off by
-        # default (FC_BAL_HELPERS=1: on): measured slower at config 2 even
-        # with the compact owner select (staggered 11.7k vs 12.0k tokens/s;
-        # DESIGN.md §4)
+        # fc_score_attend_balanced_ws: the scored heads' attention cut into
+        # chunks that idle CTAs claim (FC_BAL_CHUNKS per head).  Off by
+        # default (FC_BAL_HELPERS=1: on): measured slower at config 2 with
+        # the spread mask (9.6k vs 12.8k tokens/s)
         self.balanced_helpers = os.environ.get("FC_BAL_HELPERS", "0") == "1"
         # the same store without the counters: selections that are not
         # scheduled score evaluations (initial selection, reload prediction)
